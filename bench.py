@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""VeST CD-sweep benchmark (BASELINE.json metric: observed-nnz*iter/s).
+
+Workload (BASELINE.json configs[1], "config 2"): 3-mode 100k x 100k x 100k,
+10M observed entries at uniform-random distinct coordinates, fp64 values
+U[0,1), Tucker ranks 10x10x10, lambda = 0.01 (LF), init_random(seed) factors.
+A step = one CD iteration as fit() runs it (trainer.hpp:121-127):
+update_all_factors + update_core + residuals/RE, over all 10M entries.
+Prune events (responsibilities + prune) are timed separately ("prune_event").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+ours:       device-resident steps, CUDA events on the library stream ("value");
+            the same steps through the C-ABI with host model buffers, H2D+D2H
+            inside the timed region ("e2e"); kernel-family times for the
+            roofline; the reference CPU path timed on a bounded sample
+            ("cpu_baseline").
+reference:  the reference's own CPU implementation (oracle/_ref: the
+            unmodified reference headers; the C port when _ref is absent) on a
+            bounded sample of the same workload, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CD sweep observed-nnz*iter/s"
+UNIT = "nnz*iter/s"
+CONFIG2 = dict(dims=[100_000] * 3, nnz=10_000_000, ranks=[10, 10, 10], lam=0.01, reg=0, seed=2,
+               data_seed=20261020, values_kind=0)
+SAMPLE_NNZ = 300_000  # CPU reference sample (same shape/distribution, fewer entries)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def synth(dims, nnz, seed, values_kind=0, zipf=None):
+    from paper_1904_02603_b200 import _lib
+    L = _lib.lib()
+    d = np.asarray(dims, np.uint64)
+    z = np.asarray(zipf if zipf else [0.0] * len(dims), np.float64)
+    coords = np.empty(nnz * len(dims), np.uint32)
+    vals = np.empty(nnz, np.float64)
+    _lib.check(L.vest_synth(len(dims), _lib.ptr(d, _lib.u64p), nnz, _lib.ptr(z, _lib.f64p), values_kind, seed,
+                            _lib.ptr(coords, _lib.u32p), _lib.ptr(vals, _lib.f64p)))
+    return coords.reshape(nnz, len(dims)), vals
+
+
+# --------------------------------------------------------------- algorithmic --
+def contraction_fmas(ranks, n):
+    """FMA count per entry of the factorised delta contraction for mode n, as
+    the static kernel executes it (vest_common.cuh delta_static):
+    T(k) = J_k (T(k+1) + 1) for k < N-1, T(N-1) = J_{N-1}, T(N) = 0;
+    n == 0: J_1 J_0 (T(2) + 1);  n > 0: J_0 P(1) with P(k) = J_k (1 + P(k+1))
+    for k < n and P(n) = J_n (T(n+1) + 1)."""
+    N = len(ranks)
+
+    def T(k):
+        if k >= N:
+            return 0
+        if k == N - 1:
+            return ranks[k]
+        return ranks[k] * (T(k + 1) + 1)
+
+    def P(k):
+        if k == n:
+            return ranks[n] * (T(n + 1) + 1)
+        return ranks[k] * (1 + P(k + 1))
+
+    if n == 0:
+        return ranks[1] * ranks[0] * (T(2) + 1)
+    return ranks[0] * P(1)
+
+
+def factor_launch_model(ranks, nnz):
+    """(flops, bytes) per launch of the dominant kernel: the factor-row update
+    of one mode (k_rowpass<kStats>), averaged over the modes."""
+    N = len(ranks)
+    fl, by = 0, 0
+    for n in range(N):
+        J = ranks[n]
+        fl += 2 * nnz * (contraction_fmas(ranks, n) + J * (J + 1) // 2 + J)
+        by += nnz * ((N - 1) * 4 + 8)  # compulsory: other coords + value per entry
+    return fl / N, by / N
+
+
+# ------------------------------------------------------------------ clocks --
+class Clocks:
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------- CPU baseline leg --
+def cpu_reference_rate(steps=1, nnz=SAMPLE_NNZ, threads=None):
+    """The reference CPU path (oracle/_ref when built, else the C port) on a
+    bounded sample of config 2: same dims/ranks/lambda/value distribution,
+    `nnz` entries.  Returns (rate nnz*iter/s, kind, threads, seconds/iter)."""
+    from oracle import oracle as O  # test/baseline infrastructure only
+    kind = "reference" if O.available("reference") else "port"
+    threads = threads or os.cpu_count() or 1
+    cfg = CONFIG2
+    coords, vals = synth(cfg["dims"], nnz, cfg["data_seed"] + 1)
+    s = O.Session(cfg["dims"], coords, vals, cfg["ranks"], kind)
+    s.init_random(cfg["seed"])
+    s.cd_iteration(cfg["reg"], cfg["lam"], threads)  # warm-up (first-touch, page-in)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.cd_iteration(cfg["reg"], cfg["lam"], threads)
+    dt = (time.perf_counter() - t0) / steps
+    return nnz / dt, kind, threads, dt
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+    kind = "reference" if O.available("reference") else "port"
+    cfg = CONFIG2
+    coords, vals = synth(cfg["dims"], SAMPLE_NNZ, cfg["data_seed"] + 1)
+    s = O.Session(cfg["dims"], coords, vals, cfg["ranks"], kind)
+    s.init_random(cfg["seed"])
+    for _ in range(args.warmup):
+        s.cd_iteration(cfg["reg"], cfg["lam"], threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s.cd_iteration(cfg["reg"], cfg["lam"], threads)
+    dt = time.perf_counter() - t0
+    value = SAMPLE_NNZ * args.steps / dt
+    sample = f"config2 shape (100k^3, R=10, lambda=0.01, U[0,1)) with {SAMPLE_NNZ} entries per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(n):
+    return {"workload": "config2: 3-mode 100k^3, 10M uniform distinct entries, fp64 U[0,1), ranks 10x10x10, "
+                        "lambda 0.01 LF; step = update_all_factors + update_core + RE",
+            "nnz": CONFIG2["nnz"], "ranks": CONFIG2["ranks"], "dims": CONFIG2["dims"],
+            "parallelism": f"replicas x{n}" if n > 1 else "single",
+            "l2": "inputs larger than L2 (per-mode CSF 600 MB vs 126 MB L2)"}
+
+
+# --------------------------------------------------------------- our arm ------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_1904_02603_b200 import _lib
+    from paper_1904_02603_b200 import sparsetuck as st
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    L = _lib.lib()
+    cfg = CONFIG2
+    coords, vals = synth(cfg["dims"], cfg["nnz"], cfg["data_seed"])
+    x = st.SparseTensor(cfg["dims"], coords, vals)
+    dev = st.Device(x, cfg["ranks"], local_rank)
+    assert dev.specialised(), "rank-specialised kernels expected for config 2"
+    dev.init_random(cfg["seed"])
+    stream = torch.cuda.ExternalStream(dev.stream(), device=torch.device("cuda", local_rank))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        dev.cd_iteration(cfg["reg"], cfg["lam"])
+    # ---- device-resident timed region
+    L.vest_ctx_profile(dev.h, 1)
+    ms_arr = np.zeros(8)
+    n_arr = np.zeros(8, np.uint64)
+    L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = L.vest_launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        ev0.record(stream)
+        res = []
+        for _ in range(args.steps):
+            res.append(dev.cd_iteration(cfg["reg"], cfg["lam"]))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = L.vest_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
+    L.vest_ctx_profile(dev.h, 0)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cfg["nnz"] * args.steps * world / (ms * 1e-3)
+
+    # ---- prune event (timed separately; not an iteration)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dev.compute_responsibilities(want=False)
+    counts = dev.prune_step(0.3)
+    prune_ms = (time.perf_counter() - t0) * 1e3
+
+    # ---- e2e through the C-ABI with host buffers
+    m_host = dev.get_model()
+    pinned = []
+
+    def pin(a):
+        t = torch.empty(a.shape, dtype={np.float64: torch.float64, np.uint8: torch.uint8}[a.dtype.type],
+                        pin_memory=True)
+        t.numpy()[...] = a
+        pinned.append(t)
+        return t.numpy()
+
+    m_host = st.TuckerModel(m_host.dims, m_host.ranks, pin(m_host.core), pin(m_host.core_mask),
+                            [pin(f) for f in m_host.factors], [pin(k) for k in m_host.factor_masks])
+    h2d = m_host.core.nbytes + m_host.core_mask.nbytes + sum(f.nbytes + k.nbytes for f, k in
+                                                              zip(m_host.factors, m_host.factor_masks))
+    d2h = h2d + 8
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dev.set_model(m_host)
+        dev.cd_iteration(cfg["reg"], cfg["lam"])
+        dev.get_model(into=m_host)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = cfg["nnz"] * e2e_steps * world / e2e_s
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel family (factor-row update)
+    peak = C.c_double()
+    L.vest_measure_fp64_peak(local_rank, C.byref(peak))
+    fam_names = ["factor_update", "core_pass", "core_gemm", "core_solve", "residual", "resp", "prune"]
+    fams = {fam_names[i]: {"ms": float(ms_arr[i]), "scopes": int(n_arr[i])} for i in range(7)}
+    fl, by = factor_launch_model(cfg["ranks"], cfg["nnz"])
+    nf = max(int(n_arr[0]), 1)
+    avg_ms = ms_arr[0] / nf
+    achieved_tf = fl / (avg_ms * 1e-3) / 1e12
+    achieved_gbs = by / (avg_ms * 1e-3) / 1e9
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_factor_update.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "fp64", "kernel": "k_rowpass<StaticPolicy<10,10,10>,kStats> (factor-row update, per mode)",
+        "achieved": achieved_tf, "peak": peak.value, "unit": "TFLOP/s", "frac": achieved_tf / peak.value,
+        "peak_source": "measured live: vest_measure_fp64_peak (DFMA microbenchmark)",
+        "traffic": traffic, "flops_per_launch": fl, "avg_launch_ms": avg_ms,
+        "hbm": {"achieved": achieved_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": achieved_gbs / peaks.get("hbm_gbs", 6650.0), "bytes_per_launch": by,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "step_share": float(ms_arr[0] / ms) if ms > 0 else None,
+    }
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        rate, kind, thr, sec = cpu_reference_rate()
+        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": kind,
+               "sample": f"one CD iteration of config2 shape with {SAMPLE_NNZ} entries ({sec:.1f} s)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config 2 shape)",
+        "config": workload_config(world),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "steps": e2e_steps, "path": "vest_set_model + vest_cd_iteration + vest_get_model (pinned host)"},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "kernel_families_ms": fams,
+        "prune_event": {"ms": prune_ms, "rate": 0.3, "counts": [counts.core] + counts.factors},
+        "re_trace": res,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

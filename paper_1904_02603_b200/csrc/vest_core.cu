@@ -1,0 +1,639 @@
+// SPDX-License-Identifier: Apache-2.0
+// vest_core.cu -- the core update (updates.hpp:177-262) and the core
+// responsibilities (pruning.hpp:93-134).
+//
+// Exact Gauss-Seidel over the core cells in row-major order, blocked by
+// FIBERS along the last mode m = N-1 (a fiber = the J_m consecutive cells that
+// share the prefix beta_0..beta_{m-1}).  For a block of F fibers, with
+//   s_ef = prod_{k<m} A_k[i_k, beta_k(f)]    (per entry)
+//   p_e(f,c) = s_ef * A_m[i_m, c]
+// every block statistic factorises over the slices i_m of the last mode:
+//   c_(f,c)            = sum_e r_e p_e(f,c)  = sum_slices A_m[s,c]       * R^s_f
+//   H_(f,c),(f',c')    = sum_e p p           = sum_slices A_m[s,c]A_m[s,c'] * S^s_ff'
+// with R^s_f = sum_{e in s} s_ef r_e and S^s_ff' = sum_{e in s} s_ef s_ef'.
+// One pass over the entries (k_core_pass) produces (S, R) per slice chunk,
+// a small GEMM over the slices (k_core_gemm + k_colsum) produces (T, C), and one
+// warp solves the block's cells sequentially (k_core_solve):
+//   num_q = c_q - sum_{q' < q} dg_q' H_q'q + g_old H_qq ,  den_q = H_qq
+// which is exactly the reference's num/den (updates.hpp:211-217) for the
+// state after the earlier cells' updates; only the summation order differs.
+// The next pass applies r -= sum dg p for the finished block before it
+// accumulates the next block, and a final pass applies the last block and sums
+// r^2 (the residual/RE of compute_residuals, tucker_model.hpp:168-183).
+#include <algorithm>
+#include <vector>
+
+#include "vest_common.cuh"
+
+namespace vest {
+
+constexpr int kFMax = 10;  // fibers per block, register-accumulated pass
+constexpr int kPassWarps = 8;
+
+struct CorePassArgs {
+  DevModel m;
+  DevCSF csf;  // mode N-1
+  double* r;
+  // block fibers: prefix lin index over modes 0..m-1
+  const uint32_t* prev_fib;
+  int prev_nf;
+  const double* prev_dg;  // [prev_nf][Jm]
+  const uint32_t* cur_fib;
+  int cur_nf;
+  int kind;  // 0 sweep (S, R), 1 responsibility (R, D), 2 final (apply prev, sum r^2)
+  double* stats;
+  int stride;
+  double* chunk_sq;
+};
+
+template <int B, int E, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    sfor<B + 1, E>(f);
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void treduce(double (&v)[V], int lane) {
+  sfor<0, 5>([&](auto sc) {
+    constexpr int s = decltype(sc)::value;
+    constexpr int H = (V >> s) / 2;
+    constexpr int off = 16 >> s;
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double keep = up ? v[i + H] : v[i];
+      const double send = up ? v[i] : v[i + H];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  });
+}
+
+// One warp per chunk of a last-mode slice.  Per entry: the fiber products
+// s_f (from factor rows staged in shared memory), the previous block's residual
+// update, and the register accumulation of S (upper triangle) and R.
+template <int M>
+__global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
+  extern __shared__ double smem[];
+  __shared__ int sb[2][kFMax][M > 0 ? M : 1];  // beta of each fiber (prev, cur)
+  __shared__ double sdg[kFMax * VEST_MAXJ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Jm = a.m.J[M];
+  // fiber beta tables (decoded from the packed cell index of cell c = 0)
+  for (int t = threadIdx.x; t < 2 * kFMax * M; t += blockDim.x) {
+    const int which = t / (kFMax * M), rest = t % (kFMax * M), f = rest / M, k = rest % M;
+    const uint32_t* fl = which ? a.cur_fib : a.prev_fib;
+    const int nf = which ? a.cur_nf : a.prev_nf;
+    int b = 0;
+    if (f < nf) b = (a.m.cellbeta[fl[f] * Jm] >> (4 * k)) & 15u;
+    sb[which][f][k] = b;
+  }
+  for (int t = threadIdx.x; t < kFMax * Jm; t += blockDim.x)
+    sdg[t] = (a.prev_nf > 0 && t < a.prev_nf * Jm) ? a.prev_dg[t] : 0.0;
+  __syncthreads();
+  const uint32_t ci = blockIdx.x * kPassWarps + warp;
+  if (ci >= a.csf.nchunks) return;
+  const Chunk ch = a.csf.chunks[ci];
+
+  // stage layout: offs[k] + b rows of 32 lanes
+  int offs[M > 0 ? M : 1];
+  int tot = 0;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    offs[k] = tot;
+    tot += a.m.J[k];
+  }
+  double* st = smem + (size_t)warp * tot * 32;
+
+  // q_f = sum_c A_m[s, c] dg_prev[f][c]
+  const double* arow = a.m.factor[M] + (size_t)ch.row * a.m.ld[M];
+  double q[kFMax];
+#pragma unroll
+  for (int f = 0; f < kFMax; ++f) {
+    double t = 0.0;
+    if (f < a.prev_nf)
+      for (int c = 0; c < Jm; ++c) t = fma(__ldg(arow + c), sdg[f * Jm + c], t);
+    q[f] = t;
+  }
+
+  constexpr int NA = kFMax * (kFMax + 1) / 2 + kFMax;  // 65
+  constexpr int V = (NA + 31) / 32 * 32;              // 96
+  double acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.0;
+  double sq = 0.0;
+  const int nf = a.cur_nf;
+
+  for (uint32_t base = ch.beg; base < ch.end; base += 32) {
+    const uint32_t pos = base + lane;
+    const bool valid = pos < ch.end;
+    double r = 0.0;
+    if (valid) {
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const uint32_t i = __ldg(a.csf.oc[k] + pos);
+        const double* row = a.m.factor[k] + (size_t)i * a.m.ld[k];
+        for (int b = 0; b < a.m.J[k]; ++b) st[(offs[k] + b) * 32 + lane] = __ldg(row + b);
+      }
+      r = a.r[pos];
+    }
+    __syncwarp();
+    if (valid) {
+      if (a.prev_nf > 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int f = 0; f < kFMax; ++f) {
+          if (f < a.prev_nf) {
+            double s = 1.0;
+#pragma unroll
+            for (int k = 0; k < M; ++k) s *= st[(offs[k] + sb[0][f][k]) * 32 + lane];
+            t = fma(s, q[f], t);
+          }
+        }
+        r -= t;
+        if (a.kind != 1) a.r[pos] = r;
+      }
+      if (a.kind == 2) {
+        sq = fma(r, r, sq);
+      } else if (nf > 0) {
+        double s[kFMax];
+#pragma unroll
+        for (int f = 0; f < kFMax; ++f) {
+          double v = 0.0;
+          if (f < nf) {
+            v = 1.0;
+#pragma unroll
+            for (int k = 0; k < M; ++k) v *= st[(offs[k] + sb[1][f][k]) * 32 + lane];
+          }
+          s[f] = v;
+        }
+        if (a.kind == 0) {
+          int i = 0;
+#pragma unroll
+          for (int f = 0; f < kFMax; ++f)
+#pragma unroll
+            for (int g = f; g < kFMax; ++g) {
+              acc[i] = fma(s[f], s[g], acc[i]);
+              ++i;
+            }
+#pragma unroll
+          for (int f = 0; f < kFMax; ++f) {
+            acc[i] = fma(s[f], r, acc[i]);
+            ++i;
+          }
+        } else {
+#pragma unroll
+          for (int f = 0; f < kFMax; ++f) {
+            acc[f] = fma(s[f], r, acc[f]);
+            acc[kFMax + f] = fma(s[f], s[f], acc[kFMax + f]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  if (a.kind == 2) {
+    sq = warp_sum(sq);
+    if (lane == 0) a.chunk_sq[ci] = sq;
+    return;
+  }
+  treduce<V>(acc, lane);
+  constexpr int per = V / 32;
+  // compact: the kernel accumulates the kFMax layout; the stats row stores the
+  // nf layout (S upper triangle over nf fibers, then R) or (R, D)
+  double* out = a.stats + (size_t)ci * a.stride;
+#pragma unroll
+  for (int w = 0; w < per; ++w) {
+    const int idx = lane * per + w;
+    if (a.kind == 0) {
+      if (idx < kFMax * (kFMax + 1) / 2) {
+        int f = 0, rem = idx;
+        while (rem >= kFMax - f) {
+          rem -= kFMax - f;
+          ++f;
+        }
+        const int g = f + rem;
+        if (g < nf) out[f * nf - f * (f - 1) / 2 + (g - f)] = acc[w];
+      } else if (idx < NA) {
+        const int f = idx - kFMax * (kFMax + 1) / 2;
+        if (f < nf) out[nf * (nf + 1) / 2 + f] = acc[w];
+      }
+    } else if (idx < 2 * kFMax) {
+      const int f = idx % kFMax;
+      if (f < nf) out[(idx / kFMax) * nf + f] = acc[w];
+    }
+  }
+}
+
+// T[pS][pA] = sum_chunks S[pS] * (a_c a_c')[pA], C[f][c] = sum R[f] a_c
+// (kind 0), or C = sum R a_c, D = sum D a_c^2 (kind 1).  Each CTA covers a
+// contiguous range of chunks and writes its partial sums; k_colsum adds the
+// partials in CTA order (deterministic).
+struct CoreGemmArgs {
+  const double* stats;
+  int stride;
+  const Chunk* chunks;
+  uint32_t nchunks;
+  const double* A;  // factor of the last mode
+  int ld, Jm, nf, kind;
+  int NS, NAm, nT, nout;
+  double* partial;
+};
+
+constexpr int kGemmThreads = 256;
+constexpr int kGemmBatch = 16;
+constexpr int kTileMax = 2;  // 4x4 tiles per thread
+
+__global__ void __launch_bounds__(kGemmThreads) k_core_gemm(CoreGemmArgs a) {
+  extern __shared__ double sm[];
+  const int NSp = (a.NS + 3) & ~3, NAp = (a.NAm + 3) & ~3;
+  double* sS = sm;                                  // [batch][NSp]
+  double* sA = sS + kGemmBatch * NSp;               // [batch][NAp]
+  double* sR = sA + kGemmBatch * NAp;               // [batch][nf] (R) and [batch][nf] (D)
+  double* sa = sR + kGemmBatch * 2 * kFMax;         // [batch][Jm]
+  const uint32_t per = (a.nchunks + gridDim.x - 1) / gridDim.x;
+  const uint32_t c0 = blockIdx.x * per;
+  const uint32_t c1 = min(a.nchunks, c0 + per);
+  const int tilesS = NSp / 4, tilesA = NAp / 4;
+  const int ntiles = a.kind == 0 ? tilesS * tilesA : 0;
+  double acc[kTileMax][16];
+#pragma unroll
+  for (int k = 0; k < kTileMax; ++k)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[k][i] = 0.0;
+  double accC = 0.0, accD = 0.0;
+  const int nfj = a.nf * a.Jm;
+  for (uint32_t cb = c0; cb < c1; cb += kGemmBatch) {
+    const int nb = min((uint32_t)kGemmBatch, c1 - cb);
+    __syncthreads();
+    // stage the batch
+    for (int t = threadIdx.x; t < kGemmBatch * NSp; t += blockDim.x) {
+      const int b = t / NSp, p = t % NSp;
+      double v = 0.0;
+      if (b < nb && a.kind == 0 && p < a.NS) v = a.stats[(size_t)(cb + b) * a.stride + p];
+      sS[t] = v;
+    }
+    for (int t = threadIdx.x; t < kGemmBatch * 2 * kFMax; t += blockDim.x) {
+      const int b = t / (2 * kFMax), p = t % (2 * kFMax);
+      double v = 0.0;
+      if (b < nb) {
+        if (a.kind == 0) {
+          if (p < a.nf) v = a.stats[(size_t)(cb + b) * a.stride + a.NS + p];
+        } else if (p < 2 * a.nf) {
+          v = a.stats[(size_t)(cb + b) * a.stride + p];
+        }
+      }
+      sR[t] = v;
+    }
+    for (int t = threadIdx.x; t < kGemmBatch * a.Jm; t += blockDim.x) {
+      const int b = t / a.Jm, c = t % a.Jm;
+      sa[t] = b < nb ? __ldg(a.A + (size_t)a.chunks[cb + b].row * a.ld + c) : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kGemmBatch * NAp; t += blockDim.x) {
+      const int b = t / NAp, p = t % NAp;
+      double v = 0.0;
+      if (p < a.NAm) {
+        int c = 0, rem = p;
+        while (rem >= a.Jm - c) {
+          rem -= a.Jm - c;
+          ++c;
+        }
+        v = sa[b * a.Jm + c] * sa[b * a.Jm + c + rem];
+      }
+      sA[t] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTileMax; ++k) {
+      const int tile = threadIdx.x + k * blockDim.x;
+      if (tile < ntiles) {
+        const int ts = tile / tilesA, ta = tile % tilesA;
+        for (int b = 0; b < kGemmBatch; ++b) {
+          const double4 sv = *reinterpret_cast<const double4*>(sS + b * NSp + 4 * ts);
+          const double4 av = *reinterpret_cast<const double4*>(sA + b * NAp + 4 * ta);
+          const double s4[4] = {sv.x, sv.y, sv.z, sv.w};
+          const double a4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[k][i * 4 + j] = fma(s4[i], a4[j], acc[k][i * 4 + j]);
+        }
+      }
+    }
+    if (threadIdx.x < nfj) {
+      const int f = threadIdx.x / a.Jm, c = threadIdx.x % a.Jm;
+      for (int b = 0; b < kGemmBatch; ++b) {
+        const double av = sa[b * a.Jm + c];
+        if (a.kind == 0) {
+          accC = fma(sR[b * 2 * kFMax + f], av, accC);
+        } else {
+          accC = fma(sR[b * 2 * kFMax + f], av, accC);
+          accD = fma(sR[b * 2 * kFMax + a.nf + f], av * av, accD);
+        }
+      }
+    }
+  }
+  double* out = a.partial + (size_t)blockIdx.x * a.nout;
+#pragma unroll
+  for (int k = 0; k < kTileMax; ++k) {
+    const int tile = threadIdx.x + k * blockDim.x;
+    if (tile < ntiles) {
+      const int ts = tile / tilesA, ta = tile % tilesA;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ps = 4 * ts + i, pa = 4 * ta + j;
+          if (ps < a.NS && pa < a.NAm) out[ps * a.NAm + pa] = acc[k][i * 4 + j];
+        }
+    }
+  }
+  if (threadIdx.x < nfj) {
+    out[a.nT + threadIdx.x] = accC;
+    if (a.kind == 1) out[a.nT + nfj + threadIdx.x] = accD;
+  }
+}
+
+__global__ void k_colsum(const double* partial, int nparts, int n, double* out) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  double s = 0.0;
+  for (int p = 0; p < nparts; ++p) s += partial[(size_t)p * n + o];
+  out[o] = s;
+}
+
+__device__ __forceinline__ int tri(int i, int j, int n) {  // i <= j
+  return i * n - i * (i - 1) / 2 + (j - i);
+}
+
+// Sequential Gauss-Seidel over the block's cells (one warp).  tc = [T | C].
+__global__ void k_core_solve(const double* tc, int nf, int Jm, const uint32_t* fib, double* core,
+                             const uint8_t* core_mask, int reg, double lambda, double* dg_out) {
+  __shared__ double cc[kFMax * VEST_MAXJ];
+  const int lane = threadIdx.x;
+  const int NAm = Jm * (Jm + 1) / 2;
+  const int nT = nf * (nf + 1) / 2 * NAm;
+  const int nq = nf * Jm;
+  for (int q = lane; q < nq; q += 32) cc[q] = tc[nT + q];
+  __syncwarp();
+  for (int q = 0; q < nq; ++q) {
+    const int f = q / Jm, c = q % Jm;
+    const int lin = (int)fib[f] * Jm + c;
+    double dg = 0.0;
+    if (!core_mask[lin]) {
+      const double hqq = tc[tri(f, f, nf) * NAm + tri(c, c, Jm)];
+      const double g_old = core[lin];
+      const double num = cc[q] + g_old * hqq;
+      const double den = hqq;
+      double g_new = g_old;
+      if (reg == 0) {
+        if (den + lambda != 0.0) g_new = num / (den + lambda);
+      } else {
+        const double g = -2.0 * num;
+        const double d = 2.0 * den;
+        if (d != 0.0) g_new = g > lambda ? (lambda - g) / d : (g < -lambda ? -(lambda + g) / d : 0.0);
+      }
+      if (g_new != g_old) {
+        dg = g_new - g_old;
+        if (lane == 0) core[lin] = g_new;
+      }
+    }
+    if (lane == 0) dg_out[q] = dg;
+    if (dg != 0.0) {
+      for (int q2 = q + 1 + lane; q2 < nq; q2 += 32) {
+        const int f2 = q2 / Jm, c2 = q2 % Jm;
+        const int ps = f <= f2 ? tri(f, f2, nf) : tri(f2, f, nf);
+        const int pa = c <= c2 ? tri(c, c2, Jm) : tri(c2, c, Jm);
+        cc[q2] -= dg * tc[ps * NAm + pa];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Closed-form core responsibility (pruning.hpp:98-134): zeroing cell beta
+// shifts every residual by g p_beta, so
+//   acc = sum (r + g p)^2 = S + g (2 c + g d),  c = sum r p, d = sum p^2
+// resp = (sqrt(acc)/||x|| - re)/re; masked cells keep +inf.
+__global__ void k_core_resp_final(const double* cd, int nf, int Jm, const uint32_t* fib,
+                                  const double* core, const uint8_t* core_mask, double S,
+                                  double x_norm, double re, double* resp) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nf * Jm) return;
+  const int f = q / Jm, c = q % Jm;
+  const int lin = (int)fib[f] * Jm + c;
+  if (core_mask[lin]) return;
+  const double g = core[lin];
+  const double cq = cd[q], dq = cd[nf * Jm + q];
+  double acc = S + g * (2.0 * cq + g * dq);
+  if (acc < 0.0) acc = 0.0;
+  resp[lin] = (sqrt(acc) / x_norm - re) / re;
+}
+
+__global__ void k_fill(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// ---------------------------------------------------------------- host side --
+namespace {
+
+struct Blocks {
+  std::vector<uint32_t> fib;    // all live fibers, row-major order
+  std::vector<int> start, len;  // block ranges into fib
+};
+
+Blocks plan_blocks(const Ctx& c, int F) {
+  Blocks b;
+  const int Jm = c.ranks[c.N - 1];
+  const int P = c.G / Jm;
+  for (int p = 0; p < P; ++p) {
+    bool live = false;
+    for (int q = 0; q < Jm && !live; ++q) live = !c.h_core_mask[(size_t)p * Jm + q];
+    if (live) b.fib.push_back(p);
+  }
+  for (int s = 0; s < (int)b.fib.size(); s += F) {
+    b.start.push_back(s);
+    b.len.push_back(std::min(F, (int)b.fib.size() - s));
+  }
+  return b;
+}
+
+int pick_block(const Ctx& c) {
+  const int Jm = c.ranks[c.N - 1];
+  int F = c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax;
+  // keep the gemm outputs within the kernel's tile capacity
+  while (F > 1) {
+    const int NS = F * (F + 1) / 2, NAm = Jm * (Jm + 1) / 2;
+    const int tiles = ((NS + 3) / 4) * ((NAm + 3) / 4);
+    if (tiles <= kTileMax * kGemmThreads && F * Jm <= kGemmThreads) break;
+    --F;
+  }
+  return F;
+}
+
+void launch_pass(Ctx& c, const CorePassArgs& a) {
+  ProfScope ps(c, kProfCorePass);
+  const int M = c.N - 1;
+  int tot = 0;
+  for (int k = 0; k < M; ++k) tot += c.ranks[k];
+  const size_t sm = (size_t)kPassWarps * tot * 32 * sizeof(double);
+  const dim3 grid((a.csf.nchunks + kPassWarps - 1) / kPassWarps);
+  if (a.csf.nchunks == 0) return;
+#define VEST_PASS(MM)                                                                       \
+  case MM:                                                                                  \
+    check(cudaFuncSetAttribute(k_core_pass<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               (int)sm),                                                    \
+          "pass smem");                                                                     \
+    k_core_pass<MM><<<grid, kPassWarps * 32, sm, c.stream>>>(a);                            \
+    break;
+  switch (M) {
+    VEST_PASS(1)
+    VEST_PASS(2)
+    VEST_PASS(3)
+    VEST_PASS(4)
+    VEST_PASS(5)
+    VEST_PASS(6)
+    VEST_PASS(7)
+    default:
+      throw ArgError{"unsupported order"};
+  }
+#undef VEST_PASS
+  count_launch();
+  check(cudaGetLastError(), "core pass");
+}
+
+// (T, C) or (C, D) for one block into c.d_gemm_out; returns nout.
+int block_gemm(Ctx& c, int nf, int kind, int stride) {
+  const int m = c.N - 1, Jm = c.ranks[m];
+  CoreGemmArgs g{};
+  g.stats = c.d_chunk_stats;
+  g.stride = stride;
+  g.chunks = c.modes[m].d_chunks;
+  g.nchunks = c.modes[m].nchunks;
+  g.A = c.d_factor[m];
+  g.ld = c.ld[m];
+  g.Jm = Jm;
+  g.nf = nf;
+  g.kind = kind;
+  g.NS = kind == 0 ? nf * (nf + 1) / 2 : 0;
+  g.NAm = Jm * (Jm + 1) / 2;
+  g.nT = kind == 0 ? g.NS * g.NAm : 0;
+  g.nout = g.nT + (kind == 0 ? 1 : 2) * nf * Jm;
+  int nblocks = 0;
+  cudaDeviceGetAttribute(&nblocks, cudaDevAttrMultiProcessorCount, c.device);
+  nblocks = std::max(1, std::min<int>(2 * nblocks, (g.nchunks + kGemmBatch - 1) / kGemmBatch));
+  ensure(c, &c.d_gemm_part, &c.gemm_part_cap, (size_t)nblocks * g.nout);
+  ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)g.nout);
+  g.partial = c.d_gemm_part;
+  ProfScope ps(c, kProfCoreGemm);
+  const int NSp = (g.NS + 3) & ~3, NAp = (g.NAm + 3) & ~3;
+  const size_t sm = (size_t)kGemmBatch * (NSp + NAp + 2 * kFMax + Jm) * sizeof(double);
+  check(cudaFuncSetAttribute(k_core_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gemm smem");
+  k_core_gemm<<<nblocks, kGemmThreads, sm, c.stream>>>(g);
+  k_colsum<<<(g.nout + 255) / 256, 256, 0, c.stream>>>(c.d_gemm_part, nblocks, g.nout, c.d_gemm_out);
+  count_launch(2);
+  check(cudaGetLastError(), "core gemm");
+  return g.nout;
+}
+
+CorePassArgs pass_args(Ctx& c) {
+  CorePassArgs a{};
+  a.m = c.model_view();
+  a.csf = c.csf_view(c.N - 1);
+  a.r = c.d_r;
+  return a;
+}
+
+}  // namespace
+
+void core_sweep(Ctx& c, int reg, double lambda) {
+  const int m = c.N - 1, Jm = c.ranks[m];
+  // r = x - B(alpha) for the model after the factor updates
+  // (the reference rebuilds its reconstruction cache here, updates.hpp:190-192)
+  compute_residual(c);
+  const int F = pick_block(c);
+  const Blocks b = plan_blocks(c, F);
+  if (b.fib.empty()) return;  // fully pruned core: nothing to update
+  ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
+  check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice, c.stream),
+        "fibers");
+  const int stride = F * (F + 1) / 2 + F;
+  ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
+  ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
+  ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);
+  CorePassArgs a = pass_args(c);
+  a.stats = c.d_chunk_stats;
+  a.stride = stride;
+  a.chunk_sq = c.d_chunk_sum;
+  a.prev_dg = c.d_dg;
+  for (size_t bi = 0; bi <= b.start.size(); ++bi) {
+    const bool last = bi == b.start.size();
+    a.kind = last ? 2 : 0;
+    a.cur_fib = last ? nullptr : c.d_fibers + b.start[bi];
+    a.cur_nf = last ? 0 : b.len[bi];
+    if (bi > 0) {
+      a.prev_fib = c.d_fibers + b.start[bi - 1];
+      a.prev_nf = b.len[bi - 1];
+    } else {
+      a.prev_fib = c.d_fibers;
+      a.prev_nf = 0;
+    }
+    launch_pass(c, a);
+    if (last) break;
+    // stats layout per chunk: compact S over nf fibers, then R
+    const int nf = b.len[bi];
+    const int st_nf = stride;  // rows keep the kFMax-sized stride
+    block_gemm(c, nf, 0, st_nf);
+    ProfScope ps(c, kProfCoreSolve);
+    k_core_solve<<<1, 32, 0, c.stream>>>(c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core,
+                                         c.d_core_mask, reg, lambda, c.d_dg);
+    count_launch();
+    check(cudaGetLastError(), "core solve");
+  }
+  c.sum_sq = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);
+  c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  c.r_valid = true;
+}
+
+void core_responsibilities(Ctx& c) {
+  const int m = c.N - 1, Jm = c.ranks[m];
+  const size_t G = c.G;
+  k_fill<<<64, 256, 0, c.stream>>>(c.d_resp_core, G, INFINITY);
+  count_launch();
+  if (c.re == 0.0) return;  // perfect fit: everything +inf (pruning.hpp:102-103)
+  const int F = pick_block(c);
+  const Blocks b = plan_blocks(c, F);
+  if (b.fib.empty()) return;
+  ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
+  check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice, c.stream),
+        "fibers");
+  const int stride = 2 * kFMax;
+  ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
+  CorePassArgs a = pass_args(c);
+  a.stats = c.d_chunk_stats;
+  a.stride = stride;
+  a.kind = 1;
+  a.prev_nf = 0;
+  a.prev_fib = c.d_fibers;
+  a.prev_dg = c.d_dg ? c.d_dg : c.d_chunk_stats;
+  for (size_t bi = 0; bi < b.start.size(); ++bi) {
+    a.cur_fib = c.d_fibers + b.start[bi];
+    a.cur_nf = b.len[bi];
+    launch_pass(c, a);
+    const int nf = b.len[bi];
+    block_gemm(c, nf, 1, stride);
+    k_core_resp_final<<<(nf * Jm + 127) / 128, 128, 0, c.stream>>>(
+        c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core, c.d_core_mask, c.sum_sq,
+        c.x_norm, c.re, c.d_resp_core);
+    count_launch();
+    check(cudaGetLastError(), "core resp");
+  }
+}
+
+}  // namespace vest

@@ -1,0 +1,221 @@
+// SPDX-License-Identifier: Apache-2.0
+// vest_internal.h -- host/device shared definitions for libvest_cuda.so.
+//
+// HBM layout:
+//  * per mode n, a CSF copy of the observed entries sorted by (i_n, entry id)
+//    -- the reference's ModeIndex order (sparse_tensor.hpp:107-137) -- stored
+//    SoA: the other N-1 coordinates (uint32 each), the value (fp64) and the
+//    original entry id (uint32); row offsets (uint64, I_n + 1);
+//  * work list per mode: chunks of <= kChunk entries of one row ("light" rows
+//    are one chunk and are solved in-kernel; "heavy" rows span several chunks
+//    whose partial statistics are reduced by a second kernel);
+//  * factors I_n x ld_n fp64 (ld_n = J_n rounded up to even -> 16-byte rows
+//    for vector loads); masks I_n x J_n uint8; dense core fp64 + mask;
+//  * the residual r in the CSF order of the last mode (the core sweep's
+//    traversal order).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#define VEST_MAXN 8
+#define VEST_MAXJ 16
+
+namespace vest {
+
+constexpr uint32_t kLight = 0xFFFFFFFFu;
+constexpr uint32_t kChunk = 2048;  // max entries per work item
+
+struct Chunk {
+  uint32_t row, beg, end, slot;  // [beg, end) in the mode's CSF; slot = heavy partial index or kLight
+};
+struct Heavy {
+  uint32_t row, first_slot, nslots, pad;
+};
+
+struct DevModel {
+  double* factor[VEST_MAXN];
+  uint8_t* fmask[VEST_MAXN];
+  int ld[VEST_MAXN];
+  int J[VEST_MAXN];
+  int stride[VEST_MAXN];  // row-major core strides
+  uint64_t I[VEST_MAXN];
+  double* core;
+  uint8_t* core_mask;
+  const uint32_t* cellbeta;  // packed multi-index per core cell, 4 bits per mode
+  int N;
+  int G;
+};
+
+struct DevCSF {
+  const uint32_t* oc[VEST_MAXN];  // oc[k], k != mode
+  const double* val;
+  const uint32_t* eid;
+  const uint64_t* offsets;
+  const Chunk* chunks;
+  const Heavy* heavy;
+  uint32_t nchunks, nheavy, nslots;
+  int mode;
+};
+
+enum RowKind { kStats = 0, kResp = 1, kResid = 2 };
+
+struct RowPassArgs {
+  DevModel m;
+  DevCSF csf;
+  int mode;
+  int reg;
+  double lambda;
+  double* heavy_out;  // [nslots][stride_na]
+  int stride_na;
+  double re, re2, x2;   // responsibilities
+  double* resp_out;     // I x J (unpadded)
+  double* r_out;        // residual in CSF order
+  double* chunk_out;    // per-chunk sum of squared residuals
+};
+
+struct ModeData {
+  uint64_t* d_offsets = nullptr;
+  uint32_t* d_oc[VEST_MAXN] = {};
+  double* d_val = nullptr;
+  uint32_t* d_eid = nullptr;
+  Chunk* d_chunks = nullptr;
+  Heavy* d_heavy = nullptr;
+  uint32_t* d_empty = nullptr;  // rows with no entries
+  uint32_t nchunks = 0, nheavy = 0, nslots = 0, nempty = 0;
+  std::vector<uint64_t> h_offsets;
+};
+
+struct Ctx;
+
+// Kernel families instantiated for compile-time rank tuples.
+struct ShapeOps {
+  int N;
+  int J[VEST_MAXN];
+  cudaError_t (*rowpass)(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s);
+  cudaError_t (*coo_recon)(const DevModel& m, const uint32_t* coords, const double* values,
+                           uint64_t n, double* out, double* partial, int nblocks, cudaStream_t s);
+};
+
+struct ProfEvent {
+  cudaEvent_t a, b;
+  int fam;
+};
+
+struct Ctx {
+  int device = 0;
+  bool prof_on = false;
+  std::vector<ProfEvent> prof_events;
+  double prof_ms[8] = {};
+  uint64_t prof_n[8] = {};
+  cudaStream_t stream = nullptr;
+  int N = 0;
+  uint64_t dims[VEST_MAXN] = {};
+  int ranks[VEST_MAXN] = {};
+  uint64_t nnz = 0;
+  int G = 1;
+  double x_norm = 0.0;  // frobenius norm over observed values
+
+  ModeData modes[VEST_MAXN];
+
+  double* d_factor[VEST_MAXN] = {};
+  int ld[VEST_MAXN] = {};
+  uint8_t* d_fmask[VEST_MAXN] = {};
+  double* d_core = nullptr;
+  uint8_t* d_core_mask = nullptr;
+  uint32_t* d_cellbeta = nullptr;
+  std::vector<uint8_t> h_core_mask;
+
+  double* d_r = nullptr;  // CSF order of mode N-1
+  bool r_valid = false;
+  double sum_sq = 0.0, re = 0.0;
+
+  double* d_resp_core = nullptr;
+  double* d_resp_f[VEST_MAXN] = {};
+  bool table_valid = false;
+  double table_re = 0.0;
+
+  // scratch
+  double* d_heavy_part = nullptr;  size_t heavy_part_cap = 0;
+  double* d_chunk_stats = nullptr; size_t chunk_stats_cap = 0;
+  double* d_gemm_part = nullptr;   size_t gemm_part_cap = 0;
+  double* d_gemm_out = nullptr;    size_t gemm_out_cap = 0;
+  double* d_chunk_sum = nullptr;   size_t chunk_sum_cap = 0;
+  double* d_small = nullptr;       // small reduction outputs (pinned-mapped readback)
+  double* h_small = nullptr;
+  uint32_t* d_fibers = nullptr;    size_t fibers_cap = 0;  // fiber prefix lin indices
+  double* d_dg = nullptr;          size_t dg_cap = 0;
+  unsigned long long* d_counts = nullptr;  // prune / sparsity counters
+  void* d_sel = nullptr;           // radix-select state
+
+  bool force_generic = false;
+  int core_block = 0;  // fibers per block (0 = auto)
+  const ShapeOps* ops = nullptr;
+  uint64_t device_bytes = 0;
+
+  DevModel model_view() const;
+  DevCSF csf_view(int mode) const;
+};
+
+// ------------------------------------------------------------ host helpers --
+struct CudaError {
+  cudaError_t err;
+  std::string where;
+};
+struct ArgError {
+  std::string msg;
+};
+struct RtError {
+  std::string msg;
+};
+
+void check(cudaError_t e, const char* where);
+void* dalloc(Ctx& c, size_t bytes);
+void ensure(Ctx& c, double** p, size_t* cap, size_t n_doubles);
+uint64_t& launch_counter();
+inline void count_launch(uint64_t n = 1) { launch_counter() += n; }
+
+const ShapeOps* find_shape_ops(int N, const int* J);
+
+// Launchers implemented in the .cu files.
+cudaError_t launch_rowpass_generic(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s);
+cudaError_t launch_coo_recon_generic(const DevModel& m, const uint32_t* coords, const double* values,
+                                     uint64_t n, double* out, double* partial, int nblocks, cudaStream_t s);
+void sync_const_core(Ctx& c);  // copy d_core into every TU's constant-bank core
+
+void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values);
+void update_factor_mode(Ctx& c, int mode, int reg, double lambda);
+void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, int reg, double lambda);
+void compute_residual(Ctx& c);  // fresh r = x - B(alpha), sum_sq, re
+void core_sweep(Ctx& c, int reg, double lambda);
+void responsibilities(Ctx& c);
+void prune(Ctx& c, double pr, uint64_t* counts);
+void sparsity(Ctx& c, double* zero_frac, double* masked_frac);
+void normalize_columns(Ctx& c);
+double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n);
+
+// RAII timing scope for one kernel family (no-op unless profiling is on).
+enum ProfFamily { kProfFactor = 0, kProfCorePass, kProfCoreGemm, kProfCoreSolve, kProfResid, kProfResp, kProfPrune };
+struct ProfScope {
+  Ctx& c;
+  int fam;
+  cudaEvent_t a = nullptr;
+  ProfScope(Ctx& ctx, int f) : c(ctx), fam(f) {
+    if (c.prof_on) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, c.stream);
+    }
+  }
+  ~ProfScope() {
+    if (!c.prof_on || !a) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, c.stream);
+    c.prof_events.push_back({a, b, fam});
+  }
+};
+
+}  // namespace vest

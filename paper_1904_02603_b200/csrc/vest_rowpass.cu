@@ -1,0 +1,564 @@
+// SPDX-License-Identifier: Apache-2.0
+// vest_rowpass.cu -- the per-row passes over one mode's CSF:
+//   kStats : factor-row update (updates.hpp:64-151, update_all_factors :157-175)
+//            statistics gram = sum delta delta^T, xdelta = sum x delta over the
+//            row's entries, then the row's Gauss-Seidel solve in-kernel;
+//   kResp  : factor responsibilities (pruning.hpp:141-179);
+//   kResid : residual r = x - B(alpha) and sum r^2 (tucker_model.hpp:168-183),
+//            run on the last mode's CSF so r lands in the core sweep's order.
+// One warp per work item (a chunk of <= kChunk entries of one row); one lane
+// per observed entry; the per-entry delta is the factorised contraction of
+// vest_common.cuh with the core in the constant bank (compile-time ranks) or
+// the reference's cell loop (generic ranks).
+#include <type_traits>
+
+#include "vest_common.cuh"
+
+namespace vest {
+
+__constant__ double c_core[VEST_CONST_CORE_MAX];
+
+struct ConstCore {
+  __device__ __forceinline__ double operator()(int lin) const { return c_core[lin]; }
+};
+
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+template <int J, int MAXJ>
+__device__ __forceinline__ void load_row(const double* __restrict__ row, double (&dst)[MAXJ]) {
+#pragma unroll
+  for (int b = 0; b + 1 < J; b += 2) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(row + b));
+    dst[b] = v.x;
+    dst[b + 1] = v.y;
+  }
+  if constexpr (J & 1) dst[J - 1] = __ldg(row + J - 1);
+}
+
+// ------------------------------------------------------------------ policies --
+template <class S, int MODE>
+struct StaticPolicy {
+  static constexpr int N = S::N;
+  static constexpr int MAXJ = S::MAXJ;
+  static constexpr int JN = S::J(MODE);
+  static constexpr bool kStatic = true;
+  static constexpr int K0 = (MODE == 0) ? 1 : 0;
+  int jn;  // unused, keeps the interface uniform
+  __device__ __forceinline__ int J() const { return JN; }
+  __device__ __forceinline__ int mode() const { return MODE; }
+  // delta of the entry at CSF position pos (rows of modes != MODE gathered;
+  // mode K0 is read element-wise inside the rolled loop)
+  __device__ __forceinline__ void entry_delta(const DevModel& m, const DevCSF& csf, uint32_t pos,
+                                              double (&d)[MAXJ]) const {
+    double u[N][MAXJ];
+    const double* row0 = nullptr;
+    static_for<0, N>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      if constexpr (k != MODE) {
+        const uint32_t i = __ldg(csf.oc[k] + pos);
+        constexpr int ld = (S::J(k) + 1) & ~1;
+        if constexpr (k == K0)
+          row0 = m.factor[k] + (size_t)i * ld;
+        else
+          load_row<S::J(k)>(m.factor[k] + (size_t)i * ld, u[k]);
+      }
+    });
+    delta_static<S, MODE>(ConstCore{}, u, row0, d);
+  }
+};
+
+// Generic ranks: the reference's own cell loop (updates.hpp:42-51), skipping
+// zero cells and multiplying factors in ascending mode order, so delta is
+// bit-identical to compute_delta.
+struct DynPolicy {
+  static constexpr int N = VEST_MAXN;
+  static constexpr int MAXJ = VEST_MAXJ;
+  static constexpr bool kStatic = false;
+  int md;
+  int jn;
+  __device__ __forceinline__ int J() const { return jn; }
+  __device__ __forceinline__ int mode() const { return md; }
+  __device__ __forceinline__ void entry_delta(const DevModel& m, const DevCSF& csf, uint32_t pos,
+                                              double (&d)[MAXJ]) const {
+    double u[N][MAXJ];
+    for (int k = 0; k < m.N; ++k) {
+      if (k == md) continue;
+      const uint32_t i = __ldg(csf.oc[k] + pos);
+      const double* row = m.factor[k] + (size_t)i * m.ld[k];
+      for (int b = 0; b < m.J[k]; ++b) u[k][b] = __ldg(row + b);
+    }
+    for (int j = 0; j < jn; ++j) d[j] = 0.0;
+    for (int lin = 0; lin < m.G; ++lin) {
+      const double g = __ldg(m.core + lin);
+      if (g == 0.0) continue;
+      const uint32_t beta = __ldg(m.cellbeta + lin);
+      double p = g;
+      for (int k = 0; k < m.N; ++k)
+        if (k != md) p *= u[k][(beta >> (4 * k)) & 15u];
+      d[(beta >> (4 * md)) & 15u] += p;
+    }
+  }
+};
+
+// ----------------------------------------------------------------- row solve --
+// update_factor_row_lf (updates.hpp:96-105) / _l1 (:120-138) given the row's
+// gram (J x J, smem) and xdelta (smem): columns in ascending order, each one
+// seeing the fresh values of the columns before it.  Lane t holds element t.
+__device__ __forceinline__ void solve_row(int J, int reg, double lambda, const double* G,
+                                          const double* xd, double* row, const uint8_t* mask,
+                                          int lane) {
+  double v = lane < J ? row[lane] : 0.0;
+  for (int j = 0; j < J; ++j) {
+    if (mask[j]) continue;
+    const double prod = (lane < J && lane != j) ? G[j * J + lane] * v : 0.0;
+    const double s = warp_sum(prod);
+    const double lin = xd[j] - s;
+    const double gjj = G[j * J + j];
+    double nv = 0.0;
+    bool upd;
+    if (reg == 0) {
+      const double den = gjj + lambda;
+      upd = den != 0.0;
+      nv = lin / den;
+    } else {
+      const double g = -2.0 * lin;
+      const double d = 2.0 * gjj;
+      if (d == 0.0) {
+        upd = fabs(g) <= lambda;
+        nv = 0.0;
+      } else {
+        upd = true;
+        nv = g > lambda ? (lambda - g) / d : (g < -lambda ? -(lambda + g) / d : 0.0);
+      }
+    }
+    if (upd && lane == j) v = nv;
+  }
+  if (lane < J) row[lane] = v;
+}
+
+// pair index -> (t, j) over the upper triangle of a J x J matrix, row-major,
+// followed by J (t, J) "x column" pairs.
+__device__ __forceinline__ void pair_of(int a, int J, int& t, int& j) {
+  const int ng = J * (J + 1) / 2;
+  if (a >= ng) {
+    t = a - ng;
+    j = J;
+    return;
+  }
+  int row = 0, rem = a;
+  while (rem >= J - row) {
+    rem -= J - row;
+    ++row;
+  }
+  t = row;
+  j = row + rem;
+}
+
+// Transposed butterfly: V register values per lane (V % 32 == 0) -> after 5
+// exchange steps lane l holds the warp totals of indices [l*V/32, (l+1)*V/32).
+template <int V>
+__device__ __forceinline__ void transpose_reduce(double (&v)[V], int lane) {
+  static_assert(V % 32 == 0, "V must be a multiple of 32");
+  static_for<0, 5>([&](auto sc) {
+    constexpr int s = decltype(sc)::value;
+    constexpr int W = V >> s;  // live width before this step
+    constexpr int H = W / 2;
+    constexpr int off = 16 >> s;
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double keep = up ? v[i + H] : v[i];
+      const double send = up ? v[i] : v[i + H];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  });
+}
+
+// ------------------------------------------------------------------- kernel --
+constexpr int kRowWarps = 8;
+constexpr int kMaxSlots = 5;  // ceil((16*17/2 + 16) / 32)
+
+template <class P>
+__device__ __forceinline__ int rank_of(const P& pol) {
+  if constexpr (P::kStatic) return P::JN;
+  else return pol.J();
+}
+
+template <class P>
+constexpr int stage_words() {
+  // per-warp shared memory: 32 staged rows of (J + 1) doubles (odd stride)
+  // or the row solve area (J*J + J), whichever is larger
+  constexpr int J = P::MAXJ;
+  constexpr int st = 32 * (J + 2);
+  constexpr int sv = J * J + J;
+  return st > sv ? st : sv;
+}
+
+// Statistics of the row's entries are accumulated in "slots": slot s (owned
+// by lane s % 32) is the pair (t, j) of the gram upper triangle, or (t, x) for
+// xdelta.  Each round stages the 32 lanes' delta vectors in shared memory and
+// every lane adds its slots' 32 products -- a register-light transpose of the
+// per-entry outer products (no per-lane 65-wide accumulator, no butterfly).
+template <class P, int KIND>
+__global__ void __launch_bounds__(kRowWarps * 32) k_rowpass(RowPassArgs a, P pol) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t ci = blockIdx.x * kRowWarps + warp;
+  if (ci >= a.csf.nchunks) return;
+  const Chunk ch = a.csf.chunks[ci];
+  const int J = rank_of(pol);
+  const int mode = pol.mode();
+  constexpr int MAXJ = P::MAXJ;
+  const int NG = J * (J + 1) / 2;
+  const int NA = NG + J;
+  const int ldst = (J & 1) ? J + 2 : J + 1;  // odd stride: conflict-free staging
+  double* wsm = smem + warp * stage_words<P>();
+
+  double arow[MAXJ];
+  if constexpr (KIND != kStats) {
+    const double* r = a.m.factor[mode] + (size_t)ch.row * a.m.ld[mode];
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j)
+      if (j < J) arow[j] = __ldg(r + j);
+  }
+
+  int st_t[kMaxSlots], st_j[kMaxSlots];
+  double sacc[kMaxSlots];
+#pragma unroll
+  for (int q = 0; q < kMaxSlots; ++q) {
+    sacc[q] = 0.0;
+    st_t[q] = 0;
+    st_j[q] = 0;
+    if (lane + 32 * q < NA) pair_of(lane + 32 * q, J, st_t[q], st_j[q]);
+  }
+  double racc[MAXJ];
+#pragma unroll
+  for (int j = 0; j < MAXJ; ++j) racc[j] = 0.0;
+  double sq = 0.0;
+
+  for (uint32_t base = ch.beg; base < ch.end; base += 32) {
+    const uint32_t pos = base + lane;
+    const bool valid = pos < ch.end;
+    double d[MAXJ];
+    double x = 0.0;
+    if (valid) {
+      pol.entry_delta(a.m, a.csf, pos, d);
+      x = __ldg(a.csf.val + pos);
+    } else {
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j) d[j] = 0.0;
+    }
+    if constexpr (KIND == kStats) {
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j)
+        if (j < J) wsm[lane * ldst + j] = d[j];
+      wsm[lane * ldst + J] = x;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kMaxSlots; ++q) {
+        if (lane + 32 * q < NA) {
+          const double* pt = wsm + st_t[q];
+          const double* pj = wsm + st_j[q];
+          double acc_s = sacc[q];
+#pragma unroll 8
+          for (int l = 0; l < 32; ++l) acc_s = fma(pt[l * ldst], pj[l * ldst], acc_s);
+          sacc[q] = acc_s;
+        }
+      }
+      __syncwarp();
+    } else if (valid) {
+      double rec = 0.0;
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j)
+        if (j < J) rec = fma(d[j], arow[j], rec);
+      const double r = x - rec;
+      if constexpr (KIND == kResp) {
+#pragma unroll
+        for (int j = 0; j < MAXJ; ++j) {
+          if (j < J) {
+            const double p = d[j] * arow[j];
+            racc[j] = fma(2.0 * r + p, p, racc[j]);
+          }
+        }
+      } else {
+        a.r_out[pos] = r;
+        sq = fma(r, r, sq);
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- epilogue
+  if constexpr (KIND == kStats) {
+    double* Gs = wsm;          // J x J
+    double* xd = wsm + J * J;  // J
+#pragma unroll
+    for (int q = 0; q < kMaxSlots; ++q) {
+      const int s = lane + 32 * q;
+      if (s < NA) {
+        if (ch.slot != kLight) {
+          a.heavy_out[(size_t)ch.slot * a.stride_na + s] = sacc[q];
+        } else if (st_j[q] == J) {
+          xd[st_t[q]] = sacc[q];
+        } else {
+          Gs[st_t[q] * J + st_j[q]] = sacc[q];
+          Gs[st_j[q] * J + st_t[q]] = sacc[q];
+        }
+      }
+    }
+    if (ch.slot == kLight) {
+      __syncwarp();
+      solve_row(J, a.reg, a.lambda, Gs, xd, a.m.factor[mode] + (size_t)ch.row * a.m.ld[mode],
+                a.m.fmask[mode] + (size_t)ch.row * J, lane);
+    }
+  } else if constexpr (KIND == kResp) {
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j)
+      if (j < J) racc[j] = warp_sum(racc[j]);
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      if (j >= J || lane != j) continue;
+      if (ch.slot != kLight) {
+        a.heavy_out[(size_t)ch.slot * a.stride_na + j] = racc[j];
+      } else {
+        const size_t o = (size_t)ch.row * J + j;
+        if (a.m.fmask[mode][o]) continue;  // stays +inf
+        double err2 = a.re2 + racc[j] / a.x2;
+        if (err2 < 0.0) err2 = 0.0;
+        a.resp_out[o] = (sqrt(err2) - a.re) / a.re;
+      }
+    }
+  } else {
+    sq = warp_sum(sq);
+    if (lane == 0) a.chunk_out[ci] = sq;
+  }
+}
+
+// Heavy rows (several chunks): reduce the chunks' partial statistics in chunk
+// order, then solve (kStats) or finalise responsibilities (kResp).
+__global__ void __launch_bounds__(256) k_heavy(RowPassArgs a, int kind) {
+  __shared__ double sm[8][VEST_MAXJ * VEST_MAXJ + VEST_MAXJ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t hi = blockIdx.x * 8 + warp;
+  if (hi >= a.csf.nheavy) return;
+  const Heavy h = a.csf.heavy[hi];
+  const int mode = a.mode;
+  const int J = a.m.J[mode];
+  const int NA = kind == kStats ? J * (J + 1) / 2 + J : J;
+  double* Gs = sm[warp];
+  double* xd = Gs + J * J;
+  for (int s = lane; s < NA; s += 32) {
+    double v = 0.0;
+    for (uint32_t c = 0; c < h.nslots; ++c) v += a.heavy_out[(size_t)(h.first_slot + c) * a.stride_na + s];
+    if (kind == kStats) {
+      int t, j;
+      pair_of(s, J, t, j);
+      if (j == J) {
+        xd[t] = v;
+      } else {
+        Gs[t * J + j] = v;
+        Gs[j * J + t] = v;
+      }
+    } else {
+      const size_t o = (size_t)h.row * J + s;
+      if (!a.m.fmask[mode][o]) {
+        double err2 = a.re2 + v / a.x2;
+        if (err2 < 0.0) err2 = 0.0;
+        a.resp_out[o] = (sqrt(err2) - a.re) / a.re;
+      }
+    }
+  }
+  if (kind != kStats) return;
+  __syncwarp();
+  solve_row(J, a.reg, a.lambda, Gs, xd, a.m.factor[mode] + (size_t)h.row * a.m.ld[mode],
+            a.m.fmask[mode] + (size_t)h.row * J, lane);
+}
+
+// ------------------------------------------------------- COO reconstruction --
+// predict / evaluate_test (trainer.hpp:172-190) on entry-major coordinates.
+template <class S>
+struct CooStatic {
+  __device__ __forceinline__ static double recon(const DevModel& m, const uint32_t* at) {
+    double u[S::N][S::MAXJ];
+    static_for<0, S::N>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int ld = (S::J(k) + 1) & ~1;
+      if constexpr (k != 1) load_row<S::J(k)>(m.factor[k] + (size_t)__ldg(at + k) * ld, u[k]);
+    });
+    constexpr int ld1 = (S::J(1) + 1) & ~1;
+    double d[S::MAXJ];
+    delta_static<S, 0>(ConstCore{}, u, m.factor[1] + (size_t)__ldg(at + 1) * ld1, d);
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < S::J(0); ++j) r = fma(d[j], u[0][j], r);
+    return r;
+  }
+};
+
+struct CooDyn {
+  // reconstruct_entry (tucker_model.hpp:112-131) cell loop
+  __device__ __forceinline__ static double recon(const DevModel& m, const uint32_t* at) {
+    double acc = 0.0;
+    for (int lin = 0; lin < m.G; ++lin) {
+      const double g = __ldg(m.core + lin);
+      if (g == 0.0) continue;
+      const uint32_t beta = __ldg(m.cellbeta + lin);
+      double p = g;
+      for (int k = 0; k < m.N; ++k)
+        p *= __ldg(m.factor[k] + (size_t)__ldg(at + k) * m.ld[k] + ((beta >> (4 * k)) & 15u));
+      acc += p;
+    }
+    return acc;
+  }
+};
+
+// out[q] = B(coords[q]) (predict) when values == nullptr; otherwise per-block
+// partial (sum r^2, sum x^2) for evaluate_test.
+template <class R>
+__global__ void __launch_bounds__(256) k_coo_recon(DevModel m, const uint32_t* coords,
+                                                   const double* values, uint64_t n, double* out,
+                                                   double* partial) {
+  __shared__ double red[2][8];
+  double sr = 0.0, sx = 0.0;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const double b = R::recon(m, coords + q * m.N);
+    if (values) {
+      const double x = values[q];
+      const double r = x - b;
+      sr = fma(r, r, sr);
+      sx = fma(x, x, sx);
+    } else {
+      out[q] = b;
+    }
+  }
+  if (!values) return;
+  sr = warp_sum(sr);
+  sx = warp_sum(sx);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[0][w] = sr, red[1][w] = sx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a += red[0][i], b += red[1][i];
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// ---------------------------------------------------------------- launchers --
+template <class P>
+size_t rowpass_smem() {
+  return (size_t)kRowWarps * stage_words<P>() * sizeof(double);
+}
+
+template <class P, int KIND>
+void launch_kind(const RowPassArgs& a, uint32_t nchunks, cudaStream_t s, P pol) {
+  const dim3 grid((nchunks + kRowWarps - 1) / kRowWarps);
+  const size_t sm = rowpass_smem<P>();
+  cudaFuncSetAttribute(k_rowpass<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_rowpass<P, KIND><<<grid, kRowWarps * 32, sm, s>>>(a, pol);
+  count_launch();
+}
+
+template <class P, bool kWithResid>
+cudaError_t run_rowpass(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s, P pol) {
+  if (nchunks > 0) {
+    if (kind == kStats) launch_kind<P, kStats>(a, nchunks, s, pol);
+    else if (kind == kResp) launch_kind<P, kResp>(a, nchunks, s, pol);
+    else if constexpr (kWithResid) launch_kind<P, kResid>(a, nchunks, s, pol);
+    else return cudaErrorInvalidValue;
+  }
+  if (kind != kResid && a.csf.nheavy > 0) {
+    k_heavy<<<(a.csf.nheavy + 7) / 8, 256, 0, s>>>(a, kind);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowpass_generic(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s) {
+  DynPolicy pol;
+  pol.md = a.mode;
+  pol.jn = a.m.J[a.mode];
+  return run_rowpass<DynPolicy, true>(a, kind, nchunks, s, pol);
+}
+
+cudaError_t launch_coo_recon_generic(const DevModel& m, const uint32_t* coords, const double* values,
+                                     uint64_t n, double* out, double* partial, int nblocks,
+                                     cudaStream_t s) {
+  k_coo_recon<CooDyn><<<nblocks, 256, 0, s>>>(m, coords, values, n, out, partial);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------- compile-time rank tables --
+template <class S, int MODE>
+cudaError_t static_mode(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s) {
+  StaticPolicy<S, MODE> pol{};
+  return run_rowpass<StaticPolicy<S, MODE>, MODE == S::N - 1>(a, kind, nchunks, s, pol);
+}
+
+template <class S, int M = 0>
+cudaError_t static_rowpass(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s) {
+  if constexpr (M < S::N) {
+    if (a.mode == M) return static_mode<S, M>(a, kind, nchunks, s);
+    return static_rowpass<S, M + 1>(a, kind, nchunks, s);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
+template <class S>
+cudaError_t static_coo(const DevModel& m, const uint32_t* coords, const double* values, uint64_t n,
+                       double* out, double* partial, int nblocks, cudaStream_t s) {
+  k_coo_recon<CooStatic<S>><<<nblocks, 256, 0, s>>>(m, coords, values, n, out, partial);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int... Js>
+constexpr ShapeOps make_ops() {
+  ShapeOps o{};
+  o.N = sizeof...(Js);
+  const int js[] = {Js...};
+  for (int k = 0; k < (int)sizeof...(Js); ++k) o.J[k] = js[k];
+  o.rowpass = &static_rowpass<SShape<Js...>>;
+  o.coo_recon = &static_coo<SShape<Js...>>;
+  return o;
+}
+
+// The BASELINE.json configurations' rank tuples (plus their 2-mode analogue
+// used by the fixtures); anything else runs the generic kernels.
+static const ShapeOps kOps[] = {
+    make_ops<5, 5, 5>(),        // config 1
+    make_ops<10, 10, 10>(),     // config 2
+    make_ops<10, 10, 5>(),      // config 3
+    make_ops<8, 8, 8, 8>(),     // config 4
+    make_ops<5, 5, 5, 5, 5>(),  // config 5
+};
+
+const ShapeOps* find_shape_ops(int N, const int* J) {
+  for (const auto& o : kOps) {
+    if (o.N != N) continue;
+    bool eq = true;
+    for (int k = 0; k < N; ++k) eq = eq && o.J[k] == J[k];
+    if (eq) return &o;
+  }
+  return nullptr;
+}
+
+void sync_const_core(Ctx& c) {
+  if (c.G <= VEST_CONST_CORE_MAX) {
+    check(cudaMemcpyToSymbolAsync(c_core, c.d_core, sizeof(double) * c.G, 0,
+                                  cudaMemcpyDeviceToDevice, c.stream),
+          "core -> constant bank");
+  }
+}
+
+}  // namespace vest
