@@ -130,11 +130,23 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
     const bool valid = pos < ch.end;
     double r = 0.0;
     if (valid) {
+      // all row gathers issued before use (memory-level parallelism); rows
+      // are 16-byte aligned with even stride, so pairs never cross the row
+      uint32_t idx[M > 0 ? M : 1];
+#pragma unroll
+      for (int k = 0; k < M; ++k) idx[k] = __ldg(a.csf.oc[k] + pos);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        const uint32_t i = __ldg(a.csf.oc[k] + pos);
-        const double* row = a.m.factor[k] + (size_t)i * a.m.ld[k];
-        for (int b = 0; b < a.m.J[k]; ++b) st[(offs[k] + b) * 32 + lane] = __ldg(row + b);
+        const double* row = a.m.factor[k] + (size_t)idx[k] * a.m.ld[k];
+        const int Jk = a.m.J[k];
+#pragma unroll
+        for (int b = 0; b < VEST_MAXJ; b += 2) {
+          if (b < Jk) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(row + b));
+            st[(offs[k] + b) * 32 + lane] = v.x;
+            if (b + 1 < Jk) st[(offs[k] + b + 1) * 32 + lane] = v.y;
+          }
+        }
       }
       r = a.r[pos];
     }
@@ -369,23 +381,34 @@ __device__ __forceinline__ int tri(int i, int j, int n) {  // i <= j
   return i * n - i * (i - 1) / 2 + (j - i);
 }
 
-// Sequential Gauss-Seidel over the block's cells (one warp).  tc = [T | C].
-__global__ void k_core_solve(const double* tc, int nf, int Jm, const uint32_t* fib, double* core,
-                             const uint8_t* core_mask, int reg, double lambda, double* dg_out) {
-  __shared__ double cc[kFMax * VEST_MAXJ];
-  const int lane = threadIdx.x;
+// Sequential Gauss-Seidel over the block's cells (one warp after a CTA-wide
+// load of [T | C], the block's core values and masks into shared memory).
+__global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, int Jm, const uint32_t* fib,
+                                                    double* core, const uint8_t* core_mask, int reg,
+                                                    double lambda, double* dg_out) {
+  extern __shared__ double sm[];
   const int NAm = Jm * (Jm + 1) / 2;
   const int nT = nf * (nf + 1) / 2 * NAm;
   const int nq = nf * Jm;
-  for (int q = lane; q < nq; q += 32) cc[q] = tc[nT + q];
-  __syncwarp();
+  double* T = sm;
+  double* cc = sm + nT;
+  double* gv = cc + nq;
+  double* mk = gv + nq;
+  for (int t = threadIdx.x; t < nT + nq; t += blockDim.x) sm[t] = tc[t];
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int lin = (int)fib[q / Jm] * Jm + q % Jm;
+    gv[q] = core[lin];
+    mk[q] = core_mask[lin] ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   for (int q = 0; q < nq; ++q) {
     const int f = q / Jm, c = q % Jm;
-    const int lin = (int)fib[f] * Jm + c;
     double dg = 0.0;
-    if (!core_mask[lin]) {
-      const double hqq = tc[tri(f, f, nf) * NAm + tri(c, c, Jm)];
-      const double g_old = core[lin];
+    if (mk[q] == 0.0) {
+      const double hqq = T[tri(f, f, nf) * NAm + tri(c, c, Jm)];
+      const double g_old = gv[q];
       const double num = cc[q] + g_old * hqq;
       const double den = hqq;
       double g_new = g_old;
@@ -396,10 +419,8 @@ __global__ void k_core_solve(const double* tc, int nf, int Jm, const uint32_t* f
         const double d = 2.0 * den;
         if (d != 0.0) g_new = g > lambda ? (lambda - g) / d : (g < -lambda ? -(lambda + g) / d : 0.0);
       }
-      if (g_new != g_old) {
-        dg = g_new - g_old;
-        if (lane == 0) core[lin] = g_new;
-      }
+      if (g_new != g_old) dg = g_new - g_old;
+      if (lane == 0) gv[q] = g_new;
     }
     if (lane == 0) dg_out[q] = dg;
     if (dg != 0.0) {
@@ -407,11 +428,13 @@ __global__ void k_core_solve(const double* tc, int nf, int Jm, const uint32_t* f
         const int f2 = q2 / Jm, c2 = q2 % Jm;
         const int ps = f <= f2 ? tri(f, f2, nf) : tri(f2, f, nf);
         const int pa = c <= c2 ? tri(c, c2, Jm) : tri(c2, c, Jm);
-        cc[q2] -= dg * tc[ps * NAm + pa];
+        cc[q2] -= dg * T[ps * NAm + pa];
       }
     }
     __syncwarp();
   }
+  for (int q = lane; q < nq; q += 32)
+    if (mk[q] == 0.0) core[(int)fib[q / Jm] * Jm + q % Jm] = gv[q];
 }
 
 // Closed-form core responsibility (pruning.hpp:98-134): zeroing cell beta
@@ -439,13 +462,20 @@ __global__ void k_fill(double* p, size_t n, double v) {
 }
 
 // ---------------------------------------------------------------- host side --
+const void* find_core_ops(int N, const int* J);
+cudaError_t core_pass_structured(const void* ops, const DevModel& m, const DevCSF& csf, double* r, int prev_p,
+                                 const double* prev_dg, int cur_p, int kind, double* stats, int stride,
+                                 double* chunk_sq, cudaStream_t s);
+
 namespace {
 
 struct Blocks {
-  std::vector<uint32_t> fib;    // all live fibers, row-major order
+  std::vector<uint32_t> fib;    // fibers of all blocks, row-major order
   std::vector<int> start, len;  // block ranges into fib
+  std::vector<int> prefix;      // structured plan: the block's prefix p
 };
 
+// General plan: runs of F consecutive live fibers.
 Blocks plan_blocks(const Ctx& c, int F) {
   Blocks b;
   const int Jm = c.ranks[c.N - 1];
@@ -462,6 +492,24 @@ Blocks plan_blocks(const Ctx& c, int F) {
   return b;
 }
 
+// Structured plan (compile-time ranks): one block per prefix over modes
+// 0..N-3 that has an unmasked cell; all J_{N-2} fibers of the prefix.
+Blocks plan_structured(const Ctx& c) {
+  Blocks b;
+  const int Jm = c.ranks[c.N - 1], F = c.ranks[c.N - 2];
+  const int P = c.G / (F * Jm);
+  for (int p = 0; p < P; ++p) {
+    bool live = false;
+    for (int q = 0; q < F * Jm && !live; ++q) live = !c.h_core_mask[(size_t)p * F * Jm + q];
+    if (!live) continue;
+    b.start.push_back((int)b.fib.size());
+    b.len.push_back(F);
+    b.prefix.push_back(p);
+    for (int f = 0; f < F; ++f) b.fib.push_back(p * F + f);
+  }
+  return b;
+}
+
 int pick_block(const Ctx& c) {
   const int Jm = c.ranks[c.N - 1];
   int F = c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax;
@@ -473,6 +521,11 @@ int pick_block(const Ctx& c) {
     --F;
   }
   return F;
+}
+
+const void* structured_ops(const Ctx& c) {
+  if (c.force_generic || c.N < 3 || c.core_block > 0) return nullptr;
+  return find_core_ops(c.N, c.ranks);
 }
 
 void launch_pass(Ctx& c, const CorePassArgs& a) {
@@ -504,6 +557,34 @@ void launch_pass(Ctx& c, const CorePassArgs& a) {
 #undef VEST_PASS
   count_launch();
   check(cudaGetLastError(), "core pass");
+}
+
+// One pass of the block schedule: previous block's residual update, then
+// the current block's statistics (kind 0/1) or the sum of r^2 (kind 2).
+void run_pass(Ctx& c, const void* sops, const Blocks& b, int prev, int cur, int kind, int stride) {
+  const int m = c.N - 1;
+  if (sops) {
+    ProfScope ps(c, kProfCorePass);
+    check(core_pass_structured(sops, c.model_view(), c.csf_view(m), c.d_r, prev >= 0 ? b.prefix[prev] : -1,
+                               c.d_dg, cur >= 0 ? b.prefix[cur] : -1, kind, c.d_chunk_stats, stride,
+                               c.d_chunk_sum, c.stream),
+          "core pass (structured)");
+    return;
+  }
+  CorePassArgs a{};
+  a.m = c.model_view();
+  a.csf = c.csf_view(m);
+  a.r = c.d_r;
+  a.stats = c.d_chunk_stats;
+  a.stride = stride;
+  a.chunk_sq = c.d_chunk_sum;
+  a.prev_dg = c.d_dg;
+  a.kind = kind;
+  a.cur_fib = cur >= 0 ? c.d_fibers + b.start[cur] : c.d_fibers;
+  a.cur_nf = cur >= 0 ? b.len[cur] : 0;
+  a.prev_fib = prev >= 0 ? c.d_fibers + b.start[prev] : c.d_fibers;
+  a.prev_nf = prev >= 0 ? b.len[prev] : 0;
+  launch_pass(c, a);
 }
 
 // (T, C) or (C, D) for one block into c.d_gemm_out; returns nout.
@@ -540,12 +621,11 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
   return g.nout;
 }
 
-CorePassArgs pass_args(Ctx& c) {
-  CorePassArgs a{};
-  a.m = c.model_view();
-  a.csf = c.csf_view(c.N - 1);
-  a.r = c.d_r;
-  return a;
+void upload_fibers(Ctx& c, const Blocks& b) {
+  ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
+  check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                        c.stream),
+        "fibers");
 }
 
 }  // namespace
@@ -555,43 +635,28 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   // r = x - B(alpha) for the model after the factor updates
   // (the reference rebuilds its reconstruction cache here, updates.hpp:190-192)
   compute_residual(c);
-  const int F = pick_block(c);
-  const Blocks b = plan_blocks(c, F);
+  const void* sops = structured_ops(c);
+  const int F = sops ? c.ranks[c.N - 2] : pick_block(c);
+  const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
   if (b.fib.empty()) return;  // fully pruned core: nothing to update
-  ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
-  check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t),
-                        cudaMemcpyHostToDevice, c.stream),
-        "fibers");
+  upload_fibers(c, b);
   const int stride = F * (F + 1) / 2 + F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
-  ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
+  ensure(c, &c.d_dg, &c.dg_cap, (size_t)16 * VEST_MAXJ);
   ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);
-  CorePassArgs a = pass_args(c);
-  a.stats = c.d_chunk_stats;
-  a.stride = stride;
-  a.chunk_sq = c.d_chunk_sum;
-  a.prev_dg = c.d_dg;
-  for (size_t bi = 0; bi <= b.start.size(); ++bi) {
-    const bool last = bi == b.start.size();
-    a.kind = last ? 2 : 0;
-    a.cur_fib = last ? nullptr : c.d_fibers + b.start[bi];
-    a.cur_nf = last ? 0 : b.len[bi];
-    if (bi > 0) {
-      a.prev_fib = c.d_fibers + b.start[bi - 1];
-      a.prev_nf = b.len[bi - 1];
-    } else {
-      a.prev_fib = c.d_fibers;
-      a.prev_nf = 0;
-    }
-    launch_pass(c, a);
+  const int nb = (int)b.start.size();
+  for (int bi = 0; bi <= nb; ++bi) {
+    const bool last = bi == nb;
+    run_pass(c, sops, b, bi - 1, last ? -1 : bi, last ? 2 : 0, stride);
     if (last) break;
-    // stats layout per chunk: compact S over nf fibers, then R
     const int nf = b.len[bi];
-    const int st_nf = stride;  // rows keep the kFMax-sized stride
-    block_gemm(c, nf, 0, st_nf);
+    block_gemm(c, nf, 0, stride);
     ProfScope ps(c, kProfCoreSolve);
-    k_core_solve<<<1, 32, 0, c.stream>>>(c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core,
-                                         c.d_core_mask, reg, lambda, c.d_dg);
+    const int NAm = Jm * (Jm + 1) / 2;
+    const size_t sm = ((size_t)nf * (nf + 1) / 2 * NAm + 3 * (size_t)nf * Jm) * sizeof(double);
+    check(cudaFuncSetAttribute(k_core_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "solve smem");
+    k_core_solve<<<1, 256, sm, c.stream>>>(c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core,
+                                           c.d_core_mask, reg, lambda, c.d_dg);
     count_launch();
     check(cudaGetLastError(), "core solve");
   }
@@ -606,31 +671,21 @@ void core_responsibilities(Ctx& c) {
   k_fill<<<64, 256, 0, c.stream>>>(c.d_resp_core, G, INFINITY);
   count_launch();
   if (c.re == 0.0) return;  // perfect fit: everything +inf (pruning.hpp:102-103)
-  const int F = pick_block(c);
-  const Blocks b = plan_blocks(c, F);
+  const void* sops = structured_ops(c);
+  const int F = sops ? c.ranks[c.N - 2] : pick_block(c);
+  const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
   if (b.fib.empty()) return;
-  ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
-  check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t),
-                        cudaMemcpyHostToDevice, c.stream),
-        "fibers");
-  const int stride = 2 * kFMax;
+  upload_fibers(c, b);
+  const int stride = 2 * F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
-  CorePassArgs a = pass_args(c);
-  a.stats = c.d_chunk_stats;
-  a.stride = stride;
-  a.kind = 1;
-  a.prev_nf = 0;
-  a.prev_fib = c.d_fibers;
-  a.prev_dg = c.d_dg ? c.d_dg : c.d_chunk_stats;
-  for (size_t bi = 0; bi < b.start.size(); ++bi) {
-    a.cur_fib = c.d_fibers + b.start[bi];
-    a.cur_nf = b.len[bi];
-    launch_pass(c, a);
+  ensure(c, &c.d_dg, &c.dg_cap, (size_t)16 * VEST_MAXJ);
+  for (int bi = 0; bi < (int)b.start.size(); ++bi) {
+    run_pass(c, sops, b, -1, bi, 1, stride);
     const int nf = b.len[bi];
     block_gemm(c, nf, 1, stride);
     k_core_resp_final<<<(nf * Jm + 127) / 128, 128, 0, c.stream>>>(
-        c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core, c.d_core_mask, c.sum_sq,
-        c.x_norm, c.re, c.d_resp_core);
+        c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core, c.d_core_mask, c.sum_sq, c.x_norm, c.re,
+        c.d_resp_core);
     count_launch();
     check(cudaGetLastError(), "core resp");
   }
