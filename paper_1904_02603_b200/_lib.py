@@ -12,7 +12,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvest_cuda.so")
+LIB_PATH = os.environ.get("VEST_LIB") or os.path.join(HERE, "libvest_cuda.so")
 CSRC = os.path.join(HERE, "csrc")
 
 u64p = C.POINTER(C.c_uint64)

@@ -61,19 +61,36 @@ struct SShape {
 // delta(j) for mode n (updates.hpp:35-52, "compute_delta"): the reconstruction
 // with the mode-n factor row replaced by the j-th unit vector,
 //   delta[j] = sum_{beta: beta_n = j} G[beta] prod_{k != n} u_k[beta_k].
-// The static version is factorised: modes before n scale a running weight w,
-// modes after n are contracted innermost-first (nested dot products), so the
-// cost is |G| + |G|/J_{N-1} + ... FMAs instead of the reference's |G|*(N-1)
+// Factorised: modes before n scale a running weight w, modes after n are
+// contracted innermost-first (nested dot products), so the cost is
+// |G| + |G|/J_{N-1} + ... FMAs instead of the reference's |G|*(N-1)
 // multiplies.  Summation order differs from the reference (rounding only).
+#ifndef VEST_CONST_PAIRS
+#define VEST_CONST_PAIRS 1
+#endif
+// Single-entry form (the rolled outer loop keeps the core offset in a
+// uniform register: LDCU operands).
 template <class S, int k, class GA>
 __device__ __forceinline__ double trailing(const GA& g, const double (&u)[S::N][S::MAXJ], int lin) {
   if constexpr (k == S::N) {
     return g(lin);
   } else if constexpr (k == S::N - 1) {
-    double s = g(lin) * u[k][0];
+    if constexpr ((S::J(k) & 1) == 0 && VEST_CONST_PAIRS) {
+      // lin is a multiple of J_{N-1} (even): adjacent cells as one 128-bit load
+      double s = 0.0;
 #pragma unroll
-    for (int c = 1; c < S::J(k); ++c) s = fma(g(lin + c), u[k][c], s);
-    return s;
+      for (int c = 0; c < S::J(k); c += 2) {
+        const double2 p = g.pair(lin + c);
+        s = c == 0 ? p.x * u[k][0] : fma(p.x, u[k][c], s);
+        s = fma(p.y, u[k][c + 1], s);
+      }
+      return s;
+    } else {
+      double s = g(lin) * u[k][0];
+#pragma unroll
+      for (int c = 1; c < S::J(k); ++c) s = fma(g(lin + c), u[k][c], s);
+      return s;
+    }
   } else {
     double s = u[k][0] * trailing<S, k + 1>(g, u, lin);
 #pragma unroll
@@ -86,10 +103,19 @@ template <class S, int n, int k, class GA>
 __device__ __forceinline__ void delta_prefix(const GA& g, const double (&u)[S::N][S::MAXJ], double w,
                                              int lin, double (&delta)[S::MAXJ]) {
   if constexpr (k == n) {
+    if constexpr (n == S::N - 1 && (S::J(n) & 1) == 0 && VEST_CONST_PAIRS) {
 #pragma unroll
-    for (int j = 0; j < S::J(n); ++j) {
-      const double t = trailing<S, n + 1>(g, u, lin + j * S::stride(n));
-      delta[j] = fma(w, t, delta[j]);
+      for (int j = 0; j < S::J(n); j += 2) {
+        const double2 p = g.pair(lin + j);
+        delta[j] = fma(w, p.x, delta[j]);
+        delta[j + 1] = fma(w, p.y, delta[j + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < S::J(n); ++j) {
+        const double t = trailing<S, n + 1>(g, u, lin + j * S::stride(n));
+        delta[j] = fma(w, t, delta[j]);
+      }
     }
   } else {
 #pragma unroll
@@ -123,6 +149,160 @@ __device__ __forceinline__ void delta_static(const GA& g, const double (&u)[S::N
       delta_prefix<S, n, 1>(g, u, w0, base, delta);
     }
   }
+}
+
+
+// Multi-entry form: NE entries per lane share every core-value load (one
+// uniform constant load feeds NE DFMA), which lifts the issue bound of the
+// single-entry contraction (one LDCU per DFMA).  Same factorisation as above;
+// the outermost "other" mode k0 (first mode != n) runs as a rolled loop whose
+// factor values are read per iteration (rows0[e]) and whose core offset is a
+// warp-uniform runtime value.
+template <class S, int k, int NE, class GA>
+__device__ __forceinline__ void trailingN(const GA& g, const double (&u)[NE][S::N][S::MAXJ], int lin,
+                                          double (&s)[NE]) {
+  if constexpr (k == S::N) {
+    const double v = g(lin);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) s[e] = v;
+  } else if constexpr (k == S::N - 1) {
+    {
+      const double v = g(lin);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) s[e] = v * u[e][k][0];
+    }
+#pragma unroll
+    for (int c = 1; c < S::J(k); ++c) {
+      const double v = g(lin + c);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) s[e] = fma(v, u[e][k][c], s[e]);
+    }
+  } else {
+    double t[NE];
+    trailingN<S, k + 1, NE>(g, u, lin, t);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) s[e] = u[e][k][0] * t[e];
+#pragma unroll
+    for (int b = 1; b < S::J(k); ++b) {
+      trailingN<S, k + 1, NE>(g, u, lin + b * S::stride(k), t);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) s[e] = fma(u[e][k][b], t[e], s[e]);
+    }
+  }
+}
+
+template <class S, int n, int k, int NE, class GA>
+__device__ __forceinline__ void delta_prefixN(const GA& g, const double (&u)[NE][S::N][S::MAXJ],
+                                              const double (&w)[NE], int lin, double (&delta)[NE][S::MAXJ]) {
+  if constexpr (k == n) {
+#pragma unroll
+    for (int j = 0; j < S::J(n); ++j) {
+      double t[NE];
+      trailingN<S, n + 1, NE>(g, u, lin + j * S::stride(n), t);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) delta[e][j] = fma(w[e], t[e], delta[e][j]);
+    }
+  } else {
+#pragma unroll
+    for (int b = 0; b < S::J(k); ++b) {
+      double w2[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) w2[e] = w[e] * u[e][k][b];
+      delta_prefixN<S, n, k + 1, NE>(g, u, w2, lin + b * S::stride(k), delta);
+    }
+  }
+}
+
+#ifndef VEST_FULL_UNROLL
+#define VEST_FULL_UNROLL 0
+#endif
+constexpr int kFullUnrollN = VEST_FULL_UNROLL;
+
+template <class S, int n, int NE, class GA>
+__device__ __forceinline__ void delta_staticN(const GA& g, const double (&u)[NE][S::N][S::MAXJ],
+                                              const double* const (&rows0)[NE], double (&delta)[NE][S::MAXJ]) {
+  constexpr int k0 = (n == 0) ? 1 : 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e)
+#pragma unroll
+    for (int j = 0; j < S::J(n); ++j) delta[e][j] = 0.0;
+  if constexpr (S::G() <= kFullUnrollN) {
+    // every core index a compile-time constant: adjacent cells pair into
+    // 128-bit uniform constant loads (LDCU.128)
+    double w1[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) w1[e] = 1.0;
+    if constexpr (n == 0) {
+#pragma unroll
+      for (int j = 0; j < S::J(0); ++j) {
+        double t[NE];
+        trailingN<S, 1, NE>(g, u, j * S::stride(0), t);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) delta[e][j] = t[e];
+      }
+    } else {
+      delta_prefixN<S, n, 0, NE>(g, u, w1, 0, delta);
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int a = 0; a < S::J(k0); ++a) {
+    double w0[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) w0[e] = __ldg(rows0[e] + a);
+    const int base = a * S::stride(k0);
+    if constexpr (n == 0) {
+#pragma unroll
+      for (int j = 0; j < S::J(0); ++j) {
+        double t[NE];
+        trailingN<S, 2, NE>(g, u, base + j * S::stride(0), t);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) delta[e][j] = fma(w0[e], t[e], delta[e][j]);
+      }
+    } else {
+      delta_prefixN<S, n, 1, NE>(g, u, w0, base, delta);
+    }
+  }
+}
+
+// ------------------------------------------------------- FP64 tensor cores --
+// D(8x8) += A(8x4) B(4x8), mma.sync m8n8k4 f64 (SASS DMMA.8x8x4; tensor pipe,
+// concurrent with the DFMA pipe).  Fragments: A[g][t], B[t][g], D[g][2t + i]
+// with g = lane / 4, t = lane % 4.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Gram of 32*NE staged column vectors: X is [col][entry] with row stride
+// kXldN(NE) (== 4 mod 16: conflict-free fragment loads); accumulates the upper
+// tile blocks of X^T X for NC <= 16 columns into d[3][2] (tiles (0,0), (0,1),
+// (1,1)), one DMMA per tile per 4 entries.
+__host__ __device__ constexpr int kXldN(int ne) { return 32 * ne + 4; }
+constexpr int kXld = kXldN(1);
+template <int NC, int NE = 1>
+__device__ __forceinline__ void gram_dmma(const double* X, double (&d)[3][2], int lane) {
+  constexpr int ld = kXldN(NE);
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 8 * NE; ++kk) {
+    const int e = 4 * kk + tq;
+    const double f0 = X[g * ld + e];
+    dmma884(d[0][0], d[0][1], f0, f0);
+    if constexpr (NC > 8) {
+      const double f1 = X[(8 + g) * ld + e];
+      dmma884(d[1][0], d[1][1], f0, f1);
+      dmma884(d[2][0], d[2][1], f1, f1);
+    }
+  }
+}
+
+// (row, col) of accumulator element i of tile t for this lane
+__device__ __forceinline__ void gram_coord(int t, int i, int lane, int& row, int& col) {
+  const int I = t == 2 ? 1 : 0, J = t == 0 ? 0 : 1;
+  row = 8 * I + (lane >> 2);
+  col = 8 * J + 2 * (lane & 3) + i;
 }
 
 }  // namespace vest

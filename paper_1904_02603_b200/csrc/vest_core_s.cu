@@ -38,14 +38,7 @@ __device__ __forceinline__ void sfor_s(Fn&& f) {
   }
 }
 
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
 constexpr int kSWarps = 8;
-constexpr int kXld = 36;  // transposed stage row stride (== 4 mod 16: conflict-free fragments)
 
 template <class S>
 __global__ void __launch_bounds__(kSWarps * 32) k_core_pass_s(CorePassSArgs a) {
@@ -143,19 +136,7 @@ __global__ void __launch_bounds__(kSWarps * 32) k_core_pass_s(CorePassSArgs a) {
     for (int f = 0; f < F; ++f) X[f * kXld + lane] = wc * u[f];
     X[F * kXld + lane] = valid ? r : 0.0;
     __syncwarp();
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int e = 4 * kk + tq;
-      const double f0 = X[g * kXld + e];
-      if constexpr (NT == 1) {
-        dmma(d[0][0], d[0][1], f0, f0);
-      } else {
-        const double f1 = X[(8 + g) * kXld + e];
-        dmma(d[0][0], d[0][1], f0, f0);
-        dmma(d[1][0], d[1][1], f0, f1);
-        dmma(d[2][0], d[2][1], f1, f1);
-      }
-    }
+    gram_dmma<NC>(X, d, lane);
     __syncwarp();
   }
 

@@ -16,10 +16,15 @@
 
 namespace vest {
 
-__constant__ double c_core[VEST_CONST_CORE_MAX];
+// The core as double2 (pairs of adjacent cells): one LDCU.128 feeds two DFMA.
+__constant__ double2 c_core_pairs[VEST_CONST_CORE_MAX / 2];
 
 struct ConstCore {
-  __device__ __forceinline__ double operator()(int lin) const { return c_core[lin]; }
+  __device__ __forceinline__ double operator()(int lin) const {
+    const double2 p = c_core_pairs[lin >> 1];
+    return (lin & 1) ? p.y : p.x;
+  }
+  __device__ __forceinline__ double2 pair(int lin) const { return c_core_pairs[lin >> 1]; }  // lin even
 };
 
 template <int B, int E, class F>
@@ -42,20 +47,54 @@ __device__ __forceinline__ void load_row(const double* __restrict__ row, double 
 }
 
 // ------------------------------------------------------------------ policies --
+// A policy computes delta for NE entries per lane: the CSF positions pos[e]
+// (clamped into the chunk by the caller), rows of the other modes gathered.
 template <class S, int MODE>
 struct StaticPolicy {
+#ifndef VEST_CORE_SMEM
+#define VEST_CORE_SMEM 0
+#endif
+  static constexpr bool kSmemCore = VEST_CORE_SMEM && S::G() <= 1024;
   static constexpr int N = S::N;
   static constexpr int MAXJ = S::MAXJ;
   static constexpr int JN = S::J(MODE);
   static constexpr bool kStatic = true;
+#ifndef VEST_ROW_NE
+#define VEST_ROW_NE 2
+#endif
+  static constexpr int NE = VEST_ROW_NE;  // entries per lane per round
   static constexpr int K0 = (MODE == 0) ? 1 : 0;
   int jn;  // unused, keeps the interface uniform
   __device__ __forceinline__ int J() const { return JN; }
   __device__ __forceinline__ int mode() const { return MODE; }
-  // delta of the entry at CSF position pos (rows of modes != MODE gathered;
-  // mode K0 is read element-wise inside the rolled loop)
-  __device__ __forceinline__ void entry_delta(const DevModel& m, const DevCSF& csf, uint32_t pos,
-                                              double (&d)[MAXJ]) const {
+  __device__ __forceinline__ void entries(const DevModel& m, const DevCSF& csf, const uint32_t (&pos)[NE],
+                                          double (&d)[NE][MAXJ]) const {
+    double u[NE][N][MAXJ];
+    const double* rows0[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      static_for<0, N>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        if constexpr (k != MODE) {
+          const uint32_t i = __ldg(csf.oc[k] + pos[e]);
+          constexpr int ld = (S::J(k) + 1) & ~1;
+          if constexpr (k == K0 && S::G() > kFullUnrollN)
+            rows0[e] = m.factor[k] + (size_t)i * ld;  // read element-wise by the rolled loop
+          else
+            load_row<S::J(k)>(m.factor[k] + (size_t)i * ld, u[e][k]);
+        }
+      });
+    }
+#if VEST_CORE_SMEM
+    delta_staticN<S, MODE, NE>(SmemCore{score}, u, rows0, d);
+#else
+    delta_staticN<S, MODE, NE>(ConstCore{}, u, rows0, d);
+#endif
+  }
+  const double* score = nullptr;
+  // single entry (NE == 1): the v1 structure, called only for valid lanes
+  __device__ __forceinline__ void entry1(const DevModel& m, const DevCSF& csf, uint32_t pos,
+                                         double (&d)[MAXJ]) const {
     double u[N][MAXJ];
     const double* row0 = nullptr;
     static_for<0, N>([&](auto kc) {
@@ -74,22 +113,29 @@ struct StaticPolicy {
 };
 
 // Generic ranks: the reference's own cell loop (updates.hpp:42-51), skipping
-// zero cells and multiplying factors in ascending mode order, so delta is
-// bit-identical to compute_delta.
+// zero cells and multiplying factors in ascending mode order.
 struct DynPolicy {
+  static constexpr bool kSmemCore = false;
   static constexpr int N = VEST_MAXN;
   static constexpr int MAXJ = VEST_MAXJ;
   static constexpr bool kStatic = false;
+  static constexpr int NE = 1;
+  static constexpr int JN = VEST_MAXJ;
   int md;
   int jn;
   __device__ __forceinline__ int J() const { return jn; }
   __device__ __forceinline__ int mode() const { return md; }
-  __device__ __forceinline__ void entry_delta(const DevModel& m, const DevCSF& csf, uint32_t pos,
-                                              double (&d)[MAXJ]) const {
+  __device__ __forceinline__ void entries(const DevModel& m, const DevCSF& csf, const uint32_t (&pos)[NE],
+                                          double (&dd)[NE][MAXJ]) const {
+    entry1(m, csf, pos[0], dd[0]);
+  }
+  __device__ __forceinline__ void entry1(const DevModel& m, const DevCSF& csf, uint32_t pos0,
+                                         double (&d)[MAXJ]) const {
     double u[N][MAXJ];
+    const uint32_t pos[1] = {pos0};
     for (int k = 0; k < m.N; ++k) {
       if (k == md) continue;
-      const uint32_t i = __ldg(csf.oc[k] + pos);
+      const uint32_t i = __ldg(csf.oc[k] + pos[0]);
       const double* row = m.factor[k] + (size_t)i * m.ld[k];
       for (int b = 0; b < m.J[k]; ++b) u[k][b] = __ldg(row + b);
     }
@@ -160,66 +206,65 @@ __device__ __forceinline__ void pair_of(int a, int J, int& t, int& j) {
   j = row + rem;
 }
 
-// Transposed butterfly: V register values per lane (V % 32 == 0) -> after 5
-// exchange steps lane l holds the warp totals of indices [l*V/32, (l+1)*V/32).
-template <int V>
-__device__ __forceinline__ void transpose_reduce(double (&v)[V], int lane) {
-  static_assert(V % 32 == 0, "V must be a multiple of 32");
-  static_for<0, 5>([&](auto sc) {
-    constexpr int s = decltype(sc)::value;
-    constexpr int W = V >> s;  // live width before this step
-    constexpr int H = W / 2;
-    constexpr int off = 16 >> s;
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const double keep = up ? v[i + H] : v[i];
-      const double send = up ? v[i] : v[i + H];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  });
-}
-
 // ------------------------------------------------------------------- kernel --
 constexpr int kRowWarps = 8;
 constexpr int kMaxSlots = 5;  // ceil((16*17/2 + 16) / 32)
 
+// Gram of (delta, x) on the FP64 tensor cores (DMMA) when the row rank is a
+// compile-time constant <= 15; generic ranks use shared-memory slots.
+#ifndef VEST_TC_GRAM
+#define VEST_TC_GRAM 1
+#endif
 template <class P>
-__device__ __forceinline__ int rank_of(const P& pol) {
-  if constexpr (P::kStatic) return P::JN;
-  else return pol.J();
-}
+struct TensorGram {
+  static constexpr bool value = VEST_TC_GRAM && P::kStatic && P::MAXJ <= 15;
+};
 
 template <class P>
 constexpr int stage_words() {
-  // per-warp shared memory: 32 staged rows of (J + 1) doubles (odd stride)
-  // or the row solve area (J*J + J), whichever is larger
+  // per-warp shared memory: the transposed DMMA stage (16 x kXldN(NE)), or
+  // 32 staged rows of (J + 1) doubles (odd stride), or the row solve area
+  // (J*J + J), whichever is largest
   constexpr int J = P::MAXJ;
   constexpr int st = 32 * (J + 2);
   constexpr int sv = J * J + J;
-  return st > sv ? st : sv;
+  constexpr int tcw = 16 * kXldN(P::NE);
+  constexpr int m1 = st > sv ? st : sv;
+  return m1 > tcw ? m1 : tcw;
 }
 
-// Statistics of the row's entries are accumulated in "slots": slot s (owned
-// by lane s % 32) is the pair (t, j) of the gram upper triangle, or (t, x) for
-// xdelta.  Each round stages the 32 lanes' delta vectors in shared memory and
-// every lane adds its slots' 32 products -- a register-light transpose of the
-// per-entry outer products (no per-lane 65-wide accumulator, no butterfly).
+// Statistics of the row's entries: on the tensor pipe for static ranks (the
+// (delta, x) vectors of the round's 32*NE entries are staged transposed and
+// X^T X accumulated with DMMA, so the DFMA pipe only runs the contraction);
+// generic ranks accumulate "slots" (pair (t, j) owned by lane s % 32) over
+// shared-memory staged rows.
+#ifndef VEST_ROW_MINB
+#define VEST_ROW_MINB 2
+#endif
 template <class P, int KIND>
-__global__ void __launch_bounds__(kRowWarps * 32) k_rowpass(RowPassArgs a, P pol) {
+__global__ void __launch_bounds__(kRowWarps * 32, VEST_ROW_MINB) k_rowpass(RowPassArgs a, P pol) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if constexpr (P::kSmemCore) {
+    double* sc = smem + kRowWarps * stage_words<P>();
+    for (int t = threadIdx.x; t < a.m.G; t += blockDim.x) sc[t] = __ldg(a.m.core + t);
+    __syncthreads();
+    pol.score = sc;
+  }
   const uint32_t ci = blockIdx.x * kRowWarps + warp;
   if (ci >= a.csf.nchunks) return;
   const Chunk ch = a.csf.chunks[ci];
-  const int J = rank_of(pol);
+  constexpr int NE = P::NE;
+  const int J = pol.J();
   const int mode = pol.mode();
   constexpr int MAXJ = P::MAXJ;
   const int NG = J * (J + 1) / 2;
   const int NA = NG + J;
   const int ldst = (J & 1) ? J + 2 : J + 1;  // odd stride: conflict-free staging
   double* wsm = smem + warp * stage_words<P>();
+  constexpr bool kTC = TensorGram<P>::value;
+  constexpr int ldx = kXldN(NE);
 
   double arow[MAXJ];
   if constexpr (KIND != kStats) {
@@ -231,35 +276,82 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rowpass(RowPassArgs a, P pol
 
   int st_t[kMaxSlots], st_j[kMaxSlots];
   double sacc[kMaxSlots];
+  if constexpr (!kTC) {
 #pragma unroll
-  for (int q = 0; q < kMaxSlots; ++q) {
-    sacc[q] = 0.0;
-    st_t[q] = 0;
-    st_j[q] = 0;
-    if (lane + 32 * q < NA) pair_of(lane + 32 * q, J, st_t[q], st_j[q]);
+    for (int q = 0; q < kMaxSlots; ++q) {
+      sacc[q] = 0.0;
+      st_t[q] = 0;
+      st_j[q] = 0;
+      if (lane + 32 * q < NA) pair_of(lane + 32 * q, J, st_t[q], st_j[q]);
+    }
   }
   double racc[MAXJ];
 #pragma unroll
   for (int j = 0; j < MAXJ; ++j) racc[j] = 0.0;
   double sq = 0.0;
+  double tc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  if constexpr (KIND == kStats && kTC) {
+    // zero the padding columns once; columns <= J are rewritten every round
+    for (int t = lane; t < 16 * ldx; t += 32) wsm[t] = 0.0;
+    __syncwarp();
+  }
 
-  for (uint32_t base = ch.beg; base < ch.end; base += 32) {
-    const uint32_t pos = base + lane;
-    const bool valid = pos < ch.end;
-    double d[MAXJ];
-    double x = 0.0;
-    if (valid) {
-      pol.entry_delta(a.m, a.csf, pos, d);
-      x = __ldg(a.csf.val + pos);
-    } else {
+  for (uint32_t base = ch.beg; base < ch.end; base += 32 * NE) {
+    uint32_t pos[NE];
+    bool valid[NE];
 #pragma unroll
-      for (int j = 0; j < MAXJ; ++j) d[j] = 0.0;
+    for (int e = 0; e < NE; ++e) {
+      pos[e] = base + 32 * e + lane;
+      valid[e] = pos[e] < ch.end;
+      if (!valid[e]) pos[e] = ch.beg;  // safe gather address; result discarded
     }
-    if constexpr (KIND == kStats) {
+    double d[NE][MAXJ];
+    double x[NE];
+    if constexpr (NE == 1) {
+      if (valid[0]) {
+        pol.entry1(a.m, a.csf, pos[0], d[0]);
+        x[0] = __ldg(a.csf.val + pos[0]);
+      } else {
+        x[0] = 0.0;
+#pragma unroll
+        for (int j = 0; j < MAXJ; ++j) d[0][j] = 0.0;
+      }
+    } else {
+      // lane-uniform validity of the first entry guards the contraction (keeps
+      // the core offsets in uniform registers); later entries are clamped
+      if (valid[0]) {
+        pol.entries(a.m, a.csf, pos, d);
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+#pragma unroll
+          for (int j = 0; j < MAXJ; ++j) d[e][j] = 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        x[e] = valid[e] ? __ldg(a.csf.val + pos[e]) : 0.0;
+        if (!valid[e]) {
+#pragma unroll
+          for (int j = 0; j < MAXJ; ++j) d[e][j] = 0.0;
+        }
+      }
+    }
+    if constexpr (KIND == kStats && kTC) {
+      // stage (delta, x) transposed and accumulate X^T X on the tensor pipe
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+#pragma unroll
+        for (int j = 0; j < P::JN; ++j) wsm[j * ldx + 32 * e + lane] = d[e][j];
+        wsm[P::JN * ldx + 32 * e + lane] = x[e];
+      }
+      __syncwarp();
+      gram_dmma<P::JN + 1, NE>(wsm, tc, lane);
+      __syncwarp();
+    } else if constexpr (KIND == kStats) {
 #pragma unroll
       for (int j = 0; j < MAXJ; ++j)
-        if (j < J) wsm[lane * ldst + j] = d[j];
-      wsm[lane * ldst + J] = x;
+        if (j < J) wsm[lane * ldst + j] = d[0][j];
+      wsm[lane * ldst + J] = x[0];
       __syncwarp();
 #pragma unroll
       for (int q = 0; q < kMaxSlots; ++q) {
@@ -273,23 +365,27 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rowpass(RowPassArgs a, P pol
         }
       }
       __syncwarp();
-    } else if (valid) {
-      double rec = 0.0;
+    } else {
 #pragma unroll
-      for (int j = 0; j < MAXJ; ++j)
-        if (j < J) rec = fma(d[j], arow[j], rec);
-      const double r = x - rec;
-      if constexpr (KIND == kResp) {
+      for (int e = 0; e < NE; ++e) {
+        if (!valid[e]) continue;
+        double rec = 0.0;
 #pragma unroll
-        for (int j = 0; j < MAXJ; ++j) {
-          if (j < J) {
-            const double p = d[j] * arow[j];
-            racc[j] = fma(2.0 * r + p, p, racc[j]);
+        for (int j = 0; j < MAXJ; ++j)
+          if (j < J) rec = fma(d[e][j], arow[j], rec);
+        const double r = x[e] - rec;
+        if constexpr (KIND == kResp) {
+#pragma unroll
+          for (int j = 0; j < MAXJ; ++j) {
+            if (j < J) {
+              const double p = d[e][j] * arow[j];
+              racc[j] = fma(2.0 * r + p, p, racc[j]);
+            }
           }
+        } else {
+          a.r_out[pos[e]] = r;
+          sq = fma(r, r, sq);
         }
-      } else {
-        a.r_out[pos] = r;
-        sq = fma(r, r, sq);
       }
     }
   }
@@ -298,17 +394,42 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rowpass(RowPassArgs a, P pol
   if constexpr (KIND == kStats) {
     double* Gs = wsm;          // J x J
     double* xd = wsm + J * J;  // J
+    if constexpr (kTC) {
+      __syncwarp();
 #pragma unroll
-    for (int q = 0; q < kMaxSlots; ++q) {
-      const int s = lane + 32 * q;
-      if (s < NA) {
-        if (ch.slot != kLight) {
-          a.heavy_out[(size_t)ch.slot * a.stride_na + s] = sacc[q];
-        } else if (st_j[q] == J) {
-          xd[st_t[q]] = sacc[q];
-        } else {
-          Gs[st_t[q] * J + st_j[q]] = sacc[q];
-          Gs[st_j[q] * J + st_t[q]] = sacc[q];
+      for (int t = 0; t < (P::JN + 1 > 8 ? 3 : 1); ++t) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          int row, col;
+          gram_coord(t, i, lane, row, col);
+          const double v = tc[t][i];
+          int slot = -1;
+          if (row <= col && col < J) slot = row * J - row * (row - 1) / 2 + (col - row);
+          else if (col == J && row < J) slot = NG + row;
+          if (slot < 0) continue;
+          if (ch.slot != kLight) {
+            a.heavy_out[(size_t)ch.slot * a.stride_na + slot] = v;
+          } else if (col == J) {
+            xd[row] = v;
+          } else {
+            Gs[row * J + col] = v;
+            Gs[col * J + row] = v;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kMaxSlots; ++q) {
+        const int s = lane + 32 * q;
+        if (s < NA) {
+          if (ch.slot != kLight) {
+            a.heavy_out[(size_t)ch.slot * a.stride_na + s] = sacc[q];
+          } else if (st_j[q] == J) {
+            xd[st_t[q]] = sacc[q];
+          } else {
+            Gs[st_t[q] * J + st_j[q]] = sacc[q];
+            Gs[st_j[q] * J + st_t[q]] = sacc[q];
+          }
         }
       }
     }
@@ -385,18 +506,20 @@ __global__ void __launch_bounds__(256) k_heavy(RowPassArgs a, int kind) {
 template <class S>
 struct CooStatic {
   __device__ __forceinline__ static double recon(const DevModel& m, const uint32_t* at) {
-    double u[S::N][S::MAXJ];
+    double u[1][S::N][S::MAXJ];
     static_for<0, S::N>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
       constexpr int ld = (S::J(k) + 1) & ~1;
-      if constexpr (k != 1) load_row<S::J(k)>(m.factor[k] + (size_t)__ldg(at + k) * ld, u[k]);
+      if constexpr (k != 1 || S::G() <= kFullUnrollN)
+        load_row<S::J(k)>(m.factor[k] + (size_t)__ldg(at + k) * ld, u[0][k]);
     });
     constexpr int ld1 = (S::J(1) + 1) & ~1;
-    double d[S::MAXJ];
-    delta_static<S, 0>(ConstCore{}, u, m.factor[1] + (size_t)__ldg(at + 1) * ld1, d);
+    const double* const rows0[1] = {m.factor[1] + (size_t)__ldg(at + 1) * ld1};
+    double d[1][S::MAXJ];
+    delta_staticN<S, 0, 1>(ConstCore{}, u, rows0, d);
     double r = 0.0;
 #pragma unroll
-    for (int j = 0; j < S::J(0); ++j) r = fma(d[j], u[0][j], r);
+    for (int j = 0; j < S::J(0); ++j) r = fma(d[0][j], u[0][0][j], r);
     return r;
   }
 };
@@ -454,14 +577,14 @@ __global__ void __launch_bounds__(256) k_coo_recon(DevModel m, const uint32_t* c
 
 // ---------------------------------------------------------------- launchers --
 template <class P>
-size_t rowpass_smem() {
-  return (size_t)kRowWarps * stage_words<P>() * sizeof(double);
+size_t rowpass_smem(int G) {
+  return ((size_t)kRowWarps * stage_words<P>() + (P::kSmemCore ? (size_t)G : 0)) * sizeof(double);
 }
 
 template <class P, int KIND>
 void launch_kind(const RowPassArgs& a, uint32_t nchunks, cudaStream_t s, P pol) {
   const dim3 grid((nchunks + kRowWarps - 1) / kRowWarps);
-  const size_t sm = rowpass_smem<P>();
+  const size_t sm = rowpass_smem<P>(a.m.G);
   cudaFuncSetAttribute(k_rowpass<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_rowpass<P, KIND><<<grid, kRowWarps * 32, sm, s>>>(a, pol);
   count_launch();
@@ -555,9 +678,9 @@ const ShapeOps* find_shape_ops(int N, const int* J) {
 
 void sync_const_core(Ctx& c) {
   if (c.G <= VEST_CONST_CORE_MAX) {
-    check(cudaMemcpyToSymbolAsync(c_core, c.d_core, sizeof(double) * c.G, 0,
+    check(cudaMemcpyToSymbolAsync(c_core_pairs, c.d_core, sizeof(double) * c.G, 0,
                                   cudaMemcpyDeviceToDevice, c.stream),
-          "core -> constant bank");
+          "core -> constant bank (pairs)");
   }
 }
 
