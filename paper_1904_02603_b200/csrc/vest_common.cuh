@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "vest_internal.h"
 
 namespace vest {
@@ -264,6 +266,17 @@ __device__ __forceinline__ void delta_staticN(const GA& g, const double (&u)[NE]
     }
   }
 }
+
+// The shape without its last mode (the fused residual's contraction with
+// v = G x_{N-1} a_row).
+template <class S, class Seq>
+struct PrefixImpl;
+template <class S, int... I>
+struct PrefixImpl<S, std::integer_sequence<int, I...>> {
+  using type = SShape<S::J(I)...>;
+};
+template <class S>
+using PrefixShape = typename PrefixImpl<S, std::make_integer_sequence<int, S::N - 1>>::type;
 
 // ------------------------------------------------------- FP64 tensor cores --
 // D(8x8) += A(8x4) B(4x8), mma.sync m8n8k4 f64 (SASS DMMA.8x8x4; tensor pipe,

@@ -381,8 +381,162 @@ __device__ __forceinline__ int tri(int i, int j, int n) {  // i <= j
   return i * n - i * (i - 1) / 2 + (j - i);
 }
 
-// Sequential Gauss-Seidel over the block's cells (one warp after a CTA-wide
-// load of [T | C], the block's core values and masks into shared memory).
+// The same block GEMM on the FP64 tensor cores.  With L = the chunk
+// statistics row ([S | R] or [R | D], K = chunks) and Rt = the chunk's
+// last-mode products ([a a^T (packed) | a] or [a | a o a]), the CTA computes
+// its slice of L^T Rt with DMMA m8n8k4 (8x8 output tiles, 4 chunks per
+// k-step); k_gemm_reduce then sums the CTA partials in fixed order and maps
+// the needed blocks to [T | C] or [C | D].  Cross blocks (S^T a, R^T a a^T)
+// are computed and discarded -- cheaper than splitting the operand staging.
+struct GemmTcArgs {
+  const double* stats;
+  int stride;
+  const Chunk* chunks;
+  uint32_t nchunks;
+  const double* A;
+  int ld, Jm, nf, kind;
+  int LW, RW, MT, NT;
+  double* partial;  // [gridDim.x][MT*NT][64]
+};
+
+constexpr int kTcWarps = 8;
+constexpr int kTcTilesPerWarp = 12;
+constexpr int kTcLd = 36;  // == 4 mod 16: conflict-free fragment loads
+
+__global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
+  extern __shared__ double sm[];
+  double* Lt = sm;                           // [MT*8][kTcLd]
+  double* Rt = Lt + a.MT * 8 * kTcLd;        // [NT*8][kTcLd]
+  double* sa = Rt + a.NT * 8 * kTcLd;        // [32][Jm]
+  int* rmap = reinterpret_cast<int*>(sa + 32 * a.Jm);  // Rt column -> (c, c') packed
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int col = threadIdx.x; col < a.NT * 8; col += blockDim.x) {
+    int v = -1;
+    if (col < a.RW) {
+      const int NAm0 = a.Jm * (a.Jm + 1) / 2;
+      if (a.kind == 0 && col < NAm0) {
+        int c = 0, rem = col;
+        while (rem >= a.Jm - c) {
+          rem -= a.Jm - c;
+          ++c;
+        }
+        v = (c << 8) | (c + rem);
+      } else if (a.kind == 0) {
+        v = (1 << 16) | (col - NAm0);  // plain a_c
+      } else {
+        v = col < a.Jm ? ((1 << 16) | col) : ((2 << 16) | (col - a.Jm));  // a_c or a_c^2
+      }
+    }
+    rmap[col] = v;
+  }
+  const int g = lane >> 2, tq = lane & 3;
+  const int ntiles = a.MT * a.NT;
+  const uint32_t per = ((a.nchunks + gridDim.x - 1) / gridDim.x + 31) & ~31u;
+  const uint32_t c0 = blockIdx.x * per;
+  const uint32_t c1 = min(a.nchunks, c0 + per);
+  double acc[kTcTilesPerWarp][2];
+#pragma unroll
+  for (int i = 0; i < kTcTilesPerWarp; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int Jm = a.Jm;
+  for (uint32_t cb = c0; cb < c1; cb += 32) {
+    const int nb = min(32u, c1 - cb);
+    __syncthreads();
+    // statistics rows are contiguous per chunk: read row-major (coalesced),
+    // write transposed
+    const int LWp = a.MT * 8;
+    for (int t = threadIdx.x; t < LWp * 32; t += blockDim.x) {
+      const int k = t / LWp, col = t - k * LWp;
+      Lt[col * kTcLd + k] = (k < nb && col < a.LW) ? a.stats[(size_t)(cb + k) * a.stride + col] : 0.0;
+    }
+    for (int t = threadIdx.x; t < 32 * Jm; t += blockDim.x) {
+      const int k = t / Jm, c = t % Jm;
+      sa[t] = k < nb ? __ldg(a.A + (size_t)a.chunks[cb + k].row * a.ld + c) : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < a.NT * 8 * 32; t += blockDim.x) {
+      const int col = t >> 5, k = t & 31;
+      const int mp = rmap[col];
+      double v = 0.0;
+      if (mp >= 0) {
+        const double* ak = sa + k * Jm;
+        const int kind = mp >> 16;
+        if (kind == 0) v = ak[(mp >> 8) & 255] * ak[mp & 255];
+        else if (kind == 1) v = ak[mp & 255];
+        else v = ak[mp & 255] * ak[mp & 255];
+      }
+      Rt[col * kTcLd + k] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kTcTilesPerWarp; ++i) {
+      const int tile = warp + kTcWarps * i;
+      if (tile < ntiles) {
+        const int mt = tile / a.NT, nt = tile % a.NT;
+        const double* la = Lt + (8 * mt + g) * kTcLd + tq;
+        const double* rb = Rt + (8 * nt + g) * kTcLd + tq;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma884(acc[i][0], acc[i][1], la[4 * kk], rb[4 * kk]);
+      }
+    }
+  }
+  double* out = a.partial + (size_t)blockIdx.x * ntiles * 64;
+#pragma unroll
+  for (int i = 0; i < kTcTilesPerWarp; ++i) {
+    const int tile = warp + kTcWarps * i;
+    if (tile < ntiles) {
+      out[tile * 64 + lane * 2] = acc[i][0];
+      out[tile * 64 + lane * 2 + 1] = acc[i][1];
+    }
+  }
+}
+
+// raw[j] = sum over a group of CTA partials (fixed order); grid.y = groups
+__global__ void k_gemm_reduce1(const double* partial, int nparts, int n, int groups, double* raw) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int per = (nparts + groups - 1) / groups;
+  const int p0 = blockIdx.y * per, p1 = min(nparts, p0 + per);
+  double s = 0.0;
+  for (int p = p0; p < p1; ++p) s += partial[(size_t)p * n + j];
+  raw[(size_t)blockIdx.y * n + j] = s;
+}
+
+// out = [T | C] (kind 0) or [C | D] (kind 1) from the group sums of the tile layout
+__global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, int nf, int Jm, int NT,
+                               double* out) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int NAm = Jm * (Jm + 1) / 2;
+  const int NS = nf * (nf + 1) / 2;
+  int row, col, nout;
+  if (kind == 0) {
+    nout = NS * NAm + nf * Jm;
+    if (o >= nout) return;
+    if (o < NS * NAm) {
+      row = o / NAm;
+      col = o % NAm;
+    } else {
+      row = NS + (o - NS * NAm) / Jm;
+      col = NAm + (o - NS * NAm) % Jm;
+    }
+  } else {
+    nout = 2 * nf * Jm;
+    if (o >= nout) return;
+    const int q = o % (nf * Jm);
+    const int hi = o / (nf * Jm);
+    row = hi * nf + q / Jm;
+    col = hi * Jm + q % Jm;
+  }
+  const int j = ((row >> 3) * NT + (col >> 3)) * 64 + (row & 7) * 8 + (col & 7);
+  double s = 0.0;
+  for (int gq = 0; gq < groups; ++gq) s += raw[(size_t)gq * n + j];
+  out[o] = s;
+}
+
+// Sequential Gauss-Seidel over the block's cells.  The CTA loads [T | C],
+// the block's core values and masks into shared memory and expands the dense
+// cell Gram H (nq x nq, H_qq' = T[{f,f'}][{c,c'}]); then one warp runs the
+// nq sequential steps, each a handful of shared-memory reads plus one
+// coalesced row update of the remaining cells' c.
 __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, int Jm, const uint32_t* fib,
                                                     double* core, const uint8_t* core_mask, int reg,
                                                     double lambda, double* dg_out) {
@@ -390,46 +544,55 @@ __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, in
   const int NAm = Jm * (Jm + 1) / 2;
   const int nT = nf * (nf + 1) / 2 * NAm;
   const int nq = nf * Jm;
-  double* T = sm;
-  double* cc = sm + nT;
-  double* gv = cc + nq;
-  double* mk = gv + nq;
-  for (int t = threadIdx.x; t < nT + nq; t += blockDim.x) sm[t] = tc[t];
+  double* H = sm;             // nq x nq
+  double* cc = H + nq * nq;   // nq
+  double* gv = cc + nq;       // nq
+  double* mk = gv + nq;       // nq
+  double* rd = mk + nq;       // nq: 1 / (H_qq + lambda) (LF) or 1 / (2 H_qq) (L1)
+  for (int t = threadIdx.x; t < nq * nq; t += blockDim.x) {
+    const int q = t / nq, q2 = t % nq;
+    const int f = q / Jm, c = q % Jm, f2 = q2 / Jm, c2 = q2 % Jm;
+    const int ps = f <= f2 ? tri(f, f2, nf) : tri(f2, f, nf);
+    const int pa = c <= c2 ? tri(c, c2, Jm) : tri(c2, c, Jm);
+    H[t] = tc[ps * NAm + pa];
+  }
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    cc[q] = tc[nT + q];
     const int lin = (int)fib[q / Jm] * Jm + q % Jm;
     gv[q] = core[lin];
     mk[q] = core_mask[lin] ? 1.0 : 0.0;
+    // the denominators do not depend on the sweep state: invert them in
+    // parallel, off the sequential critical path
+    const int f = q / Jm, c = q % Jm;
+    const double hqq = tc[tri(f, f, nf) * NAm + tri(c, c, Jm)];
+    const double den = reg == 0 ? hqq + lambda : 2.0 * hqq;
+    rd[q] = den != 0.0 ? 1.0 / den : 0.0;
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   for (int q = 0; q < nq; ++q) {
-    const int f = q / Jm, c = q % Jm;
     double dg = 0.0;
     if (mk[q] == 0.0) {
-      const double hqq = T[tri(f, f, nf) * NAm + tri(c, c, Jm)];
+      const double hqq = H[q * nq + q];
       const double g_old = gv[q];
       const double num = cc[q] + g_old * hqq;
       const double den = hqq;
       double g_new = g_old;
+      const double r = rd[q];
       if (reg == 0) {
-        if (den + lambda != 0.0) g_new = num / (den + lambda);
+        if (den + lambda != 0.0) g_new = num * r;
       } else {
         const double g = -2.0 * num;
-        const double d = 2.0 * den;
-        if (d != 0.0) g_new = g > lambda ? (lambda - g) / d : (g < -lambda ? -(lambda + g) / d : 0.0);
+        if (2.0 * den != 0.0) g_new = g > lambda ? (lambda - g) * r : (g < -lambda ? -(lambda + g) * r : 0.0);
       }
       if (g_new != g_old) dg = g_new - g_old;
       if (lane == 0) gv[q] = g_new;
     }
     if (lane == 0) dg_out[q] = dg;
     if (dg != 0.0) {
-      for (int q2 = q + 1 + lane; q2 < nq; q2 += 32) {
-        const int f2 = q2 / Jm, c2 = q2 % Jm;
-        const int ps = f <= f2 ? tri(f, f2, nf) : tri(f2, f, nf);
-        const int pa = c <= c2 ? tri(c, c2, Jm) : tri(c2, c, Jm);
-        cc[q2] -= dg * T[ps * NAm + pa];
-      }
+      const double* hr = H + q * nq;
+      for (int q2 = q + 1 + lane; q2 < nq; q2 += 32) cc[q2] = fma(-dg, hr[q2], cc[q2]);
     }
     __syncwarp();
   }
@@ -611,6 +774,39 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
   ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)g.nout);
   g.partial = c.d_gemm_part;
   ProfScope ps(c, kProfCoreGemm);
+  GemmTcArgs t{};
+  t.stats = g.stats;
+  t.stride = stride;
+  t.chunks = g.chunks;
+  t.nchunks = g.nchunks;
+  t.A = g.A;
+  t.ld = g.ld;
+  t.Jm = Jm;
+  t.nf = nf;
+  t.kind = kind;
+  t.LW = kind == 0 ? g.NS + nf : 2 * nf;
+  t.RW = kind == 0 ? g.NAm + Jm : 2 * Jm;
+  t.MT = (t.LW + 7) / 8;
+  t.NT = (t.RW + 7) / 8;
+  const int ntiles = t.MT * t.NT;
+  if (ntiles <= kTcWarps * kTcTilesPerWarp) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    const int nparts = std::max(1, std::min<int>(2 * sms, (g.nchunks + 31) / 32));
+    const int n = ntiles * 64;
+    const int groups = 16;
+    ensure(c, &c.d_gemm_part, &c.gemm_part_cap, (size_t)nparts * n + (size_t)groups * n);
+    t.partial = c.d_gemm_part;
+    double* raw = c.d_gemm_part + (size_t)nparts * n;
+    const size_t sm = ((size_t)(t.MT + t.NT) * 8 * kTcLd + 32 * Jm) * sizeof(double) + (size_t)t.NT * 8 * sizeof(int);
+    check(cudaFuncSetAttribute(k_core_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gemm smem");
+    k_core_gemm_tc<<<nparts, kTcWarps * 32, sm, c.stream>>>(t);
+    k_gemm_reduce1<<<dim3((n + 255) / 256, groups), 256, 0, c.stream>>>(t.partial, nparts, n, groups, raw);
+    k_gemm_reduce2<<<(g.nout + 255) / 256, 256, 0, c.stream>>>(raw, n, groups, kind, nf, Jm, t.NT, c.d_gemm_out);
+    count_launch(3);
+    check(cudaGetLastError(), "core gemm (tensor cores)");
+    return g.nout;
+  }
   const int NSp = (g.NS + 3) & ~3, NAp = (g.NAm + 3) & ~3;
   const size_t sm = (size_t)kGemmBatch * (NSp + NAp + 2 * kFMax + Jm) * sizeof(double);
   check(cudaFuncSetAttribute(k_core_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gemm smem");
@@ -633,8 +829,9 @@ void upload_fibers(Ctx& c, const Blocks& b) {
 void core_sweep(Ctx& c, int reg, double lambda) {
   const int m = c.N - 1, Jm = c.ranks[m];
   // r = x - B(alpha) for the model after the factor updates
-  // (the reference rebuilds its reconstruction cache here, updates.hpp:190-192)
-  compute_residual(c);
+  // (the reference rebuilds its reconstruction cache here, updates.hpp:190-192);
+  // already fresh when the last factor mode emitted it
+  if (!c.r_fresh) compute_residual(c);
   const void* sops = structured_ops(c);
   const int F = sops ? c.ranks[c.N - 2] : pick_block(c);
   const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
@@ -652,8 +849,8 @@ void core_sweep(Ctx& c, int reg, double lambda) {
     const int nf = b.len[bi];
     block_gemm(c, nf, 0, stride);
     ProfScope ps(c, kProfCoreSolve);
-    const int NAm = Jm * (Jm + 1) / 2;
-    const size_t sm = ((size_t)nf * (nf + 1) / 2 * NAm + 3 * (size_t)nf * Jm) * sizeof(double);
+    const size_t nq = (size_t)nf * Jm;
+    const size_t sm = (nq * nq + 4 * nq) * sizeof(double);
     check(cudaFuncSetAttribute(k_core_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "solve smem");
     k_core_solve<<<1, 256, sm, c.stream>>>(c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core,
                                            c.d_core_mask, reg, lambda, c.d_dg);
@@ -663,6 +860,7 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   c.sum_sq = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);
   c.re = std::sqrt(c.sum_sq) / c.x_norm;
   c.r_valid = true;
+  c.r_fresh = true;
 }
 
 void core_responsibilities(Ctx& c) {

@@ -283,6 +283,14 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
       }
       slot += nch;
     }
+    std::vector<Chunk> hchunks;
+    for (const Chunk& ch : chunks)
+      if (ch.slot != kLight) hchunks.push_back(ch);
+    md.nheavy_chunks = (uint32_t)hchunks.size();
+    md.d_heavy_chunks = static_cast<Chunk*>(dalloc(c, std::max<size_t>(1, hchunks.size()) * sizeof(Chunk)));
+    if (!hchunks.empty())
+      check(cudaMemcpy(md.d_heavy_chunks, hchunks.data(), hchunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice),
+            "heavy chunks");
     md.nchunks = (uint32_t)chunks.size();
     md.nheavy = (uint32_t)heavy.size();
     md.nslots = slot;
@@ -314,7 +322,7 @@ static cudaError_t run_rows(Ctx& c, const RowPassArgs& a, int kind, uint32_t nch
   return launch_rowpass_generic(a, kind, nchunks, c.stream);
 }
 
-void update_factor_mode(Ctx& c, int mode, int reg, double lambda) {
+void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resid) {
   RowPassArgs a = row_args(c, mode);
   const int J = c.ranks[mode];
   a.reg = reg;
@@ -322,11 +330,34 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda) {
   a.stride_na = J * (J + 1) / 2 + J;
   ensure(c, &c.d_heavy_part, &c.heavy_part_cap, (size_t)c.modes[mode].nslots * a.stride_na + 1);
   a.heavy_out = c.d_heavy_part;
-  ProfScope ps(c, kProfFactor);
-  check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
-  if (reg == 1) l1_empty_rows(c, mode, lambda);
+  // the last mode's update can emit the residual of the updated model for the
+  // core sweep (rank-specialised kernels only; see fused_residual)
+  const bool fuse = fuse_resid && mode == c.N - 1 && c.ops && !c.force_generic;
+  a.fuse_resid = fuse ? 1 : 0;
+  a.r_out = c.d_r;
+  {
+    ProfScope ps(c, kProfFactor);
+    check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
+    if (reg == 1) l1_empty_rows(c, mode, lambda);
+  }
   c.r_valid = false;
+  c.r_fresh = false;
   c.table_valid = false;
+  if (fuse) {
+    const ModeData& md = c.modes[mode];
+    if (md.nheavy_chunks > 0) {
+      // heavy rows were solved by k_heavy: their residual needs a second pass
+      RowPassArgs b = row_args(c, mode);
+      b.csf.chunks = md.d_heavy_chunks;
+      b.csf.nchunks = md.nheavy_chunks;
+      b.r_out = c.d_r;
+      ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, md.nchunks + 1);
+      b.chunk_out = c.d_chunk_sum;
+      ProfScope ps(c, kProfResid);
+      check(run_rows(c, b, kResid, b.csf.nchunks), "heavy-row residual");
+    }
+    c.r_fresh = true;
+  }
 }
 
 void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, int reg, double lambda) {
@@ -391,6 +422,7 @@ void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, 
   cudaFree(dhv);
   cudaFree(dem);
   c.r_valid = false;
+    c.r_fresh = false;
   c.table_valid = false;
 }
 
@@ -408,6 +440,7 @@ void compute_residual(Ctx& c) {
   c.sum_sq = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);
   c.re = std::sqrt(c.sum_sq) / c.x_norm;
   c.r_valid = true;
+  c.r_fresh = true;
 }
 
 void responsibilities(Ctx& c) {
@@ -491,6 +524,7 @@ void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const do
   }
   check(cudaStreamSynchronize(c.stream), "set_model");
   c.r_valid = false;
+    c.r_fresh = false;
   c.table_valid = false;
 }
 
@@ -645,6 +679,7 @@ int vest_ctx_destroy(vest_ctx* h) {
     cudaFree(md.d_chunks);
     cudaFree(md.d_heavy);
     cudaFree(md.d_empty);
+    cudaFree(md.d_heavy_chunks);
     cudaFree(c.d_factor[n]);
     cudaFree(c.d_fmask[n]);
     cudaFree(c.d_resp_f[n]);
@@ -748,7 +783,7 @@ int vest_update_all_factors(vest_ctx* h, int reg, double lambda) {
     check_reg(reg);
     set_dev(c);
     sync_const_core(c);
-    for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda);
+    for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda, false);
     check(cudaStreamSynchronize(c.stream), "factors");
   });
 }
@@ -760,7 +795,7 @@ int vest_update_factor_mode(vest_ctx* h, int mode, int reg, double lambda) {
     if (mode < 0 || mode >= c.N) throw ArgError{"mode out of range"};
     set_dev(c);
     sync_const_core(c);
-    update_factor_mode(c, mode, reg, lambda);
+    update_factor_mode(c, mode, reg, lambda, false);
     check(cudaStreamSynchronize(c.stream), "factor mode");
   });
 }
@@ -816,7 +851,7 @@ int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
     if (c.x_norm == 0.0) throw ArgError{"zero-norm tensor"};
     set_dev(c);
     sync_const_core(c);
-    for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda);
+    for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda, true);
     core_sweep(c, reg, lambda);
     c.table_valid = false;
     if (re) *re = c.re;
@@ -901,6 +936,7 @@ int vest_prune_step(vest_ctx* h, double pr, const double* core_resp, const doubl
     }
     prune(c, pr, counts);
     c.r_valid = false;
+    c.r_fresh = false;
     c.table_valid = false;
   });
 }
@@ -919,6 +955,7 @@ int vest_normalize_columns(vest_ctx* h) {
     set_dev(c);
     normalize_columns(c);
     c.r_valid = false;
+    c.r_fresh = false;
     c.table_valid = false;
   });
 }

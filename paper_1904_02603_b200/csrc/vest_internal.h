@@ -75,6 +75,7 @@ struct RowPassArgs {
   double* resp_out;     // I x J (unpadded)
   double* r_out;        // residual in CSF order
   double* chunk_out;    // per-chunk sum of squared residuals
+  int fuse_resid;       // kStats on the last mode: write r = x - B(alpha) for light rows
 };
 
 struct ModeData {
@@ -85,7 +86,8 @@ struct ModeData {
   Chunk* d_chunks = nullptr;
   Heavy* d_heavy = nullptr;
   uint32_t* d_empty = nullptr;  // rows with no entries
-  uint32_t nchunks = 0, nheavy = 0, nslots = 0, nempty = 0;
+  Chunk* d_heavy_chunks = nullptr;  // the chunks of heavy rows (residual pass after their solve)
+  uint32_t nchunks = 0, nheavy = 0, nslots = 0, nempty = 0, nheavy_chunks = 0;
   std::vector<uint64_t> h_offsets;
 };
 
@@ -130,7 +132,8 @@ struct Ctx {
   std::vector<uint8_t> h_core_mask;
 
   double* d_r = nullptr;  // CSF order of mode N-1
-  bool r_valid = false;
+  bool r_valid = false;   // r, sum_sq and re match the current model
+  bool r_fresh = false;   // r matches the current model (sum_sq not computed)
   double sum_sq = 0.0, re = 0.0;
 
   double* d_resp_core = nullptr;
@@ -187,7 +190,7 @@ cudaError_t launch_coo_recon_generic(const DevModel& m, const uint32_t* coords, 
 void sync_const_core(Ctx& c);  // copy d_core into every TU's constant-bank core
 
 void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values);
-void update_factor_mode(Ctx& c, int mode, int reg, double lambda);
+void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resid);
 void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, int reg, double lambda);
 void compute_residual(Ctx& c);  // fresh r = x - B(alpha), sum_sq, re
 void core_sweep(Ctx& c, int reg, double lambda);

@@ -27,6 +27,14 @@ struct ConstCore {
   __device__ __forceinline__ double2 pair(int lin) const { return c_core_pairs[lin >> 1]; }  // lin even
 };
 
+// A core held in shared memory (broadcast LDS reads): the fused residual's
+// v = G x_m a, and the VEST_CORE_SMEM experiment.
+struct SmemCore {
+  const double* p;
+  __device__ __forceinline__ double operator()(int lin) const { return p[lin]; }
+  __device__ __forceinline__ double2 pair(int lin) const { return reinterpret_cast<const double2*>(p)[lin >> 1]; }
+};
+
 template <int B, int E, class F>
 __device__ __forceinline__ void static_for(F&& f) {
   if constexpr (B < E) {
@@ -55,6 +63,7 @@ struct StaticPolicy {
 #define VEST_CORE_SMEM 0
 #endif
   static constexpr bool kSmemCore = VEST_CORE_SMEM && S::G() <= 1024;
+  using Shape = S;
   static constexpr int N = S::N;
   static constexpr int MAXJ = S::MAXJ;
   static constexpr int JN = S::J(MODE);
@@ -238,6 +247,47 @@ constexpr int stage_words() {
 // X^T X accumulated with DMMA, so the DFMA pipe only runs the contraction);
 // generic ranks accumulate "slots" (pair (t, j) owned by lane s % 32) over
 // shared-memory staged rows.
+// Residual of a freshly solved row of the last mode m (fuse_resid): with the
+// new row a = A_m[s, :], B(alpha_e) = sum_{beta<m} v[beta] prod_{k<m} u_k[beta_k]
+// where v = G x_m a (|G| / J_m values, computed once per row into shared
+// memory), so each entry costs the (N-1)-mode contraction instead of a full
+// reconstruction.  Writes r (CSF order of mode m) for the chunk's entries.
+template <class P>
+__device__ __forceinline__ void fused_residual(const RowPassArgs& a, const Chunk& ch, double* v, int lane) {
+  if constexpr (P::kStatic) {
+    using S = typename P::Shape;
+    if constexpr (S::N >= 3) {
+      using Q = PrefixShape<S>;
+      constexpr int m = S::N - 1;
+      constexpr int Jm = S::J(m);
+      constexpr int NV = S::G() / Jm;
+      const double* arow = a.m.factor[m] + (size_t)ch.row * a.m.ld[m];
+      double an[Jm];
+#pragma unroll
+      for (int c = 0; c < Jm; ++c) an[c] = arow[c];
+      for (int p = lane; p < NV; p += 32) {
+        double t = 0.0;
+#pragma unroll
+        for (int c = 0; c < Jm; ++c) t = fma(ConstCore{}(p * Jm + c), an[c], t);
+        v[p] = t;
+      }
+      __syncwarp();
+      const SmemCore gv{v};
+      for (uint32_t pos = ch.beg + lane; pos < ch.end; pos += 32) {
+        double u[1][Q::N][Q::MAXJ];
+        static_for<0, Q::N>([&](auto kc) {
+          constexpr int k = decltype(kc)::value;
+          constexpr int ld = (S::J(k) + 1) & ~1;
+          load_row<S::J(k)>(a.m.factor[k] + (size_t)__ldg(a.csf.oc[k] + pos) * ld, u[0][k]);
+        });
+        double rec[1];
+        trailingN<Q, 0, 1>(gv, u, 0, rec);
+        a.r_out[pos] = __ldg(a.csf.val + pos) - rec[0];
+      }
+    }
+  }
+}
+
 #ifndef VEST_ROW_MINB
 #define VEST_ROW_MINB 2
 #endif
@@ -437,6 +487,12 @@ __global__ void __launch_bounds__(kRowWarps * 32, VEST_ROW_MINB) k_rowpass(RowPa
       __syncwarp();
       solve_row(J, a.reg, a.lambda, Gs, xd, a.m.factor[mode] + (size_t)ch.row * a.m.ld[mode],
                 a.m.fmask[mode] + (size_t)ch.row * J, lane);
+      if constexpr (P::kStatic) {
+        if (a.fuse_resid) {
+          __syncwarp();
+          fused_residual<P>(a, ch, wsm + 128, lane);
+        }
+      }
     }
   } else if constexpr (KIND == kResp) {
 #pragma unroll
