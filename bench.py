@@ -202,7 +202,7 @@ def workload_config(n):
     return {"workload": "config2: 3-mode 100k^3, 10M uniform distinct entries, fp64 U[0,1), ranks 10x10x10, "
                         "lambda 0.01 LF; step = update_all_factors + update_core + RE",
             "nnz": CONFIG2["nnz"], "ranks": CONFIG2["ranks"], "dims": CONFIG2["dims"],
-            "parallelism": f"replicas x{n}" if n > 1 else "single",
+            "parallelism": f"rows sharded x{n} (NCCL)" if n > 1 else "single",
             "l2": "inputs larger than L2 (per-mode CSF 600 MB vs 126 MB L2)"}
 
 
@@ -221,7 +221,13 @@ def run_ours(args, rank, world, local_rank):
     cfg = CONFIG2
     coords, vals = synth(cfg["dims"], cfg["nnz"], cfg["data_seed"])
     x = st.SparseTensor(cfg["dims"], coords, vals)
-    dev = st.Device(x, cfg["ranks"], local_rank)
+    if world > 1:
+        # rows of every mode sharded by nnz-balanced ranges; NCCL exchanges
+        # (paper_1904_02603_b200/sharded.py)
+        from paper_1904_02603_b200 import sharded as sh
+        dev = sh.ShardDevice(x, cfg["ranks"], rank, world, sh.TorchComm("cuda"), local_rank)
+    else:
+        dev = st.Device(x, cfg["ranks"], local_rank)
     assert dev.specialised(), "rank-specialised kernels expected for config 2"
     dev.init_random(cfg["seed"])
     stream = torch.cuda.ExternalStream(dev.stream(), device=torch.device("cuda", local_rank))
@@ -258,7 +264,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = cfg["nnz"] * args.steps * world / (ms * 1e-3)
+    value = cfg["nnz"] * args.steps / (ms * 1e-3)  # whole job: the N ranks share the nnz
 
     # ---- prune event (timed separately; not an iteration)
     torch.cuda.synchronize()
@@ -297,7 +303,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = cfg["nnz"] * e2e_steps * world / e2e_s
+    e2e_value = cfg["nnz"] * e2e_steps / e2e_s
 
     if rank != 0:
         if dist is not None:
@@ -340,7 +346,7 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"one CD iteration of config2 shape with {SAMPLE_NNZ} entries ({sec:.1f} s)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config 2 shape)",
         "config": workload_config(world),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

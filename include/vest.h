@@ -70,6 +70,32 @@ int vest_ctx_force_generic(vest_ctx* ctx, int on);
 /* Tuning: fibers per core-sweep block (0 = default). */
 int vest_ctx_set_core_block(vest_ctx* ctx, int fibers);
 
+/* ---------------------------------------------------------------- sharding --
+ * Multi-GPU (one process per GPU): a shard context owns the rows
+ * [row_lo[n], row_hi[n]) of every mode n (nnz-balanced ranges from
+ * vest_partition_rows).  It holds the whole tensor and full model replicas but
+ * only updates / traverses its own rows; the exchange points call the
+ * communication hooks below, all on the context stream:
+ *   - after each factor mode: allgather_rows(mode, factor, ld)  (all ranks end
+ *     with every updated row);
+ *   - per core block: allreduce_sum of the block statistics [T | C];
+ *   - the residual sum of squares, and core-responsibility statistics:
+ *     allreduce_sum;
+ *   - factor responsibilities: allgather_rows(mode, table, J).
+ * Every rank then runs the identical block solves and prune selection. */
+typedef struct vest_comm {
+  void* user;
+  int (*allreduce_sum)(void* user, double* p, uint64_t n, void* stream);
+  int (*allgather_rows)(void* user, int mode, double* base, uint64_t ld, void* stream);
+} vest_comm;
+int vest_ctx_create_shard(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                          const double* values, const uint64_t* ranks, int device,
+                          const uint64_t* row_lo, const uint64_t* row_hi, vest_ctx** out);
+/* Install (or clear with NULL) the communication hooks. */
+int vest_ctx_set_comm(vest_ctx* ctx, const vest_comm* comm);
+/* Observed entries in this context's rows of `mode`. */
+uint64_t vest_ctx_local_nnz(vest_ctx* ctx, int mode);
+
 /* ------------------------------------------------------------------ model --
  * init_random (tucker_model.hpp:88-108): mt19937_64(seed), U[0,1) draws in
  * the documented order (factor 0 row-major, ..., factor N-1, then core). */

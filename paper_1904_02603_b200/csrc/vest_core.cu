@@ -847,7 +847,8 @@ void core_sweep(Ctx& c, int reg, double lambda) {
     run_pass(c, sops, b, bi - 1, last ? -1 : bi, last ? 2 : 0, stride);
     if (last) break;
     const int nf = b.len[bi];
-    block_gemm(c, nf, 0, stride);
+    const int nout = block_gemm(c, nf, 0, stride);
+    comm_allreduce(c, c.d_gemm_out, (uint64_t)nout);  // block statistics over the shards
     ProfScope ps(c, kProfCoreSolve);
     const size_t nq = (size_t)nf * Jm;
     const size_t sm = (nq * nq + 4 * nq) * sizeof(double);
@@ -880,7 +881,8 @@ void core_responsibilities(Ctx& c) {
   for (int bi = 0; bi < (int)b.start.size(); ++bi) {
     run_pass(c, sops, b, -1, bi, 1, stride);
     const int nf = b.len[bi];
-    block_gemm(c, nf, 1, stride);
+    const int nout = block_gemm(c, nf, 1, stride);
+    comm_allreduce(c, c.d_gemm_out, (uint64_t)nout);
     k_core_resp_final<<<(nf * Jm + 127) / 128, 128, 0, c.stream>>>(
         c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core, c.d_core_mask, c.sum_sq, c.x_norm, c.re,
         c.d_resp_core);

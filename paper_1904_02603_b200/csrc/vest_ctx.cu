@@ -30,6 +30,17 @@ void check(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw CudaError{e, where};
 }
 
+void comm_allreduce(Ctx& c, double* p, uint64_t n) {
+  if (!c.comm.allreduce_sum) return;
+  if (c.comm.allreduce_sum(c.comm.user, p, n, (void*)c.stream) != 0) throw RtError{"allreduce_sum hook failed"};
+}
+
+void comm_allgather_rows(Ctx& c, int mode, double* base, uint64_t ld) {
+  if (!c.comm.allgather_rows) return;
+  if (c.comm.allgather_rows(c.comm.user, mode, base, ld, (void*)c.stream) != 0)
+    throw RtError{"allgather_rows hook failed"};
+}
+
 void* dalloc(Ctx& c, size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
@@ -265,7 +276,8 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
     std::vector<Heavy> heavy;
     std::vector<uint32_t> empty;
     uint32_t slot = 0;
-    for (uint64_t i = 0; i < c.dims[n]; ++i) {
+    c.local_nnz[n] = md.h_offsets[c.row_hi[n]] - md.h_offsets[c.row_lo[n]];
+    for (uint64_t i = c.row_lo[n]; i < c.row_hi[n]; ++i) {  // this context's rows
       const uint64_t b = md.h_offsets[i], e = md.h_offsets[i + 1], len = e - b;
       if (len == 0) {
         empty.push_back((uint32_t)i);
@@ -358,6 +370,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
     }
     c.r_fresh = true;
   }
+  comm_allgather_rows(c, mode, c.d_factor[mode], (uint64_t)c.ld[mode]);
 }
 
 void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, int reg, double lambda) {
@@ -465,6 +478,7 @@ void responsibilities(Ctx& c) {
     ensure(c, &c.d_heavy_part, &c.heavy_part_cap, (size_t)c.modes[n].nslots * a.stride_na + 1);
     a.heavy_out = c.d_heavy_part;
     check(run_rows(c, a, kResp, a.csf.nchunks), "factor resp");
+    comm_allgather_rows(c, n, c.d_resp_f[n], (uint64_t)c.ranks[n]);
   }
   check(cudaStreamSynchronize(c.stream), "resp sync");
   c.table_valid = true;
@@ -598,8 +612,39 @@ const char* vest_last_error(void) { return g_err.c_str(); }
 const char* vest_version(void) { return "vest-b200 0.1 (sm_100a)"; }
 uint64_t vest_launch_count(void) { return launch_counter(); }
 
+static int create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords, const double* values,
+                       const uint64_t* ranks, int device, const uint64_t* row_lo, const uint64_t* row_hi,
+                       vest_ctx** out);
+
 int vest_ctx_create(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords, const double* values,
                     const uint64_t* ranks, int device, vest_ctx** out) {
+  return create_impl(order, dims, nnz, coords, values, ranks, device, nullptr, nullptr, out);
+}
+
+int vest_ctx_create_shard(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                          const double* values, const uint64_t* ranks, int device, const uint64_t* row_lo,
+                          const uint64_t* row_hi, vest_ctx** out) {
+  return create_impl(order, dims, nnz, coords, values, ranks, device, row_lo, row_hi, out);
+}
+
+int vest_ctx_set_comm(vest_ctx* h, const vest_comm* comm) {
+  Ctx& c = h->c;
+  c.comm = CommHooks{};
+  if (comm) {
+    c.comm.user = comm->user;
+    c.comm.allreduce_sum = comm->allreduce_sum;
+    c.comm.allgather_rows = comm->allgather_rows;
+  }
+  return VEST_OK;
+}
+
+uint64_t vest_ctx_local_nnz(vest_ctx* h, int mode) {
+  return (mode >= 0 && mode < h->c.N) ? h->c.local_nnz[mode] : 0;
+}
+
+static int create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords, const double* values,
+                       const uint64_t* ranks, int device, const uint64_t* row_lo, const uint64_t* row_hi,
+                       vest_ctx** out) {
   *out = nullptr;
   auto* h = new vest_ctx();
   Ctx& c = h->c;
@@ -619,6 +664,9 @@ int vest_ctx_create(int order, const uint64_t* dims, uint64_t nnz, const uint32_
     c.nnz = nnz;
     c.G = 1;
     for (int k = 0; k < order; ++k) {
+      c.row_lo[k] = row_lo ? row_lo[k] : 0;
+      c.row_hi[k] = row_hi ? row_hi[k] : dims[k];
+      if (c.row_lo[k] > c.row_hi[k] || c.row_hi[k] > dims[k]) throw ArgError{"shard row range out of bounds"};
       c.dims[k] = dims[k];
       c.ranks[k] = (int)ranks[k];
       c.G *= (int)ranks[k];

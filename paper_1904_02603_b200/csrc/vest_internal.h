@@ -107,8 +107,17 @@ struct ProfEvent {
   int fam;
 };
 
+struct CommHooks {
+  void* user = nullptr;
+  int (*allreduce_sum)(void* user, double* p, uint64_t n, void* stream) = nullptr;
+  int (*allgather_rows)(void* user, int mode, double* base, uint64_t ld, void* stream) = nullptr;
+};
+
 struct Ctx {
   int device = 0;
+  uint64_t row_lo[VEST_MAXN] = {}, row_hi[VEST_MAXN] = {};  // owned rows per mode
+  uint64_t local_nnz[VEST_MAXN] = {};
+  CommHooks comm;
   bool prof_on = false;
   std::vector<ProfEvent> prof_events;
   double prof_ms[8] = {};
@@ -199,6 +208,8 @@ void prune(Ctx& c, double pr, uint64_t* counts);
 void sparsity(Ctx& c, double* zero_frac, double* masked_frac);
 void normalize_columns(Ctx& c);
 double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n);
+void comm_allreduce(Ctx& c, double* p, uint64_t n);
+void comm_allgather_rows(Ctx& c, int mode, double* base, uint64_t ld);
 
 // RAII timing scope for one kernel family (no-op unless profiling is on).
 enum ProfFamily { kProfFactor = 0, kProfCorePass, kProfCoreGemm, kProfCoreSolve, kProfResid, kProfResp, kProfPrune };

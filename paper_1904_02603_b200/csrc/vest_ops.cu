@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(1024) k_sum(const double* in, uint64_t n, doub
 double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n) {
   k_sum<<<1, 1024, 0, c.stream>>>(d_in, n, c.d_small);
   count_launch();
+  comm_allreduce(c, c.d_small, 1);  // residual sums are global over the shards
   check(cudaMemcpyAsync(c.h_small, c.d_small, sizeof(double), cudaMemcpyDeviceToHost, c.stream),
         "sum readback");
   check(cudaStreamSynchronize(c.stream), "sum sync");
