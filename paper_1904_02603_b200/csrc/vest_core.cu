@@ -438,19 +438,41 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
 #pragma unroll
   for (int i = 0; i < kTcTilesPerWarp; ++i) acc[i][0] = acc[i][1] = 0.0;
   const int Jm = a.Jm;
-  for (uint32_t cb = c0; cb < c1; cb += 32) {
-    const int nb = min(32u, c1 - cb);
-    __syncthreads();
-    // statistics rows are contiguous per chunk: read row-major (coalesced),
-    // write transposed
-    const int LWp = a.MT * 8;
-    for (int t = threadIdx.x; t < LWp * 32; t += blockDim.x) {
+  const int LWp = a.MT * 8;
+  // software pipeline: the next batch's statistics rows and last-mode factor
+  // rows are loaded into registers while the current batch runs on DMMA
+  constexpr int kLPer = 12, kAPer = 2;  // per-thread staging share (LWp*32 <= 3072, 32*Jm <= 512)
+  double lv[kLPer], av[kAPer];
+  auto prefetch = [&](uint32_t cb) {
+    const int nb = (int)min(32u, c1 - cb);
+#pragma unroll
+    for (int i = 0; i < kLPer; ++i) {
+      const int t = threadIdx.x + i * blockDim.x;
       const int k = t / LWp, col = t - k * LWp;
-      Lt[col * kTcLd + k] = (k < nb && col < a.LW) ? a.stats[(size_t)(cb + k) * a.stride + col] : 0.0;
+      lv[i] = (t < LWp * 32 && k < nb && col < a.LW) ? a.stats[(size_t)(cb + k) * a.stride + col] : 0.0;
     }
-    for (int t = threadIdx.x; t < 32 * Jm; t += blockDim.x) {
-      const int k = t / Jm, c = t % Jm;
-      sa[t] = k < nb ? __ldg(a.A + (size_t)a.chunks[cb + k].row * a.ld + c) : 0.0;
+#pragma unroll
+    for (int i = 0; i < kAPer; ++i) {
+      const int t = threadIdx.x + i * blockDim.x;
+      const int k = t / Jm, c = t - (t / Jm) * Jm;
+      av[i] = (t < 32 * Jm && k < nb) ? __ldg(a.A + (size_t)a.chunks[cb + k].row * a.ld + c) : 0.0;
+    }
+  };
+  if (c0 < c1) prefetch(c0);
+  for (uint32_t cb = c0; cb < c1; cb += 32) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kLPer; ++i) {
+      const int t = threadIdx.x + i * blockDim.x;
+      if (t < LWp * 32) {
+        const int k = t / LWp, col = t - k * LWp;
+        Lt[col * kTcLd + k] = lv[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kAPer; ++i) {
+      const int t = threadIdx.x + i * blockDim.x;
+      if (t < 32 * Jm) sa[t] = av[i];
     }
     __syncthreads();
     for (int t = threadIdx.x; t < a.NT * 8 * 32; t += blockDim.x) {
@@ -467,6 +489,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
       Rt[col * kTcLd + k] = v;
     }
     __syncthreads();
+    if (cb + 32 < c1) prefetch(cb + 32);
 #pragma unroll
     for (int i = 0; i < kTcTilesPerWarp; ++i) {
       const int tile = warp + kTcWarps * i;
@@ -628,7 +651,10 @@ __global__ void k_fill(double* p, size_t n, double v) {
 const void* find_core_ops(int N, const int* J);
 cudaError_t core_pass_structured(const void* ops, const DevModel& m, const DevCSF& csf, double* r, int prev_p,
                                  const double* prev_dg, int cur_p, int kind, double* stats, int stride,
-                                 double* chunk_sq, cudaStream_t s);
+                                 double* chunk_sq, const double* U, const double* W, uint64_t wstride,
+                                 cudaStream_t s);
+cudaError_t core_pack_structured(const void* ops, const DevModel& m, const DevCSF& csf, uint64_t p0, uint64_t p1,
+                                 double* U, double* W, uint64_t wstride, cudaStream_t s);
 
 namespace {
 
@@ -730,7 +756,7 @@ void run_pass(Ctx& c, const void* sops, const Blocks& b, int prev, int cur, int 
     ProfScope ps(c, kProfCorePass);
     check(core_pass_structured(sops, c.model_view(), c.csf_view(m), c.d_r, prev >= 0 ? b.prefix[prev] : -1,
                                c.d_dg, cur >= 0 ? b.prefix[cur] : -1, kind, c.d_chunk_stats, stride,
-                               c.d_chunk_sum, c.stream),
+                               c.d_chunk_sum, c.d_pack_u, c.d_pack_w, c.nnz, c.stream),
           "core pass (structured)");
     return;
   }
@@ -789,7 +815,7 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
   t.MT = (t.LW + 7) / 8;
   t.NT = (t.RW + 7) / 8;
   const int ntiles = t.MT * t.NT;
-  if (ntiles <= kTcWarps * kTcTilesPerWarp) {
+  if (ntiles <= kTcWarps * kTcTilesPerWarp && t.MT * 8 * 32 <= 12 * 256 && 32 * Jm <= 2 * 256) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     const int nparts = std::max(1, std::min<int>(2 * sms, (g.nchunks + 31) / 32));
@@ -824,6 +850,21 @@ void upload_fibers(Ctx& c, const Blocks& b) {
         "fibers");
 }
 
+// Pack the structured pass operands (U, W) for this context's positions of the
+// last mode's CSF (the factors are fixed during the sweep / responsibilities).
+void pack_operands(Ctx& c, const void* sops) {
+  const int m = c.N - 1, F = c.ranks[c.N - 2];
+  const int P = c.G / (F * c.ranks[m]);
+  ensure(c, &c.d_pack_u, &c.pack_u_cap, (size_t)c.nnz * F + 1);
+  ensure(c, &c.d_pack_w, &c.pack_w_cap, (size_t)c.nnz * P + 1);
+  const ModeData& md = c.modes[m];
+  const uint64_t p0 = md.h_offsets[c.row_lo[m]], p1 = md.h_offsets[c.row_hi[m]];
+  ProfScope ps(c, kProfCorePass);
+  check(core_pack_structured(sops, c.model_view(), c.csf_view(m), p0, p1, c.d_pack_u, c.d_pack_w, c.nnz,
+                             c.stream),
+        "pack operands");
+}
+
 }  // namespace
 
 void core_sweep(Ctx& c, int reg, double lambda) {
@@ -837,6 +878,7 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
   if (b.fib.empty()) return;  // fully pruned core: nothing to update
   upload_fibers(c, b);
+  if (sops) pack_operands(c, sops);
   const int stride = F * (F + 1) / 2 + F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
   ensure(c, &c.d_dg, &c.dg_cap, (size_t)16 * VEST_MAXJ);
@@ -875,6 +917,7 @@ void core_responsibilities(Ctx& c) {
   const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
   if (b.fib.empty()) return;
   upload_fibers(c, b);
+  if (sops) pack_operands(c, sops);
   const int stride = 2 * F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
   ensure(c, &c.d_dg, &c.dg_cap, (size_t)16 * VEST_MAXJ);

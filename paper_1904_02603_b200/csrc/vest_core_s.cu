@@ -28,7 +28,76 @@ struct CorePassSArgs {
   double* stats;
   int stride;
   double* chunk_sq;
+  // packed per-entry operands (CSF order of the last mode), built once per sweep:
+  // U[pos][f] = A_{m-1}[i_{m-1}, f], W[p][pos] = prod_{k<m-1} A_k[i_k, beta_k(p)]
+  const double* U;
+  const double* W;
+  uint64_t wstride;
 };
+
+// Pack U and W for positions [p0, p1) of the last mode's CSF.  The factors do
+// not change during the core sweep, so the passes stream these coalesced
+// instead of re-gathering factor rows and coordinates every pass.
+template <class S>
+__global__ void __launch_bounds__(256) k_pack_uw(DevModel m, DevCSF csf, uint64_t p0, uint64_t p1, double* U,
+                                                 double* W, uint64_t wstride) {
+  constexpr int N = S::N;
+  constexpr int mm = N - 2;
+  constexpr int F = S::J(mm);
+  constexpr int P = S::G() / (F * S::J(N - 1));
+  for (uint64_t pos = p0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pos < p1;
+       pos += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t idx[N - 1];
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) idx[k] = __ldg(csf.oc[k] + pos);
+    constexpr int ldu = (F + 1) & ~1;
+    const double* urow = m.factor[mm] + (size_t)idx[mm] * ldu;
+    double u[F];
+#pragma unroll
+    for (int f = 0; f + 1 < F; f += 2) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(urow + f));
+      u[f] = v.x;
+      u[f + 1] = v.y;
+    }
+    if constexpr (F & 1) u[F - 1] = __ldg(urow + F - 1);
+    if constexpr (N == 3) {
+      // W[p][pos] = A_0[i_0, p]: one vectorised row gather
+      constexpr int J0 = S::J(0);
+      constexpr int ld0 = (J0 + 1) & ~1;
+      const double* row0 = m.factor[0] + (size_t)idx[0] * ld0;
+      double w[J0];
+#pragma unroll
+      for (int p = 0; p + 1 < J0; p += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(row0 + p));
+        w[p] = v.x;
+        w[p + 1] = v.y;
+      }
+      if constexpr (J0 & 1) w[J0 - 1] = __ldg(row0 + J0 - 1);
+#pragma unroll
+      for (int p = 0; p < J0; ++p) __stcs(W + (uint64_t)p * wstride + pos, w[p]);
+    } else {
+#pragma unroll 1
+      for (int p = 0; p < P; ++p) {
+        int rest = p;
+        double w = 1.0;
+#pragma unroll
+        for (int k = mm - 1; k >= 0; --k) {
+          const int b = rest % S::J(k);
+          rest /= S::J(k);
+          w *= __ldg(m.factor[k] + (size_t)idx[k] * m.ld[k] + b);
+        }
+        __stcs(W + (uint64_t)p * wstride + pos, w);
+      }
+    }
+    if constexpr ((F & 1) == 0) {
+#pragma unroll
+      for (int f = 0; f < F; f += 2) __stcs(reinterpret_cast<double2*>(U + pos * F + f), make_double2(u[f], u[f + 1]));
+    } else {
+#pragma unroll
+      for (int f = 0; f < F; ++f) __stcs(U + pos * F + f, u[f]);
+    }
+  }
+}
 
 template <int B, int E, class Fn>
 __device__ __forceinline__ void sfor_s(Fn&& f) {
@@ -94,26 +163,44 @@ __global__ void __launch_bounds__(kSWarps * 32) k_core_pass_s(CorePassSArgs a) {
     double u[F];
     double wp = 1.0, wc = 1.0, r = 0.0;
     if (valid) {
-      uint32_t idx[m];
-#pragma unroll
-      for (int k = 0; k < m; ++k) idx[k] = __ldg(a.csf.oc[k] + pos);
       r = a.r[pos];
-      constexpr int ldu = (F + 1) & ~1;
-      const double* urow = a.m.factor[mm] + (size_t)idx[mm] * ldu;
+      if (a.U) {
+        // packed operands: contiguous per entry (coalesced across the warp)
+        const double* urow = a.U + (size_t)pos * F;
+        if constexpr ((F & 1) == 0) {
 #pragma unroll
-      for (int f = 0; f + 1 < F; f += 2) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(urow + f));
-        u[f] = v.x;
-        u[f + 1] = v.y;
+          for (int f = 0; f < F; f += 2) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(urow + f));
+            u[f] = v.x;
+            u[f + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int f = 0; f < F; ++f) u[f] = __ldcs(urow + f);
+        }
+        if (has_prev) wp = __ldcs(a.W + (uint64_t)a.prev_p * a.wstride + pos);
+        if (acc) wc = __ldcs(a.W + (uint64_t)a.cur_p * a.wstride + pos);
+      } else {
+        uint32_t idx[m];
+#pragma unroll
+        for (int k = 0; k < m; ++k) idx[k] = __ldg(a.csf.oc[k] + pos);
+        constexpr int ldu = (F + 1) & ~1;
+        const double* urow = a.m.factor[mm] + (size_t)idx[mm] * ldu;
+#pragma unroll
+        for (int f = 0; f + 1 < F; f += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(urow + f));
+          u[f] = v.x;
+          u[f + 1] = v.y;
+        }
+        if constexpr (F & 1) u[F - 1] = __ldg(urow + F - 1);
+        sfor_s<0, mm>([&](auto kc) {
+          constexpr int k = decltype(kc)::value;
+          constexpr int ld = (S::J(k) + 1) & ~1;
+          const double* row = a.m.factor[k] + (size_t)idx[k] * ld;
+          if (has_prev) wp *= __ldg(row + bp[k]);
+          if (acc) wc *= __ldg(row + bc[k]);
+        });
       }
-      if constexpr (F & 1) u[F - 1] = __ldg(urow + F - 1);
-      sfor_s<0, mm>([&](auto kc) {
-        constexpr int k = decltype(kc)::value;
-        constexpr int ld = (S::J(k) + 1) & ~1;
-        const double* row = a.m.factor[k] + (size_t)idx[k] * ld;
-        if (has_prev) wp *= __ldg(row + bp[k]);
-        if (acc) wc *= __ldg(row + bc[k]);
-      });
       if (has_prev) {
         double t = 0.0;
 #pragma unroll
@@ -177,10 +264,22 @@ cudaError_t run_core_pass_s(const CorePassSArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <class S>
+cudaError_t run_pack_uw(const DevModel& m, const DevCSF& csf, uint64_t p0, uint64_t p1, double* U, double* W,
+                        uint64_t wstride, cudaStream_t s) {
+  if (p1 > p0) {
+    k_pack_uw<S><<<1184, 256, 0, s>>>(m, csf, p0, p1, U, W, wstride);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
 struct CoreSOps {
   int N;
   int J[VEST_MAXN];
   cudaError_t (*pass)(const CorePassSArgs& a, cudaStream_t s);
+  cudaError_t (*pack)(const DevModel& m, const DevCSF& csf, uint64_t p0, uint64_t p1, double* U, double* W,
+                      uint64_t wstride, cudaStream_t s);
 };
 
 template <int... Js>
@@ -190,6 +289,7 @@ constexpr CoreSOps make_core_ops() {
   const int js[] = {Js...};
   for (int k = 0; k < (int)sizeof...(Js); ++k) o.J[k] = js[k];
   o.pass = &run_core_pass_s<SShape<Js...>>;
+  o.pack = &run_pack_uw<SShape<Js...>>;
   return o;
 }
 
@@ -209,10 +309,19 @@ const void* find_core_ops(int N, const int* J) {
   return nullptr;
 }
 
+cudaError_t core_pack_structured(const void* ops, const DevModel& m, const DevCSF& csf, uint64_t p0, uint64_t p1,
+                                 double* U, double* W, uint64_t wstride, cudaStream_t s) {
+  return static_cast<const CoreSOps*>(ops)->pack(m, csf, p0, p1, U, W, wstride, s);
+}
+
 cudaError_t core_pass_structured(const void* ops, const DevModel& m, const DevCSF& csf, double* r, int prev_p,
                                  const double* prev_dg, int cur_p, int kind, double* stats, int stride,
-                                 double* chunk_sq, cudaStream_t s) {
+                                 double* chunk_sq, const double* U, const double* W, uint64_t wstride,
+                                 cudaStream_t s) {
   CorePassSArgs a{};
+  a.U = U;
+  a.W = W;
+  a.wstride = wstride;
   a.m = m;
   a.csf = csf;
   a.r = r;

@@ -745,6 +745,8 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_small);
   cudaFree(c.d_fibers);
   cudaFree(c.d_dg);
+  cudaFree(c.d_pack_u);
+  cudaFree(c.d_pack_w);
   cudaFree(c.d_counts);
   cudaFree(c.d_sel);
   if (c.h_small) cudaFreeHost(c.h_small);

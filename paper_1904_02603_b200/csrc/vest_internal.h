@@ -160,6 +160,8 @@ struct Ctx {
   double* h_small = nullptr;
   uint32_t* d_fibers = nullptr;    size_t fibers_cap = 0;  // fiber prefix lin indices
   double* d_dg = nullptr;          size_t dg_cap = 0;
+  double* d_pack_u = nullptr;      size_t pack_u_cap = 0;   // structured core pass operands
+  double* d_pack_w = nullptr;      size_t pack_w_cap = 0;
   unsigned long long* d_counts = nullptr;  // prune / sparsity counters
   void* d_sel = nullptr;           // radix-select state
 

@@ -265,10 +265,12 @@ __device__ __forceinline__ void fused_residual(const RowPassArgs& a, const Chunk
       double an[Jm];
 #pragma unroll
       for (int c = 0; c < Jm; ++c) an[c] = arow[c];
+      // per-lane cells: read the core through L1 (a per-lane constant-bank
+      // index would serialise 32-way)
       for (int p = lane; p < NV; p += 32) {
         double t = 0.0;
 #pragma unroll
-        for (int c = 0; c < Jm; ++c) t = fma(ConstCore{}(p * Jm + c), an[c], t);
+        for (int c = 0; c < Jm; ++c) t = fma(__ldg(a.m.core + p * Jm + c), an[c], t);
         v[p] = t;
       }
       __syncwarp();
