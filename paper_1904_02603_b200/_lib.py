@@ -55,6 +55,10 @@ SIGNATURES = {
     "vest_ctx_profile": (C.c_int, [vp, C.c_int]),
     "vest_ctx_profile_read": (C.c_int, [vp, f64p, u64p, C.c_int]),
     "vest_measure_fp64_peak": (C.c_int, [C.c_int, f64p]),
+    "vest_ctx_create_shard": (C.c_int, [C.c_int, u64p, C.c_uint64, u32p, f64p, u64p, C.c_int, u64p, u64p,
+                                        C.POINTER(vp)]),
+    "vest_ctx_set_comm": (C.c_int, [vp, vp]),
+    "vest_ctx_local_nnz": (C.c_uint64, [vp, C.c_int]),
     "vest_synth": (C.c_int, [C.c_int, u64p, C.c_uint64, f64p, C.c_int, C.c_uint64, u32p, f64p]),
     "vest_split_ids": (C.c_int, [C.c_uint64, C.c_double, C.c_uint64, u64p, u64p, u64p, u64p]),
     "vest_partition_rows": (C.c_int, [u64p, C.c_uint64, C.c_int, u64p]),

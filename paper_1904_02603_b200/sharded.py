@@ -79,7 +79,7 @@ class ShardDevice(Device):
         self.h = h
         self.comm = comm
         self._hooks = comm.hooks(self)  # keep the ctypes callbacks alive
-        check(L.vest_ctx_set_comm(self.h, C.byref(self._hooks)))
+        check(L.vest_ctx_set_comm(self.h, C.cast(C.pointer(self._hooks), C.c_void_p)))
 
     def local_nnz(self, mode: int) -> int:
         return int(self._L.vest_ctx_local_nnz(self.h, mode))

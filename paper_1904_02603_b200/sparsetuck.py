@@ -680,3 +680,33 @@ def fit(x: SparseTensor, cfg: TrainConfig, device: int = 0) -> FitResult:
     report.elapsed_sec = time.perf_counter() - t_start
     dev.close()
     return FitResult(model, report)
+
+
+@dataclass
+class RateResult:
+    rate: float
+    pruned: PruneCounts
+    sparsity: float
+    train_re: float
+    test_re: float
+
+
+def auto_search(x_train: SparseTensor, x_test: SparseTensor, model: TuckerModel, rates: Sequence[float],
+                device: int = 0) -> list:
+    """Prune-rate sweep (BASELINE config 5; SURVEY App. C option (i)): for each
+    rate, start from the trained model, score responsibilities on the training
+    entries (pruning.hpp:181-191), prune_step(rate) (pruning.hpp:234-247) and
+    evaluate the relative error on the training and held-out entries
+    (tucker_model.hpp:186-188, trainer.hpp:188-190).  Device-resident: the
+    trained model is uploaded once per rate; the evaluation is the inner loop."""
+    dev = Device(x_train, model.ranks, device)
+    out = []
+    for pr in rates:
+        dev.set_model(model)
+        dev.compute_responsibilities(want=False)
+        counts = dev.prune_step(float(pr))
+        train_re = dev.compute_residuals().re
+        test_re = dev.evaluate(x_test)
+        out.append(RateResult(float(pr), counts, dev.sparsity()[0], train_re, test_re))
+    dev.close()
+    return out
