@@ -364,8 +364,85 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------ the other BASELINE configs --
+CONFIGS = {
+    1: dict(desc="3-mode 1000^3, 100k uniform, fp64 U[0,1), R 5^3, lambda 0.01; 10 iterations then prune 0.5",
+            dims=[1000] * 3, nnz=100_000, ranks=[5, 5, 5], lam=0.01, zipf=None, values_kind=0, iters=10,
+            prune=[(10, 0.5)], core_keep=1.0),
+    2: dict(desc="3-mode 100k^3, 10M uniform, fp64 U[0,1), R 10^3, lambda 0.01; 20 iterations, prune 0.3 every 5",
+            dims=[100_000] * 3, nnz=10_000_000, ranks=[10, 10, 10], lam=0.01, zipf=None, values_kind=0, iters=20,
+            prune=[(5, 0.3), (10, 0.3), (15, 0.3)], core_keep=1.0),
+    3: dict(desc="3-mode 1M x 200k x 1000, 50M, Zipf(1.1) on modes 1-2, integers 1..5, R (10,10,5), lambda 0.1; "
+                 "10 iterations", dims=[1_000_000, 200_000, 1000], nnz=50_000_000, ranks=[10, 10, 5], lam=0.1,
+            zipf=[1.1, 1.1, 0.0], values_kind=1, iters=10, prune=[], core_keep=1.0),
+    4: dict(desc="4-mode 1M^4, 200M uniform, N(0,1) as float, R 8^4 core pruned to 10% nonzero, lambda 0.01; "
+                 "10 iterations", dims=[1_000_000] * 4, nnz=200_000_000, ranks=[8, 8, 8, 8], lam=0.01, zipf=None,
+            values_kind=2, iters=10, prune=[], core_keep=0.1),
+    5: dict(desc="5-mode 100k^5, 100M Zipf(1.0) per mode, fp64 U[0,1), R 5^5; 90/10 split; prune-rate sweep "
+                 "0.1..0.9 with train/test RE", dims=[100_000] * 5, nnz=100_000_000, ranks=[5] * 5, lam=0.01,
+            zipf=[1.0] * 5, values_kind=0, iters=5, prune=[], core_keep=1.0, sweep=True),
+}
+
+
+def run_config(cfg_id, iters_override=None):
+    """Full-size run of BASELINE config `cfg_id` on one GPU: per-iteration device
+    time (CUDA events on the library stream), prune events timed separately."""
+    import torch
+    from paper_1904_02603_b200 import sparsetuck as st
+
+    c = CONFIGS[cfg_id]
+    t0 = time.perf_counter()
+    coords, vals = synth(c["dims"], c["nnz"], 1000 + cfg_id, c["values_kind"], c["zipf"])
+    gen_s = time.perf_counter() - t0
+    x = st.SparseTensor(c["dims"], coords, vals)
+    test = None
+    if c.get("sweep"):
+        x, test = st.split_train_test(x, 0.1, 2026)
+    t0 = time.perf_counter()
+    dev = st.Device(x, c["ranks"], 0)
+    build_s = time.perf_counter() - t0
+    m = st.init_random(c["dims"], c["ranks"], 7)
+    if c["core_keep"] < 1.0:  # seeded core mask (SURVEY App. C, config 4)
+        rng = np.random.default_rng(44)
+        mask = (rng.random(m.core.shape) >= c["core_keep"]).astype(np.uint8)
+        m.core[mask == 1] = 0.0
+        m.core_mask = mask
+    dev.set_model(m)
+    stream = torch.cuda.ExternalStream(dev.stream())
+    iters = iters_override or c["iters"]
+    times, res, prunes = [], [], []
+    for t in range(1, iters + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res.append(dev.cd_iteration(0, c["lam"]))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        for (at, pr) in c["prune"]:
+            if at == t:
+                p0 = time.perf_counter()
+                dev.compute_responsibilities(want=False)
+                cnt = dev.prune_step(pr)
+                prunes.append({"iter": t, "rate": pr, "ms": (time.perf_counter() - p0) * 1e3,
+                               "counts": [cnt.core] + cnt.factors})
+    med = statistics.median(times[1:] if len(times) > 1 else times)
+    line = {"config": cfg_id, "workload": c["desc"], "nnz": x.nnz(), "ms_per_iter_median": med,
+            "ms_per_iter": times, "value": x.nnz() / (med * 1e-3), "unit": UNIT, "re_trace": res,
+            "prune_events": prunes, "gen_s": gen_s, "ctx_build_s": build_s, "specialised": dev.specialised(),
+            "device_gb": dev.device_bytes() / 1e9}
+    if c.get("sweep"):
+        p0 = time.perf_counter()
+        sweep = st.auto_search(x, test, dev.get_model(), [round(0.1 * k, 1) for k in range(1, 10)])
+        line["sweep"] = [{"rate": r.rate, "train_re": r.train_re, "test_re": r.test_re, "sparsity": r.sparsity}
+                         for r in sweep]
+        line["sweep_s"] = time.perf_counter() - p0
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=0, help="run BASELINE config 1..5 at full size (diagnostic)")
+    ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
@@ -375,6 +452,9 @@ def main():
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
+    if args.config:
+        run_config(args.config, args.iters or None)
+        return
     if args.impl == "reference":
         run_reference_arm(args, rank)
         return

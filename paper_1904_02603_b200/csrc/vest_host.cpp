@@ -5,6 +5,7 @@
 // sharding.
 #include <algorithm>
 #include <cmath>
+#include <parallel/algorithm>
 #include <cstdint>
 #include <cstring>
 #include <random>
@@ -45,6 +46,18 @@ struct Zipf {
 };
 }  // namespace
 
+// Deterministic and thread-count independent: draws come in chunks of
+// kSynthChunk, each from its own engine seeded by (seed, round, chunk); the
+// keys are sorted and deduplicated (parallel sort), and the shortfall redrawn.
+constexpr uint64_t kSynthChunk = 1u << 20;
+
+static uint64_t chunk_seed(uint64_t seed, uint64_t round, uint64_t chunk) {
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull * (round * 1000003ull + chunk + 1);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
 extern "C" int vest_synth(int order, const uint64_t* dims, uint64_t nnz, const double* zipf_s, int values_kind,
                           uint64_t seed, uint32_t* coords_out, double* values_out) {
   try {
@@ -60,7 +73,6 @@ extern "C" int vest_synth(int order, const uint64_t* dims, uint64_t nnz, const d
     long double cells = 1;
     for (int k = 0; k < order; ++k) cells *= (long double)dims[k];
     if ((long double)nnz > cells) throw std::invalid_argument("nnz exceeds tensor cell count");
-    std::mt19937_64 rng(seed);
     std::vector<Zipf> z;
     z.reserve(order);
     std::vector<int> use_z(order, 0);
@@ -68,43 +80,56 @@ extern "C" int vest_synth(int order, const uint64_t* dims, uint64_t nnz, const d
       use_z[k] = zipf_s && zipf_s[k] > 0.0;
       z.emplace_back(use_z[k] ? dims[k] : 1, use_z[k] ? zipf_s[k] : 1.0);
     }
-    std::uniform_real_distribution<double> unif(0.0, 1.0);
-    auto draw_key = [&]() {
-      u128 key = 0;
-      for (int k = 0; k < order; ++k) {
-        uint64_t c;
-        if (use_z[k]) {
-          c = z[k].draw(unif(rng));
-        } else {
-          std::uniform_int_distribution<uint64_t> pick(0, dims[k] - 1);
-          c = pick(rng);
-        }
-        key |= (u128)c << shift[k];
-      }
-      return key;
-    };
-    // draw, sort, deduplicate; redraw the shortfall until nnz distinct tuples
     std::vector<u128> keys;
     keys.reserve(nnz);
-    for (int round = 0; keys.size() < nnz; ++round) {
+    for (uint64_t round = 0; keys.size() < nnz; ++round) {
       if (round > 10000) throw std::runtime_error("could not draw enough distinct coordinates");
-      const uint64_t need = nnz - keys.size();
-      for (uint64_t q = 0; q < need; ++q) keys.push_back(draw_key());
-      std::sort(keys.begin(), keys.end());
+      const uint64_t have = keys.size(), need = nnz - have;
+      keys.resize(nnz);
+      const uint64_t nch = (need + kSynthChunk - 1) / kSynthChunk;
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int64_t ch = 0; ch < (int64_t)nch; ++ch) {
+        std::mt19937_64 rng(chunk_seed(seed, round, (uint64_t)ch));
+        std::uniform_real_distribution<double> unif(0.0, 1.0);
+        const uint64_t b = have + (uint64_t)ch * kSynthChunk, e = std::min<uint64_t>(nnz, b + kSynthChunk);
+        for (uint64_t q = b; q < e; ++q) {
+          u128 key = 0;
+          for (int k = 0; k < order; ++k) {
+            uint64_t c;
+            if (use_z[k]) {
+              c = z[k].draw(unif(rng));
+            } else {
+              std::uniform_int_distribution<uint64_t> pick(0, dims[k] - 1);
+              c = pick(rng);
+            }
+            key |= (u128)c << shift[k];
+          }
+          keys[q] = key;
+        }
+      }
+      __gnu_parallel::sort(keys.begin(), keys.end());
       keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
     }
     // canonical entry order: row-major over the coordinate tuple
-    for (uint64_t e = 0; e < nnz; ++e)
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < (int64_t)nnz; ++e)
       for (int k = 0; k < order; ++k)
         coords_out[e * order + k] = (uint32_t)((keys[e] >> shift[k]) & (((u128)1 << bits[k]) - 1));
-    if (values_kind == 0) {
-      for (uint64_t e = 0; e < nnz; ++e) values_out[e] = unif(rng);
-    } else if (values_kind == 1) {
-      std::uniform_int_distribution<int> d(1, 5);
-      for (uint64_t e = 0; e < nnz; ++e) values_out[e] = double(d(rng));
-    } else {
-      std::normal_distribution<double> d(0.0, 1.0);
-      for (uint64_t e = 0; e < nnz; ++e) values_out[e] = double(float(d(rng)));
+    const uint64_t nch = (nnz + kSynthChunk - 1) / kSynthChunk;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t ch = 0; ch < (int64_t)nch; ++ch) {
+      std::mt19937_64 rng(chunk_seed(seed ^ 0x5EED5EEDull, 0, (uint64_t)ch));
+      const uint64_t b = (uint64_t)ch * kSynthChunk, e = std::min<uint64_t>(nnz, b + kSynthChunk);
+      if (values_kind == 0) {
+        std::uniform_real_distribution<double> d(0.0, 1.0);
+        for (uint64_t q = b; q < e; ++q) values_out[q] = d(rng);
+      } else if (values_kind == 1) {
+        std::uniform_int_distribution<int> d(1, 5);
+        for (uint64_t q = b; q < e; ++q) values_out[q] = double(d(rng));
+      } else {
+        std::normal_distribution<double> d(0.0, 1.0);
+        for (uint64_t q = b; q < e; ++q) values_out[q] = double(float(d(rng)));
+      }
     }
     return 0;
   } catch (const std::invalid_argument& e) {
