@@ -410,6 +410,9 @@ def run_config(cfg_id, iters_override=None):
     dev.set_model(m)
     stream = torch.cuda.ExternalStream(dev.stream())
     iters = iters_override or c["iters"]
+    from paper_1904_02603_b200 import _lib
+    L = _lib.lib()
+    L.vest_ctx_profile(dev.h, 1)
     times, res, prunes = [], [], []
     for t in range(1, iters + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -425,11 +428,16 @@ def run_config(cfg_id, iters_override=None):
                 cnt = dev.prune_step(pr)
                 prunes.append({"iter": t, "rate": pr, "ms": (time.perf_counter() - p0) * 1e3,
                                "counts": [cnt.core] + cnt.factors})
+    ms_arr = np.zeros(8)
+    n_arr = np.zeros(8, np.uint64)
+    L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
+    fam_names = ["factor_update", "core_pass", "core_gemm", "core_solve", "residual", "resp", "prune"]
+    fams = {fam_names[i]: {"ms": float(ms_arr[i]), "scopes": int(n_arr[i])} for i in range(7)}
     med = statistics.median(times[1:] if len(times) > 1 else times)
     line = {"config": cfg_id, "workload": c["desc"], "nnz": x.nnz(), "ms_per_iter_median": med,
             "ms_per_iter": times, "value": x.nnz() / (med * 1e-3), "unit": UNIT, "re_trace": res,
             "prune_events": prunes, "gen_s": gen_s, "ctx_build_s": build_s, "specialised": dev.specialised(),
-            "device_gb": dev.device_bytes() / 1e9}
+            "device_gb": dev.device_bytes() / 1e9, "kernel_families_ms": fams}
     if c.get("sweep"):
         p0 = time.perf_counter()
         sweep = st.auto_search(x, test, dev.get_model(), [round(0.1 * k, 1) for k in range(1, 10)])

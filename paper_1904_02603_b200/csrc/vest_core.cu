@@ -27,7 +27,7 @@
 
 namespace vest {
 
-constexpr int kFMax = 10;  // fibers per block, register-accumulated pass
+constexpr int kFMax = 15;  // fibers per block (general pass: 15 s-columns + r on DMMA)
 constexpr int kPassWarps = 8;
 
 struct CorePassArgs {
@@ -70,17 +70,21 @@ __device__ __forceinline__ void treduce(double (&v)[V], int lane) {
   });
 }
 
-// One warp per chunk of a last-mode slice.  Per entry: the fiber products
-// s_f (from factor rows staged in shared memory), the previous block's residual
-// update, and the register accumulation of S (upper triangle) and R.
+// One warp per chunk of a last-mode slice (runtime ranks / sparse fiber
+// lists).  Per entry: the rows of modes < m are gathered once (vector loads,
+// all issued before use) into a lane-major shared-memory stage; the previous
+// block's residual update and the current block's fiber products
+// s_f = prod_k row_k[beta_k(f)] read it; the (s_0..s_{nf-1}, r) vectors are
+// staged transposed (r in column 15) and S = sum s s^T, R = sum s r are
+// accumulated on the FP64 tensor cores (DMMA), as in the structured pass.
 template <int M>
 __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
   extern __shared__ double smem[];
   __shared__ int sb[2][kFMax][M > 0 ? M : 1];  // beta of each fiber (prev, cur)
   __shared__ double sdg[kFMax * VEST_MAXJ];
+  __shared__ double sq_q[kPassWarps][kFMax];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Jm = a.m.J[M];
-  // fiber beta tables (decoded from the packed cell index of cell c = 0)
   for (int t = threadIdx.x; t < 2 * kFMax * M; t += blockDim.x) {
     const int which = t / (kFMax * M), rest = t % (kFMax * M), f = rest / M, k = rest % M;
     const uint32_t* fl = which ? a.cur_fib : a.prev_fib;
@@ -91,12 +95,6 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
   }
   for (int t = threadIdx.x; t < kFMax * Jm; t += blockDim.x)
     sdg[t] = (a.prev_nf > 0 && t < a.prev_nf * Jm) ? a.prev_dg[t] : 0.0;
-  __syncthreads();
-  const uint32_t ci = blockIdx.x * kPassWarps + warp;
-  if (ci >= a.csf.nchunks) return;
-  const Chunk ch = a.csf.chunks[ci];
-
-  // stage layout: offs[k] + b rows of 32 lanes
   int offs[M > 0 ? M : 1];
   int tot = 0;
 #pragma unroll
@@ -104,37 +102,38 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
     offs[k] = tot;
     tot += a.m.J[k];
   }
-  double* st = smem + (size_t)warp * tot * 32;
+  double* st = smem + (size_t)warp * (tot * 32 + 16 * kXld);
+  double* X = st + tot * 32;
+  for (int t = lane; t < 16 * kXld; t += 32) X[t] = 0.0;
+  __syncthreads();
+  const uint32_t ci = blockIdx.x * kPassWarps + warp;
+  if (ci >= a.csf.nchunks) return;
+  const Chunk ch = a.csf.chunks[ci];
 
   // q_f = sum_c A_m[s, c] dg_prev[f][c]
   const double* arow = a.m.factor[M] + (size_t)ch.row * a.m.ld[M];
-  double q[kFMax];
-#pragma unroll
-  for (int f = 0; f < kFMax; ++f) {
+  if (lane < kFMax) {
     double t = 0.0;
-    if (f < a.prev_nf)
-      for (int c = 0; c < Jm; ++c) t = fma(__ldg(arow + c), sdg[f * Jm + c], t);
-    q[f] = t;
+    if (lane < a.prev_nf)
+      for (int c = 0; c < Jm; ++c) t = fma(__ldg(arow + c), sdg[lane * Jm + c], t);
+    sq_q[warp][lane] = t;
   }
+  __syncwarp();
 
-  constexpr int NA = kFMax * (kFMax + 1) / 2 + kFMax;  // 65
-  constexpr int V = (NA + 31) / 32 * 32;              // 96
-  double acc[V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) acc[i] = 0.0;
+  double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
   double sq = 0.0;
   const int nf = a.cur_nf;
+  const bool acc = a.kind != 2 && nf > 0;
 
   for (uint32_t base = ch.beg; base < ch.end; base += 32) {
     const uint32_t pos = base + lane;
     const bool valid = pos < ch.end;
     double r = 0.0;
     if (valid) {
-      // all row gathers issued before use (memory-level parallelism); rows
-      // are 16-byte aligned with even stride, so pairs never cross the row
       uint32_t idx[M > 0 ? M : 1];
 #pragma unroll
       for (int k = 0; k < M; ++k) idx[k] = __ldg(a.csf.oc[k] + pos);
+      r = a.r[pos];
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         const double* row = a.m.factor[k] + (size_t)idx[k] * a.m.ld[k];
@@ -148,60 +147,43 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
           }
         }
       }
-      r = a.r[pos];
     }
     __syncwarp();
-    if (valid) {
-      if (a.prev_nf > 0) {
-        double t = 0.0;
+    if (valid && a.prev_nf > 0) {
+      double t = 0.0;
 #pragma unroll
-        for (int f = 0; f < kFMax; ++f) {
-          if (f < a.prev_nf) {
-            double s = 1.0;
+      for (int f = 0; f < kFMax; ++f) {
+        if (f < a.prev_nf) {
+          double s = 1.0;
 #pragma unroll
-            for (int k = 0; k < M; ++k) s *= st[(offs[k] + sb[0][f][k]) * 32 + lane];
-            t = fma(s, q[f], t);
-          }
+          for (int k = 0; k < M; ++k) s *= st[(offs[k] + sb[0][f][k]) * 32 + lane];
+          t = fma(s, sq_q[warp][f], t);
         }
-        r -= t;
-        if (a.kind != 1) a.r[pos] = r;
       }
-      if (a.kind == 2) {
-        sq = fma(r, r, sq);
-      } else if (nf > 0) {
-        double s[kFMax];
+      r -= t;
+      if (a.kind != 1) a.r[pos] = r;
+    }
+    if (a.kind == 2) {
+      sq = fma(r, r, sq);
+      __syncwarp();
+      continue;
+    }
+    if (acc) {
 #pragma unroll
-        for (int f = 0; f < kFMax; ++f) {
+      for (int f = 0; f < kFMax; ++f) {
+        if (f < nf) {
           double v = 0.0;
-          if (f < nf) {
+          if (valid) {
             v = 1.0;
 #pragma unroll
             for (int k = 0; k < M; ++k) v *= st[(offs[k] + sb[1][f][k]) * 32 + lane];
           }
-          s[f] = v;
-        }
-        if (a.kind == 0) {
-          int i = 0;
-#pragma unroll
-          for (int f = 0; f < kFMax; ++f)
-#pragma unroll
-            for (int g = f; g < kFMax; ++g) {
-              acc[i] = fma(s[f], s[g], acc[i]);
-              ++i;
-            }
-#pragma unroll
-          for (int f = 0; f < kFMax; ++f) {
-            acc[i] = fma(s[f], r, acc[i]);
-            ++i;
-          }
-        } else {
-#pragma unroll
-          for (int f = 0; f < kFMax; ++f) {
-            acc[f] = fma(s[f], r, acc[f]);
-            acc[kFMax + f] = fma(s[f], s[f], acc[kFMax + f]);
-          }
+          X[f * kXld + lane] = v;
         }
       }
+      X[15 * kXld + lane] = valid ? r : 0.0;
+      __syncwarp();
+      gram_dmma<16>(X, d, lane);
     }
     __syncwarp();
   }
@@ -211,30 +193,23 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
     if (lane == 0) a.chunk_sq[ci] = sq;
     return;
   }
-  treduce<V>(acc, lane);
-  constexpr int per = V / 32;
-  // compact: the kernel accumulates the kFMax layout; the stats row stores the
-  // nf layout (S upper triangle over nf fibers, then R) or (R, D)
+  if (!acc) return;
   double* out = a.stats + (size_t)ci * a.stride;
+  const int NS = nf * (nf + 1) / 2;
 #pragma unroll
-  for (int w = 0; w < per; ++w) {
-    const int idx = lane * per + w;
-    if (a.kind == 0) {
-      if (idx < kFMax * (kFMax + 1) / 2) {
-        int f = 0, rem = idx;
-        while (rem >= kFMax - f) {
-          rem -= kFMax - f;
-          ++f;
-        }
-        const int g = f + rem;
-        if (g < nf) out[f * nf - f * (f - 1) / 2 + (g - f)] = acc[w];
-      } else if (idx < NA) {
-        const int f = idx - kFMax * (kFMax + 1) / 2;
-        if (f < nf) out[nf * (nf + 1) / 2 + f] = acc[w];
+  for (int t = 0; t < 3; ++t) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      int row, col;
+      gram_coord(t, i, lane, row, col);
+      const double v = d[t][i];
+      if (a.kind == 0) {
+        if (row <= col && col < nf) out[row * nf - row * (row - 1) / 2 + (col - row)] = v;
+        else if (col == 15 && row < nf) out[NS + row] = v;
+      } else {
+        if (col == 15 && row < nf) out[row] = v;
+        else if (row == col && row < nf) out[nf + row] = v;
       }
-    } else if (idx < 2 * kFMax) {
-      const int f = idx % kFMax;
-      if (f < nf) out[(idx / kFMax) * nf + f] = acc[w];
     }
   }
 }
@@ -400,7 +375,8 @@ struct GemmTcArgs {
 };
 
 constexpr int kTcWarps = 8;
-constexpr int kTcTilesPerWarp = 12;
+constexpr int kTcTilesPerWarp = 14;
+constexpr int kTcLPer = 18;
 constexpr int kTcLd = 36;  // == 4 mod 16: conflict-free fragment loads
 
 __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
@@ -441,7 +417,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
   const int LWp = a.MT * 8;
   // software pipeline: the next batch's statistics rows and last-mode factor
   // rows are loaded into registers while the current batch runs on DMMA
-  constexpr int kLPer = 12, kAPer = 2;  // per-thread staging share (LWp*32 <= 3072, 32*Jm <= 512)
+  constexpr int kLPer = kTcLPer, kAPer = 2;  // per-thread staging share (LWp*32 <= kTcLPer*256, 32*Jm <= 512)
   double lv[kLPer], av[kAPer];
   auto prefetch = [&](uint32_t cb) {
     const int nb = (int)min(32u, c1 - cb);
@@ -702,11 +678,15 @@ Blocks plan_structured(const Ctx& c) {
 int pick_block(const Ctx& c) {
   const int Jm = c.ranks[c.N - 1];
   int F = c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax;
-  // keep the gemm outputs within the kernel's tile capacity
+  // keep the block within the solve's shared memory (dense H of (F*Jm)^2) and
+  // the tensor-core gemm's staging / tile capacity
   while (F > 1) {
     const int NS = F * (F + 1) / 2, NAm = Jm * (Jm + 1) / 2;
-    const int tiles = ((NS + 3) / 4) * ((NAm + 3) / 4);
-    if (tiles <= kTileMax * kGemmThreads && F * Jm <= kGemmThreads) break;
+    const int nq = F * Jm;
+    const int MT = (NS + F + 7) / 8, NT = (NAm + Jm + 7) / 8;
+    const bool solve_ok = (size_t)(nq * nq + 4 * nq) * 8 <= 200 * 1024;
+    const bool tc_ok = MT * NT <= kTcWarps * kTcTilesPerWarp && MT * 8 * 32 <= kTcLPer * 256 && 32 * Jm <= 512;
+    if (solve_ok && tc_ok) break;
     --F;
   }
   return F;
@@ -722,7 +702,7 @@ void launch_pass(Ctx& c, const CorePassArgs& a) {
   const int M = c.N - 1;
   int tot = 0;
   for (int k = 0; k < M; ++k) tot += c.ranks[k];
-  const size_t sm = (size_t)kPassWarps * tot * 32 * sizeof(double);
+  const size_t sm = (size_t)kPassWarps * (tot * 32 + 16 * kXld) * sizeof(double);
   const dim3 grid((a.csf.nchunks + kPassWarps - 1) / kPassWarps);
   if (a.csf.nchunks == 0) return;
 #define VEST_PASS(MM)                                                                       \
@@ -815,7 +795,7 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
   t.MT = (t.LW + 7) / 8;
   t.NT = (t.RW + 7) / 8;
   const int ntiles = t.MT * t.NT;
-  if (ntiles <= kTcWarps * kTcTilesPerWarp && t.MT * 8 * 32 <= 12 * 256 && 32 * Jm <= 2 * 256) {
+  if (ntiles <= kTcWarps * kTcTilesPerWarp && t.MT * 8 * 32 <= kTcLPer * 256 && 32 * Jm <= 2 * 256) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     const int nparts = std::max(1, std::min<int>(2 * sms, (g.nchunks + 31) / 32));
