@@ -160,7 +160,8 @@ int vest_frobenius_norm(vest_ctx* ctx, double* out);
 /* ------------------------------------------------------------ measurement --
  * Kernel-family timing with CUDA events on the context stream (bench.py's
  * per-kernel roofline).  Families: 0 factor-row update, 1 core pass,
- * 2 core gemm, 3 core solve, 4 residual, 5 responsibilities, 6 prune. */
+ * 2 core gemm, 3 core solve, 4 residual, 5 responsibilities, 6 prune,
+ * 7 last-mode factor update with the fused residual. */
 #define VEST_PROF_FAMILIES 8
 int vest_ctx_profile(vest_ctx* ctx, int on);
 /* ms[f] = summed device time, launches[f] = timed scopes, since the last reset. */

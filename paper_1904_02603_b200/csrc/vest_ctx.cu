@@ -348,7 +348,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
   a.fuse_resid = fuse ? 1 : 0;
   a.r_out = c.d_r;
   {
-    ProfScope ps(c, kProfFactor);
+    ProfScope ps(c, fuse ? kProfFactorFused : kProfFactor);
     check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
     if (reg == 1) l1_empty_rows(c, mode, lambda);
   }

@@ -214,7 +214,16 @@ void comm_allreduce(Ctx& c, double* p, uint64_t n);
 void comm_allgather_rows(Ctx& c, int mode, double* base, uint64_t ld);
 
 // RAII timing scope for one kernel family (no-op unless profiling is on).
-enum ProfFamily { kProfFactor = 0, kProfCorePass, kProfCoreGemm, kProfCoreSolve, kProfResid, kProfResp, kProfPrune };
+enum ProfFamily {
+  kProfFactor = 0,  // factor-row update, modes 0..N-2 (and the last mode when not fused)
+  kProfCorePass,
+  kProfCoreGemm,
+  kProfCoreSolve,
+  kProfResid,
+  kProfResp,
+  kProfPrune,
+  kProfFactorFused  // last mode with the fused residual
+};
 struct ProfScope {
   Ctx& c;
   int fam;

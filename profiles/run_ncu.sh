@@ -1,7 +1,7 @@
 #!/bin/bash
-# ncu recipe (run under gpurun on one B200): launch list + full capture of the
-# top kernels of one CD iteration of the bench workload.  Outputs land in
-# gpurun_out/ and summaries are copied into profiles/ by hand.
+# ncu recipe (run under gpurun on one B200): the launch list of one bench step
+# (cold-cache, serialised per-launch times) and a full capture of the top
+# kernels.  Summaries are extracted by profiles/summarize_ncu.py into profiles/.
 set -e
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu"
 mkdir -p gpurun_out
@@ -10,5 +10,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 $CMD > gpurun_out/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"${NCU_KERNELS:-k_rowpass|k_core_pass_s|k_core_gemm|k_core_solve}" -s ${NCU_SKIP:-0} -c ${NCU_COUNT:-8} \
+    -k regex:"${NCU_KERNELS:-k_rowpass|k_core_pass_s|k_core_gemm_tc|k_core_solve|k_pack_uw}" -s ${NCU_SKIP:-0} -c ${NCU_COUNT:-8} \
     -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
