@@ -219,6 +219,10 @@ __device__ __forceinline__ void delta_prefixN(const GA& g, const double (&u)[NE]
 #define VEST_FULL_UNROLL 0
 #endif
 constexpr int kFullUnrollN = VEST_FULL_UNROLL;
+#ifndef VEST_K0_UNROLL
+#define VEST_K0_UNROLL 2
+#endif
+constexpr int kK0Unroll = VEST_K0_UNROLL;  // unroll of the rolled k0 loop
 
 template <class S, int n, int NE, class GA>
 __device__ __forceinline__ void delta_staticN(const GA& g, const double (&u)[NE][S::N][S::MAXJ],
@@ -247,7 +251,7 @@ __device__ __forceinline__ void delta_staticN(const GA& g, const double (&u)[NE]
     }
     return;
   }
-#pragma unroll 1
+#pragma unroll kK0Unroll
   for (int a = 0; a < S::J(k0); ++a) {
     double w0[NE];
 #pragma unroll

@@ -21,6 +21,7 @@
 // accumulates the next block, and a final pass applies the last block and sums
 // r^2 (the residual/RE of compute_residuals, tucker_model.hpp:168-183).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "vest_common.cuh"
@@ -632,7 +633,20 @@ cudaError_t core_pass_structured(const void* ops, const DevModel& m, const DevCS
 cudaError_t core_pack_structured(const void* ops, const DevModel& m, const DevCSF& csf, uint64_t p0, uint64_t p1,
                                  double* U, double* W, uint64_t wstride, cudaStream_t s);
 
+void core_sweep_sall(Ctx& c, const void* ops, int reg, double lambda, const std::vector<int>& prefixes,
+                     const std::vector<int>& starts);
+
 namespace {
+
+// VEST_CORE_BLOCK_PASSES=1: the per-block statistics passes (packed operands,
+// one GEMM per block) instead of the all-prefix sweep -- kept for A/B timing.
+bool legacy_block_passes() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_CORE_BLOCK_PASSES");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 
 struct Blocks {
   std::vector<uint32_t> fib;    // fibers of all blocks, row-major order
@@ -858,6 +872,10 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
   if (b.fib.empty()) return;  // fully pruned core: nothing to update
   upload_fibers(c, b);
+  if (sops && c.N == 3 && !legacy_block_passes()) {
+    core_sweep_sall(c, sops, reg, lambda, b.prefix, b.start);
+    return;
+  }
   if (sops) pack_operands(c, sops);
   const int stride = F * (F + 1) / 2 + F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);

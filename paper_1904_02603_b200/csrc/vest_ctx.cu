@@ -353,6 +353,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
     if (reg == 1) l1_empty_rows(c, mode, lambda);
   }
   c.r_valid = false;
+  c.r_pending = -1;
   c.r_fresh = false;
   c.table_valid = false;
   if (fuse) {
@@ -435,11 +436,15 @@ void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, 
   cudaFree(dhv);
   cudaFree(dem);
   c.r_valid = false;
+  c.r_pending = -1;
     c.r_fresh = false;
   c.table_valid = false;
 }
 
+bool core_apply_pending(Ctx& c);
+
 void compute_residual(Ctx& c) {
+  if (core_apply_pending(c)) return;  // r lacks only the last core block's update
   const int m = c.N - 1;
   RowPassArgs a = row_args(c, m);
   ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);
@@ -538,6 +543,7 @@ void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const do
   }
   check(cudaStreamSynchronize(c.stream), "set_model");
   c.r_valid = false;
+  c.r_pending = -1;
     c.r_fresh = false;
   c.table_valid = false;
 }
@@ -747,6 +753,7 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_dg);
   cudaFree(c.d_pack_u);
   cudaFree(c.d_pack_w);
+  cudaFree(c.d_counter);
   cudaFree(c.d_counts);
   cudaFree(c.d_sel);
   if (c.h_small) cudaFreeHost(c.h_small);
@@ -986,6 +993,7 @@ int vest_prune_step(vest_ctx* h, double pr, const double* core_resp, const doubl
     }
     prune(c, pr, counts);
     c.r_valid = false;
+    c.r_pending = -1;
     c.r_fresh = false;
     c.table_valid = false;
   });
@@ -1005,6 +1013,7 @@ int vest_normalize_columns(vest_ctx* h) {
     set_dev(c);
     normalize_columns(c);
     c.r_valid = false;
+    c.r_pending = -1;
     c.r_fresh = false;
     c.table_valid = false;
   });

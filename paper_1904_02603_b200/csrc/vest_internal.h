@@ -143,6 +143,8 @@ struct Ctx {
   double* d_r = nullptr;  // CSF order of mode N-1
   bool r_valid = false;   // r, sum_sq and re match the current model
   bool r_fresh = false;   // r matches the current model (sum_sq not computed)
+  int r_pending = -1;     // r still lacks the last core block's update (prefix; d_dg holds its dg)
+  const void* r_pending_ops = nullptr;
   double sum_sq = 0.0, re = 0.0;
 
   double* d_resp_core = nullptr;
@@ -162,6 +164,7 @@ struct Ctx {
   double* d_dg = nullptr;          size_t dg_cap = 0;
   double* d_pack_u = nullptr;      size_t pack_u_cap = 0;   // structured core pass operands
   double* d_pack_w = nullptr;      size_t pack_w_cap = 0;
+  unsigned* d_counter = nullptr;   // last-CTA arrival counter (block pass)
   unsigned long long* d_counts = nullptr;  // prune / sparsity counters
   void* d_sel = nullptr;           // radix-select state
 
