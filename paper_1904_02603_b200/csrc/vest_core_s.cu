@@ -266,100 +266,166 @@ __device__ __forceinline__ void tri_pair(int p, int n, int& i, int& j) {
 
 // S_p for every prefix p of one chunk per warp (persistent over chunks).
 // FP64 pipe, lane-owned outputs: lane l owns the pairs l, l+32, ... for every
-// p, so the chunk's sums need no cross-lane reduction.  The 32 entries of a
-// round are staged (w^2, u) in shared memory and read back as broadcasts.
+// p, so the chunk's sums need no cross-lane reduction.  Rounds of 32 entries
+// are staged in shared memory by cp.async one round ahead (double buffer;
+// the coordinates two rounds ahead), so the FMA loop never waits on the L2
+// gathers; a per-round fix-up pass squares the weights in place and writes
+// the raw ones (W, SoA) for the block passes.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// staged row stride: [w | u] padded to == 4 (mod 16) doubles, so the DMMA
+// fragment loads (4 rows x 4..8 columns per half-warp) are conflict-free
+__host__ __device__ constexpr int sall_ldr(int P, int F) {
+  return (((P + 1) & ~1) + ((F + 1) & ~1)) + ((4 - (((P + 1) & ~1) + ((F + 1) & ~1)) % 16) + 16) % 16;
+}
+
 template <class S>
 __global__ void __launch_bounds__(kAllWarps * 32, 2) k_core_sall(DevModel m, DevCSF csf, double* stats, double* W,
                                                                  uint64_t wstride) {
   static_assert(S::N == 3, "all-prefix statistics: 3-mode shapes");
-  constexpr int P = S::J(0), F = S::J(1), NV = F * (F + 1) / 2, KP = (NV + 31) / 32;
+  constexpr int P = S::J(0), F = S::J(1), NV = F * (F + 1) / 2;
   constexpr int ld0 = (P + 1) & ~1, ld1 = (F + 1) & ~1;
-  __shared__ __align__(16) double ws[kAllWarps][32 * ld0];
-  __shared__ __align__(16) double us[kAllWarps][32 * ld1];
+  constexpr int LDR = sall_ldr(P, F);  // staged row: [w (ld0) | u (ld1) | pad]
+  extern __shared__ __align__(16) double sall_smem[];  // [warp][2][32 * LDR]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* W2 = ws[warp];
-  double* U = us[warp];
-  int pi[KP], pj[KP];
+  double* const stage0 = sall_smem + (size_t)warp * 2 * 32 * LDR;
+  // DMMA tiling: A = w^2 (rows = prefixes, MT tiles), B = u_i u_j (cols =
+  // pairs, NT tiles); fragments A[g][t], B[t][g], D[g][2t + i]
+  constexpr int MT = (P + 7) / 8, NT = (NV + 7) / 8;
+  const int g = lane >> 2, tq = lane & 3;
+  int bi[NT], bj[NT];  // this lane's B-fragment pair (u offsets), per column tile
 #pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    pi[k] = pj[k] = 0;
-    if (lane + 32 * k < NV) tri_pair(lane + 32 * k, F, pi[k], pj[k]);
+  for (int nt = 0; nt < NT; ++nt) {
+    bi[nt] = bj[nt] = -1;
+    if (8 * nt + g < NV) tri_pair(8 * nt + g, F, bi[nt], bj[nt]);
   }
-  for (uint32_t ci = blockIdx.x * kAllWarps + warp; ci < csf.nchunks; ci += gridDim.x * kAllWarps) {
-    const Chunk ch = csf.chunks[ci];
-    double acc[KP][P];
+  const uint32_t stride = gridDim.x * kAllWarps;
+  // round cursor: (chunk, base); advance = next 32 entries of the chunk, else
+  // the warp's next chunk
+  struct Cur {
+    uint32_t ci, beg, end, base;
+  };
+  auto first = [&](uint32_t ci) {
+    Cur c{ci, 0, 0, 0};
+    if (ci < csf.nchunks) {
+      const Chunk ch = csf.chunks[ci];
+      c.beg = ch.beg;
+      c.end = ch.end;
+      c.base = ch.beg;
+    }
+    return c;
+  };
+  auto next = [&](const Cur& c) {
+    if (c.base + 32 < c.end) return Cur{c.ci, c.beg, c.end, c.base + 32};
+    return first(c.ci + stride);
+  };
+  // issue round c's row copies into buffer b (coordinates already loaded)
+  auto issue = [&](const Cur& c, int b, uint32_t i0, uint32_t i1) {
+    double* row = stage0 + b * 32 * LDR + lane * LDR;
+    if (c.ci < csf.nchunks && c.base + lane < c.end) {
+      const double* r0 = m.factor[0] + (size_t)i0 * ld0;
+      const double* r1 = m.factor[1] + (size_t)i1 * ld1;
 #pragma unroll
-    for (int k = 0; k < KP; ++k)
+      for (int t = 0; t < ld0 / 2; ++t) cp_async16(row + 2 * t, r0 + 2 * t);
 #pragma unroll
-      for (int b = 0; b < P; ++b) acc[k][b] = 0.0;
-    for (uint32_t base = ch.beg; base < ch.end; base += 32) {
-      const uint32_t pos = base + lane;
-      if (pos < ch.end) {
-        const uint32_t i0 = __ldg(csf.oc[0] + pos), i1 = __ldg(csf.oc[1] + pos);
-        const double2* r0 = reinterpret_cast<const double2*>(m.factor[0] + (size_t)i0 * ld0);
-        const double2* r1 = reinterpret_cast<const double2*>(m.factor[1] + (size_t)i1 * ld1);
+      for (int t = 0; t < ld1 / 2; ++t) cp_async16(row + ld0 + 2 * t, r1 + 2 * t);
+    } else {
+      // zero weight: padded entries contribute nothing
+#pragma unroll
+      for (int t = 0; t < LDR; ++t) row[t] = 0.0;
+    }
+  };
+  auto coords = [&](const Cur& c, uint32_t& i0, uint32_t& i1) {
+    i0 = i1 = 0;
+    if (c.ci < csf.nchunks && c.base + lane < c.end) {
+      i0 = __ldg(csf.oc[0] + c.base + lane);
+      i1 = __ldg(csf.oc[1] + c.base + lane);
+    }
+  };
+
+  Cur cur = first(blockIdx.x * kAllWarps + warp);
+  if (cur.ci >= csf.nchunks) return;
+  uint32_t a0, a1;
+  coords(cur, a0, a1);
+  issue(cur, 0, a0, a1);
+  Cur nxt = next(cur);
+  uint32_t n0, n1;
+  coords(nxt, n0, n1);
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  int buf = 0;
+  while (true) {
+    // this round's rows have landed: square the weights (and emit the raw ones)
+    cp_async_wait_all();
+    __syncwarp();
+    {
+      double* row = stage0 + buf * 32 * LDR + lane * LDR;
+      const uint32_t pos = cur.base + lane;
+      if (pos < cur.end) {
 #pragma unroll
         for (int t = 0; t < ld0 / 2; ++t) {
-          const double2 v = __ldg(r0 + t);
-          reinterpret_cast<double2*>(W2 + lane * ld0)[t] = make_double2(v.x * v.x, v.y * v.y);
-          // the block passes' weights, SoA in this CSF order (coalesced there)
+          const double2 v = reinterpret_cast<const double2*>(row)[t];
           __stcs(W + (uint64_t)(2 * t) * wstride + pos, v.x);
           if (2 * t + 1 < P) __stcs(W + (uint64_t)(2 * t + 1) * wstride + pos, v.y);
+          reinterpret_cast<double2*>(row)[t] = make_double2(v.x * v.x, v.y * v.y);
         }
-#pragma unroll
-        for (int t = 0; t < ld1 / 2; ++t) reinterpret_cast<double2*>(U + lane * ld1)[t] = __ldg(r1 + t);
-      } else {
-        // zero weight: padded entries contribute nothing (fixed trip count below)
-#pragma unroll
-        for (int t = 0; t < ld0 / 2; ++t) reinterpret_cast<double2*>(W2 + lane * ld0)[t] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int t = 0; t < ld1 / 2; ++t) reinterpret_cast<double2*>(U + lane * ld1)[t] = make_double2(0.0, 0.0);
       }
-      __syncwarp();
-      // entries in pairs (the odd tail is a zero-weight pad); operands of the
-      // next entry are loaded while the current entry's FMAs issue
-      const int n = ((int)min(32u, ch.end - base) + 1) & ~1;
-      double wc[ld0], uc[KP][2];
-      auto load = [&](int e, double (&w)[ld0], double (&uq)[KP][2]) {
-        const double2* w2 = reinterpret_cast<const double2*>(W2 + e * ld0);
-#pragma unroll
-        for (int t = 0; t < ld0 / 2; ++t) {
-          const double2 v = w2[t];
-          w[2 * t] = v.x;
-          w[2 * t + 1] = v.y;
-        }
-        const double* u = U + e * ld1;
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          uq[k][0] = u[pi[k]];
-          uq[k][1] = u[pj[k]];
-        }
-      };
-      auto fmas = [&](const double (&w)[ld0], const double (&uq)[KP][2]) {
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          const double uu = uq[k][0] * uq[k][1];
-#pragma unroll
-          for (int b = 0; b < P; ++b) acc[k][b] = fma(w[b], uu, acc[k][b]);
-        }
-      };
-      load(0, wc, uc);
-#pragma unroll 1
-      for (int e = 0; e < n; e += 2) {
-        double wn[ld0], un[KP][2];
-        load(e + 1, wn, un);
-        fmas(wc, uc);
-        if (e + 2 < n) load(e + 2, wc, uc);
-        fmas(wn, un);
-      }
-      __syncwarp();
     }
-    double* out = stats + (size_t)ci * (P * NV);
+    __syncwarp();
+    // next round's copies go out now (their coordinates arrived a round ago)
+    const bool more = nxt.ci < csf.nchunks;
+    if (more) issue(nxt, buf ^ 1, n0, n1);
+    const Cur nn = more ? next(nxt) : nxt;
+    uint32_t m0 = 0, m1 = 0;
+    if (more) coords(nn, m0, m1);
+    // X^T-style product over this round on the FP64 tensor cores: 8 k-steps
+    // of 4 entries (rows past the chunk end were zeroed at staging)
+    {
+      const double* st = stage0 + buf * 32 * LDR;
+      const int nk = (int)(min(32u, cur.end - cur.base) + 3) >> 2;
+#pragma unroll 2
+      for (int kk = 0; kk < nk; ++kk) {
+        const double* row = st + (4 * kk + tq) * LDR;
+        double a[MT];
 #pragma unroll
-    for (int k = 0; k < KP; ++k)
-      if (lane + 32 * k < NV)
+        for (int mt = 0; mt < MT; ++mt) a[mt] = (8 * mt + g < P) ? row[8 * mt + g] : 0.0;
 #pragma unroll
-        for (int b = 0; b < P; ++b) out[b * NV + lane + 32 * k] = acc[k][b];
+        for (int nt = 0; nt < NT; ++nt) {
+          const double b = bi[nt] >= 0 ? row[ld0 + bi[nt]] * row[ld0 + bj[nt]] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b);
+        }
+      }
+    }
+    // chunk finished: write its statistics
+    if (!more || nxt.ci != cur.ci) {
+      double* out = stats + (size_t)cur.ci * (P * NV);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int b = 8 * mt + g, pr = 8 * nt + 2 * tq + i;
+            if (b < P && pr < NV) out[b * NV + pr] = acc[mt][nt][i];
+            acc[mt][nt][i] = 0.0;
+          }
+    }
+    if (!more) break;
+    __syncwarp();
+    cur = nxt;
+    nxt = nn;
+    n0 = m0;
+    n1 = m1;
+    buf ^= 1;
   }
 }
 
@@ -859,7 +925,10 @@ template <class S>
 cudaError_t run_core_sall(const DevModel& m, const DevCSF& csf, double* stats, double* W, uint64_t wstride,
                           int grid, cudaStream_t s) {
   if (csf.nchunks == 0) return cudaSuccess;
-  k_core_sall<S><<<grid, kAllWarps * 32, 0, s>>>(m, csf, stats, W, wstride);
+  constexpr int LDR = sall_ldr(S::J(0), S::J(1));
+  const int smem = kAllWarps * 2 * 32 * LDR * (int)sizeof(double);
+  cudaFuncSetAttribute(k_core_sall<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_core_sall<S><<<grid, kAllWarps * 32, smem, s>>>(m, csf, stats, W, wstride);
   count_launch();
   return cudaGetLastError();
 }
@@ -1011,7 +1080,7 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   double* Cb = Hd + nH;                                    // [C (nq) | sum r^2]
   {
     ProfScope ps(c, kProfCorePass);
-    check(ops->sall(mv, csf, c.d_chunk_stats, c.d_pack_w, c.nnz, 2 * sms * 4, c.stream),
+    check(ops->sall(mv, csf, c.d_chunk_stats, c.d_pack_w, c.nnz, 2 * sms, c.stream),
           "core all-prefix statistics");
   }
   {
