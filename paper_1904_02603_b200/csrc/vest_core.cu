@@ -635,6 +635,7 @@ cudaError_t core_pack_structured(const void* ops, const DevModel& m, const DevCS
 
 void core_sweep_sall(Ctx& c, const void* ops, int reg, double lambda, const std::vector<int>& prefixes,
                      const std::vector<int>& starts);
+const void* find_core_all_ops(int N, const int* J);
 
 namespace {
 
@@ -872,9 +873,11 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
   if (b.fib.empty()) return;  // fully pruned core: nothing to update
   upload_fibers(c, b);
-  if (sops && c.N == 3 && !legacy_block_passes()) {
-    core_sweep_sall(c, sops, reg, lambda, b.prefix, b.start);
-    return;
+  if (sops && !legacy_block_passes()) {
+    if (const void* aops = find_core_all_ops(c.N, c.ranks)) {
+      core_sweep_sall(c, aops, reg, lambda, b.prefix, b.start);
+      return;
+    }
   }
   if (sops) pack_operands(c, sops);
   const int stride = F * (F + 1) / 2 + F;

@@ -353,7 +353,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
     if (reg == 1) l1_empty_rows(c, mode, lambda);
   }
   c.r_valid = false;
-  c.r_pending = -1;
+  c.r_pending[0] = c.r_pending[1] = -1;
   c.r_fresh = false;
   c.table_valid = false;
   if (fuse) {
@@ -436,7 +436,7 @@ void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, 
   cudaFree(dhv);
   cudaFree(dem);
   c.r_valid = false;
-  c.r_pending = -1;
+  c.r_pending[0] = c.r_pending[1] = -1;
     c.r_fresh = false;
   c.table_valid = false;
 }
@@ -543,7 +543,7 @@ void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const do
   }
   check(cudaStreamSynchronize(c.stream), "set_model");
   c.r_valid = false;
-  c.r_pending = -1;
+  c.r_pending[0] = c.r_pending[1] = -1;
     c.r_fresh = false;
   c.table_valid = false;
 }
@@ -993,7 +993,7 @@ int vest_prune_step(vest_ctx* h, double pr, const double* core_resp, const doubl
     }
     prune(c, pr, counts);
     c.r_valid = false;
-    c.r_pending = -1;
+    c.r_pending[0] = c.r_pending[1] = -1;
     c.r_fresh = false;
     c.table_valid = false;
   });
@@ -1013,7 +1013,7 @@ int vest_normalize_columns(vest_ctx* h) {
     set_dev(c);
     normalize_columns(c);
     c.r_valid = false;
-    c.r_pending = -1;
+    c.r_pending[0] = c.r_pending[1] = -1;
     c.r_fresh = false;
     c.table_valid = false;
   });

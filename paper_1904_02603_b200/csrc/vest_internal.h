@@ -143,7 +143,7 @@ struct Ctx {
   double* d_r = nullptr;  // CSF order of mode N-1
   bool r_valid = false;   // r, sum_sq and re match the current model
   bool r_fresh = false;   // r matches the current model (sum_sq not computed)
-  int r_pending = -1;     // r still lacks the last core block's update (prefix; d_dg holds its dg)
+  int r_pending[2] = {-1, -1};  // r still lacks the last core group's update (prefixes; d_dg holds the dg)
   const void* r_pending_ops = nullptr;
   double sum_sq = 0.0, re = 0.0;
 

@@ -1,7 +1,7 @@
-// Microbenchmark (tooling): the core-block solve kernel alone, phase clocks.
+// Microbenchmark (tooling): the core-block solve kernel alone, single block and pair group.
 //   nvcc -O3 -std=c++17 --expt-relaxed-constexpr -gencode arch=compute_100a,code=sm_100a \
-//        -DVEST_SOLVE_CLOCKS -Ipaper_1904_02603_b200/csrc -o build/ubench_solve profiles/ubench_solve.cu
-#include "vest_core_s.cu"
+//        -Ipaper_1904_02603_b200/csrc -o build/ubench_solve profiles/ubench_solve.cu
+#include "vest_core_sall.cu"
 #include <cstdio>
 #include <vector>
 namespace vest {
@@ -16,11 +16,11 @@ DevCSF Ctx::csf_view(int) const { return {}; }
 using namespace vest;
 int main() {
   const int nf = 10, Jm = 10, NS = 55, NAm = 55, nq = 100;
-  std::vector<double> T(NS * NAm), C(nq + 1), core(1000);
+  std::vector<double> T(NS * NAm), C(2 * nq + 1), core(1000);
   for (int i = 0; i < NS * NAm; ++i) T[i] = 1e-3 * ((i * 7919) % 101);
   for (int f = 0; f < nf; ++f)  // dominant diagonal
-    for (int c = 0; c < Jm; ++c) T[tri_s_host(f, f, nf) * NAm + tri_s_host(c, c, Jm)] += 10.0;
-  for (int i = 0; i <= nq; ++i) C[i] = 0.1 * (i % 13);
+    for (int c = 0; c < Jm; ++c) T[tri_idx(f, f, nf) * NAm + tri_idx(c, c, Jm)] += 10.0;
+  for (int i = 0; i <= 2 * nq; ++i) C[i] = 0.1 * (i % 13);
   for (int i = 0; i < 1000; ++i) core[i] = 0.01 * (i % 17);
   std::vector<uint32_t> fib(nf);
   for (int f = 0; f < nf; ++f) fib[f] = 30 + f;
@@ -34,27 +34,28 @@ int main() {
   cudaMemcpy(dcore, core.data(), 8000, cudaMemcpyHostToDevice);
   cudaMemcpy(dfib, fib.data(), 4 * nf, cudaMemcpyHostToDevice);
   cudaMemset(dmask, 0, 1000);
-  const size_t smem = ((size_t)nq * nq + kSolveSlack + nq) * 8;
+  const size_t smem = (2 * (h_stride(nq) + kSolveSlack) + 2 * nq) * 8;
   double* dH;
   cudaMalloc(&dH, nq * nq * 8 + 16);
   k_expand_h<<<40, 256>>>(dT, 1, nf, Jm, dH);
-  cudaFuncSetAttribute(k_core_solve_s<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_core_solve_s<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_core_solve_g<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_core_solve_g<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int reg = 0; reg < 2; ++reg) {
-    auto kern = reg == 0 ? k_core_solve_s<0> : k_core_solve_s<1>;
-    kern<<<1, 32, smem>>>(dH, dC, nf, Jm, dfib, dcore, dmask, 0.01, ddg, ds);
+    auto kern = reg == 0 ? k_core_solve_g<0> : k_core_solve_g<1>;
+    for (int two = 0; two < 2; ++two) {
+    const double* Hb = two ? dH : nullptr;
+    kern<<<1, 32, smem>>>(dH, Hb, Hb, dC, nf, Jm, dfib, dfib, dcore, dmask, 0.01, ddg, ds);
     cudaEventRecord(e0);
-    for (int i = 0; i < 100; ++i) kern<<<1, 32, smem>>>(dH, dC, nf, Jm, dfib, dcore, dmask, 0.01, ddg, ds);
+    for (int i = 0; i < 100; ++i) kern<<<1, 32, smem>>>(dH, Hb, Hb, dC, nf, Jm, dfib, dfib, dcore, dmask, 0.01, ddg, ds);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    long long clk[4];
-    cudaMemcpyFromSymbol(clk, vest_solve_clocks, sizeof(clk));
-    printf("reg %d: %.2f us/launch; phases (cycles): load H %lld, sync %lld, init %lld, GS %lld  err=%s\n", reg,
-           ms * 10, clk[0], clk[1], clk[2], clk[3], cudaGetErrorString(cudaGetLastError()));
+    printf("reg %d, %s: %.2f us/launch  err=%s\n", reg, two ? "pair" : "single", ms * 10,
+           cudaGetErrorString(cudaGetLastError()));
+    }
   }
   return 0;
 }
