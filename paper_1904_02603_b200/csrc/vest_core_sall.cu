@@ -248,21 +248,32 @@ __global__ void __launch_bounds__(kAllWarps * 32) k_core_sall(DevModel m, DevCSF
 
 // ------------------------------------------------------------------ GEMM --
 // Every block Gram at once: out[(r, ff'), cc'] = sum_chunks S[chunk][(r, ff')]
-// a_c a_c' on DMMA.  grid = (K splits, 64-row groups); warp w owns the 8-row
-// tile w of its group against all column tiles; the next 32-chunk batch is
-// prefetched into registers while the current one runs.
+// a_c a_c' on DMMA.  grid = (K splits, 128-row groups); warp w owns the 8-row
+// tiles w and w + 8 of its group against all column tiles (each B fragment
+// feeds two MMAs); the next 32-chunk batch is prefetched into registers while
+// the current one runs.
+constexpr int kSgRows = 128;
+// staging element t -> (row r, chunk k): each warp access covers 8 rows x 4
+// chunks, i.e. 4 runs of 8 consecutive doubles in global memory and 2-way
+// (minimal) bank use in the transposed tile (row stride kSgLd == 4 mod 16)
+__device__ __forceinline__ void lt_coord(int t, int& r, int& k) {
+  const int lane = t & 31, wi = t >> 5;
+  r = (wi % (kSgRows / 8)) * 8 + (lane & 7);
+  k = (wi / (kSgRows / 8)) * 4 + (lane >> 3);
+}
 template <class S>
 __global__ void __launch_bounds__(256) k_sall_gemm(const double* stats, int LW, const Chunk* chunks,
                                                    uint32_t nchunks, const double* A, double* partial) {
   constexpr int Jm = S::J(2), NAm = Jm * (Jm + 1) / 2, NT = (NAm + 7) / 8;
   constexpr int ld2 = (Jm + 1) & ~1;
-  __shared__ double Lt[64 * kSgLd];
-  __shared__ double Rt[NT * 8 * kSgLd];
-  __shared__ double sa[32 * Jm];
+  extern __shared__ __align__(16) double sg_smem[];
+  double* Lt = sg_smem;                    // [kSgRows][kSgLd]
+  double* Rt = Lt + kSgRows * kSgLd;       // [NT * 8][kSgLd]
+  double* sa = Rt + NT * 8 * kSgLd;        // [32][Jm]
   __shared__ int rmap[NT * 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int row0 = blockIdx.y * 64;
+  const int row0 = blockIdx.y * kSgRows;
   for (int col = threadIdx.x; col < NT * 8; col += blockDim.x) {
     int v = -1;
     if (col < NAm) {
@@ -275,17 +286,19 @@ __global__ void __launch_bounds__(256) k_sall_gemm(const double* stats, int LW, 
   const uint32_t per = ((nchunks + gridDim.x - 1) / gridDim.x + 31) & ~31u;
   const uint32_t c0 = blockIdx.x * per;
   const uint32_t c1 = min(nchunks, c0 + per);
-  double acc[NT][2];
+  double acc[2][NT][2];
 #pragma unroll
-  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-  constexpr int kL = 64 * 32 / 256, kA = (32 * Jm + 255) / 256;
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[h][t][0] = acc[h][t][1] = 0.0;
+  constexpr int kL = kSgRows * 32 / 256, kA = (32 * Jm + 255) / 256;
   double lv[kL], av[kA];
   auto prefetch = [&](uint32_t cb) {
     const int nb = (int)min(32u, c1 - cb);
 #pragma unroll
     for (int i = 0; i < kL; ++i) {
-      const int t = threadIdx.x + 256 * i;
-      const int k = t >> 6, r = t & 63;
+      int r, k;
+      lt_coord(threadIdx.x + 256 * i, r, k);
       lv[i] = (k < nb && row0 + r < LW) ? __ldcs(stats + (size_t)(cb + k) * LW + row0 + r) : 0.0;
     }
 #pragma unroll
@@ -300,8 +313,9 @@ __global__ void __launch_bounds__(256) k_sall_gemm(const double* stats, int LW, 
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kL; ++i) {
-      const int t = threadIdx.x + 256 * i;
-      Lt[(t & 63) * kSgLd + (t >> 6)] = lv[i];
+      int r, k;
+      lt_coord(threadIdx.x + 256 * i, r, k);
+      Lt[r * kSgLd + k] = lv[i];
     }
 #pragma unroll
     for (int i = 0; i < kA; ++i) {
@@ -316,24 +330,38 @@ __global__ void __launch_bounds__(256) k_sall_gemm(const double* stats, int LW, 
     }
     __syncthreads();
     if (cb + 32 < c1) prefetch(cb + 32);
-    const double* la = Lt + (8 * warp + g) * kSgLd + tq;
+    const double* la0 = Lt + (8 * warp + g) * kSgLd + tq;
+    const double* la1 = Lt + (8 * (warp + 8) + g) * kSgLd + tq;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const double a = la[4 * kk];
+      const double a0 = la0[4 * kk], a1 = la1[4 * kk];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) dmma884(acc[t][0], acc[t][1], a, Rt[(8 * t + g) * kSgLd + tq + 4 * kk]);
+      for (int t = 0; t < NT; ++t) {
+        const double b = Rt[(8 * t + g) * kSgLd + tq + 4 * kk];
+        dmma884(acc[0][t][0], acc[0][t][1], a0, b);
+        dmma884(acc[1][t][0], acc[1][t][1], a1, b);
+      }
     }
   }
-  const int row = row0 + 8 * warp + g;
-  if (row >= LW) return;
-  double* out = partial + (size_t)blockIdx.x * LW * NAm + (size_t)row * NAm;
 #pragma unroll
-  for (int t = 0; t < NT; ++t)
+  for (int h = 0; h < 2; ++h) {
+    const int row = row0 + 8 * (warp + 8 * h) + g;
+    if (row >= LW) continue;
+    double* out = partial + (size_t)blockIdx.x * LW * NAm + (size_t)row * NAm;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int col = 8 * t + 2 * tq + i;
-      if (col < NAm) out[col] = acc[t][i];
-    }
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int col = 8 * t + 2 * tq + i;
+        if (col < NAm) out[col] = acc[h][t][i];
+      }
+  }
+}
+
+template <class S>
+constexpr int sgemm_smem() {
+  constexpr int NT = (S::J(2) * (S::J(2) + 1) / 2 + 7) / 8;
+  return (kSgRows * kSgLd + NT * 8 * kSgLd + 32 * S::J(2)) * (int)sizeof(double);
 }
 
 __global__ void k_colsum_s(const double* partial, int nparts, int n, double* out) {
@@ -839,8 +867,9 @@ int rpass_occupancy() {
 template <class S>
 cudaError_t run_sall_gemm(const double* stats, int LW, const Chunk* chunks, uint32_t nchunks, const double* A,
                           double* partial, int ksplit, cudaStream_t s) {
-  const dim3 grid(ksplit, (LW + 63) / 64);
-  k_sall_gemm<S><<<grid, 256, 0, s>>>(stats, LW, chunks, nchunks, A, partial);
+  const dim3 grid(ksplit, (LW + kSgRows - 1) / kSgRows);
+  cudaFuncSetAttribute(k_sall_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgemm_smem<S>());
+  k_sall_gemm<S><<<grid, 256, sgemm_smem<S>(), s>>>(stats, LW, chunks, nchunks, A, partial);
   count_launch();
   return cudaGetLastError();
 }
@@ -915,7 +944,9 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
   const size_t nT = (size_t)LW * NAm;
-  const int ksplit = std::max(1, std::min<int>(64, (int)((csf.nchunks + 1023) / 1024)));
+  // one wave: (K splits) x (row groups) == 2 CTAs per SM
+  const int gy = (LW + kSgRows - 1) / kSgRows;
+  const int ksplit = std::max(1, std::min<int>((2 * sms) / gy, (int)((csf.nchunks + 255) / 256)));
   const int rgrid = rpass_grid(c, ops);
   const size_t hs = h_stride(nq);
   const size_t nH = (size_t)RW * hs + 2;  // (+2: bulk copies round up to 16 bytes)
