@@ -525,6 +525,47 @@ int guard(F&& f) {
 
 void set_dev(const Ctx& c) { check(cudaSetDevice(c.device), "cudaSetDevice"); }
 
+// packed [rows][J] <-> strided [rows][ld] on the device (ld = J rounded up to
+// even): host transfers stay single contiguous DMAs
+__global__ void k_restride(const double* src, int sld, double* dst, int dld, int J, uint64_t rows) {
+  const uint64_t n = rows * (uint64_t)J;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = t / J;
+    const int j = (int)(t - r * J);
+    dst[r * dld + j] = src[r * sld + j];
+  }
+}
+
+void copy_factor_h2d(Ctx& c, int n, const double* host) {
+  const int J = c.ranks[n];
+  const size_t bytes = c.dims[n] * J * sizeof(double);
+  if (c.ld[n] == J) {
+    check(cudaMemcpyAsync(c.d_factor[n], host, bytes, cudaMemcpyHostToDevice, c.stream), "factor");
+    return;
+  }
+  ensure(c, &c.d_xfer, &c.xfer_cap, c.dims[n] * J);
+  check(cudaMemcpyAsync(c.d_xfer, host, bytes, cudaMemcpyHostToDevice, c.stream), "factor");
+  k_restride<<<592, 256, 0, c.stream>>>(c.d_xfer, J, c.d_factor[n], c.ld[n], J, c.dims[n]);
+  count_launch();
+  check(cudaGetLastError(), "factor restride");
+}
+
+void copy_factor_d2h(Ctx& c, int n, double* host) {
+  const int J = c.ranks[n];
+  const size_t bytes = c.dims[n] * J * sizeof(double);
+  if (c.ld[n] == J) {
+    check(cudaMemcpyAsync(host, c.d_factor[n], bytes, cudaMemcpyDeviceToHost, c.stream), "factor");
+    return;
+  }
+  ensure(c, &c.d_xfer, &c.xfer_cap, c.dims[n] * J);
+  k_restride<<<592, 256, 0, c.stream>>>(c.d_factor[n], c.ld[n], c.d_xfer, J, J, c.dims[n]);
+  count_launch();
+  check(cudaGetLastError(), "factor restride");
+  check(cudaMemcpyAsync(host, c.d_xfer, bytes, cudaMemcpyDeviceToHost, c.stream), "factor");
+  // (the staging buffer is reused by the next factor: keep the copies ordered)
+  check(cudaStreamSynchronize(c.stream), "factor d2h");
+}
+
 void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const double* const* factors,
                   const uint8_t* const* fmasks) {
   if (core) check(cudaMemcpyAsync(c.d_core, core, c.G * sizeof(double), cudaMemcpyHostToDevice, c.stream), "core");
@@ -534,10 +575,10 @@ void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const do
   }
   for (int n = 0; n < c.N; ++n) {
     const int J = c.ranks[n];
-    if (factors && factors[n])
-      check(cudaMemcpy2DAsync(c.d_factor[n], c.ld[n] * sizeof(double), factors[n], J * sizeof(double),
-                              J * sizeof(double), c.dims[n], cudaMemcpyHostToDevice, c.stream),
-            "factor");
+    if (factors && factors[n]) {
+      copy_factor_h2d(c, n, factors[n]);
+      if (c.ld[n] != J) check(cudaStreamSynchronize(c.stream), "factor h2d");  // staging reuse
+    }
     if (fmasks && fmasks[n])
       check(cudaMemcpyAsync(c.d_fmask[n], fmasks[n], c.dims[n] * J, cudaMemcpyHostToDevice, c.stream), "fmask");
   }
@@ -754,6 +795,7 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_pack_u);
   cudaFree(c.d_pack_w);
   cudaFree(c.d_counter);
+  cudaFree(c.d_xfer);
   cudaFree(c.d_counts);
   cudaFree(c.d_sel);
   if (c.h_small) cudaFreeHost(c.h_small);
@@ -818,10 +860,7 @@ int vest_get_model(vest_ctx* h, double* core, uint8_t* core_mask, double* const*
     if (core_mask) check(cudaMemcpyAsync(core_mask, c.d_core_mask, c.G, cudaMemcpyDeviceToHost, c.stream), "mask");
     for (int n = 0; n < c.N; ++n) {
       const int J = c.ranks[n];
-      if (factors && factors[n])
-        check(cudaMemcpy2DAsync(factors[n], J * sizeof(double), c.d_factor[n], c.ld[n] * sizeof(double),
-                                J * sizeof(double), c.dims[n], cudaMemcpyDeviceToHost, c.stream),
-              "factor");
+      if (factors && factors[n]) copy_factor_d2h(c, n, factors[n]);
       if (factor_masks && factor_masks[n])
         check(cudaMemcpyAsync(factor_masks[n], c.d_fmask[n], c.dims[n] * J, cudaMemcpyDeviceToHost, c.stream),
               "fmask");

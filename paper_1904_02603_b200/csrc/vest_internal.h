@@ -154,6 +154,7 @@ struct Ctx {
 
   // scratch
   double* d_heavy_part = nullptr;  size_t heavy_part_cap = 0;
+  double* d_xfer = nullptr;        size_t xfer_cap = 0;  // packed factor staging (ld != J)
   double* d_chunk_stats = nullptr; size_t chunk_stats_cap = 0;
   double* d_gemm_part = nullptr;   size_t gemm_part_cap = 0;
   double* d_gemm_out = nullptr;    size_t gemm_out_cap = 0;
