@@ -132,14 +132,16 @@ __device__ __forceinline__ void delta_prefix(const GA& g, const double (&u)[S::N
 // its factor value is read per iteration (L1-resident row) and the core index
 // gets a warp-uniform runtime offset, which keeps the unrolled body at
 // |G|/J_k0 cells and the register footprint small.  u[k0] is unused.
-template <class S, int n, class GA>
+// kFull: the k0 loop fully unrolled (every core offset an immediate: uniform
+// constant loads even inside divergent code, e.g. a chunk's tail round)
+template <class S, int n, class GA, bool kFull = false>
 __device__ __forceinline__ void delta_static(const GA& g, const double (&u)[S::N][S::MAXJ],
                                              const double* __restrict__ row_k0,
                                              double (&delta)[S::MAXJ]) {
   constexpr int k0 = (n == 0) ? 1 : 0;
 #pragma unroll
   for (int j = 0; j < S::J(n); ++j) delta[j] = 0.0;
-#pragma unroll 1
+#pragma unroll(kFull ? S::J(k0) : 1)
   for (int a = 0; a < S::J(k0); ++a) {
     const double w0 = __ldg(row_k0 + a);
     const int base = a * S::stride(k0);

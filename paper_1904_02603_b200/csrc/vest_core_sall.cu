@@ -425,6 +425,20 @@ struct RStage {  // one round's staged operands, per warp (doubles)
   static constexpr int A2 = Rr + 32;       // [ld2]
   static constexpr int size = (A2 + ld2 + 1) & ~1;
 };
+// v[i] summed over the warp, scattered: lane l returns with v[0] = sum of v[l]
+// (5 butterfly rounds exchanging 16, 8, 4, 2, 1 values)
+__device__ __forceinline__ void transpose_reduce(double (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool hi = lane & s;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = hi ? v[i] : v[i + s];
+      const double keep = hi ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
@@ -434,6 +448,7 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
   static_assert(S::N == 3, "block pass: 3-mode shapes");
   constexpr int F = S::J(1), Jm = S::J(2), NQ = F * Jm;
   constexpr int NC = 2 * NQ, NP = NC + 1, KC = (NC + 31) / 32;
+  static_assert(2 * F + 1 <= 32, "chunk sums fit one reduce-scatter");
   using RS = RStage<F, Jm>;
   constexpr int ld1 = RS::ld1, ld2 = RS::ld2;
   extern __shared__ __align__(16) double rp_smem[];  // [warp][2][RS::size]
@@ -567,21 +582,22 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
           sq = warp_sum(sq);
           if (lane == 0) a.chunk_sq[cur.ci] = sq;
         } else {
+          {
+            // all 2F (+ sum r^2) chunk sums at once: butterfly reduce-scatter,
+            // lane l ends with sum l (31 exchanges instead of 5 per value)
+            double v[32];
 #pragma unroll
-          for (int f = 0; f < F; ++f) {
-            const double v0 = warp_sum(R0[f]);
-            if (lane == 0) rs[warp][0][f] = v0;
-          }
-          if (nc > 1) {
+            for (int f = 0; f < 32; ++f) v[f] = 0.0;
 #pragma unroll
             for (int f = 0; f < F; ++f) {
-              const double v1 = warp_sum(R1[f]);
-              if (lane == 0) rs[warp][1][f] = v1;
+              v[f] = R0[f];
+              v[F + f] = R1[f];
             }
-          }
-          if (a.want_sq) {
-            sq = warp_sum(sq);
-            if (lane == 0) sqs[warp] += sq;
+            v[2 * F] = sq;
+            transpose_reduce(v, lane);
+            if (lane < F) rs[warp][0][lane] = v[0];
+            else if (lane < 2 * F) rs[warp][1][lane - F] = v[0];
+            else if (lane == 2 * F && a.want_sq) sqs[warp] += v[0];
           }
           __syncwarp();
           // C_j[f][c] += R_j[f] a_c (lane-owned, in shared memory)

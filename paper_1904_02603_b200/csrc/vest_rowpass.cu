@@ -58,6 +58,9 @@ __device__ __forceinline__ void load_row(const double* __restrict__ row, double 
 // A policy computes delta for NE entries per lane: the CSF positions pos[e]
 // (clamped into the chunk by the caller), rows of the other modes gathered.
 template <class S, int MODE>
+#ifndef VEST_ROW_TAIL1
+#define VEST_ROW_TAIL1 0  // measured slower (larger kernel body): 1.36 vs 1.27 ms per mode
+#endif
 struct StaticPolicy {
 #ifndef VEST_CORE_SMEM
 #define VEST_CORE_SMEM 0
@@ -117,7 +120,7 @@ struct StaticPolicy {
           load_row<S::J(k)>(m.factor[k] + (size_t)i * ld, u[k]);
       }
     });
-    delta_static<S, MODE>(ConstCore{}, u, row0, d);
+    delta_static<S, MODE, ConstCore, (bool)VEST_ROW_TAIL1>(ConstCore{}, u, row0, d);
   }
 };
 
@@ -293,6 +296,7 @@ __device__ __forceinline__ void fused_residual(const RowPassArgs& a, const Chunk
 #ifndef VEST_ROW_MINB
 #define VEST_ROW_MINB 2
 #endif
+
 template <class P, int KIND>
 __global__ void __launch_bounds__(kRowWarps * 32, VEST_ROW_MINB) k_rowpass(RowPassArgs a, P pol) {
   extern __shared__ double smem[];
@@ -370,9 +374,20 @@ __global__ void __launch_bounds__(kRowWarps * 32, VEST_ROW_MINB) k_rowpass(RowPa
       }
     } else {
       // lane-uniform validity of the first entry guards the contraction (keeps
-      // the core offsets in uniform registers); later entries are clamped
+      // the core offsets in uniform registers); later entries are clamped.
+      // A chunk's tail of <= 32 entries runs one entry per lane (the empty
+      // second slots would cost the full contraction).
+      const bool tail = VEST_ROW_TAIL1 && P::kStatic && ch.end - base <= 32;
       if (valid[0]) {
-        pol.entries(a.m, a.csf, pos, d);
+        if (tail) {
+          pol.entry1(a.m, a.csf, pos[0], d[0]);
+#pragma unroll
+          for (int e = 1; e < NE; ++e)
+#pragma unroll
+            for (int j = 0; j < MAXJ; ++j) d[e][j] = 0.0;
+        } else {
+          pol.entries(a.m, a.csf, pos, d);
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < NE; ++e)
