@@ -131,6 +131,14 @@ int vest_compute_residuals(vest_ctx* ctx, double* r_out, double* sum_sq, double*
 /* One CD iteration as fit() runs it (trainer.hpp:121-127):
  * update_all_factors + update_core + compute_residuals; returns re. */
 int vest_cd_iteration(vest_ctx* ctx, int reg, double lambda, double* re);
+/* The same iteration on a model held in HOST memory, updated in place (the
+ * reference's calling convention: update_all_factors / update_core mutate the
+ * caller's TuckerModel).  Uploads the model, runs the iteration, and streams
+ * every factor back as soon as its mode is final (overlapping the rest of the
+ * iteration), then the core.  Masks are inputs only (an iteration does not
+ * change them).  Equivalent to set_model + cd_iteration + get_model. */
+int vest_cd_iteration_host(vest_ctx* ctx, double* core, const uint8_t* core_mask, double* const* factors,
+                           const uint8_t* const* factor_masks, int reg, double lambda, double* re);
 /* compute_delta (updates.hpp:35-52) at one coordinate. */
 int vest_compute_delta(vest_ctx* ctx, const uint32_t* at, int mode, double* out);
 /* predict (trainer.hpp:172-185): reconstruction at nq coordinates. */

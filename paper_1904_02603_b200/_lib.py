@@ -44,6 +44,8 @@ SIGNATURES = {
     "vest_update_core": (C.c_int, [vp, C.c_int, C.c_double]),
     "vest_compute_residuals": (C.c_int, [vp, f64p, f64p, f64p, f64p]),
     "vest_cd_iteration": (C.c_int, [vp, C.c_int, C.c_double, f64p]),
+    "vest_cd_iteration_host": (C.c_int, [vp, f64p, u8p, C.POINTER(f64p), C.POINTER(u8p), C.c_int, C.c_double,
+                                         f64p]),
     "vest_compute_delta": (C.c_int, [vp, u32p, C.c_int, f64p]),
     "vest_predict": (C.c_int, [vp, u32p, C.c_uint64, f64p]),
     "vest_evaluate": (C.c_int, [vp, u32p, f64p, C.c_uint64, f64p]),

@@ -800,6 +800,9 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_sel);
   if (c.h_small) cudaFreeHost(c.h_small);
   if (c.stream) cudaStreamDestroy(c.stream);
+  if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+  for (auto& e : c.ev_copy)
+    if (e) cudaEventDestroy(e);
   delete h;
   return VEST_OK;
 }
@@ -950,6 +953,53 @@ int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
     for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda, true);
     core_sweep(c, reg, lambda);
     c.table_valid = false;
+    if (re) *re = c.re;
+  });
+}
+
+int vest_cd_iteration_host(vest_ctx* h, double* core, const uint8_t* core_mask, double* const* factors,
+                           const uint8_t* const* factor_masks, int reg, double lambda, double* re) {
+  Ctx& c = h->c;
+  return guard([&] {
+    check_reg(reg);
+    if (c.x_norm == 0.0) throw ArgError{"zero-norm tensor"};
+    set_dev(c);
+    if (!c.copy_stream) {
+      check(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking), "copy stream");
+      for (auto& e : c.ev_copy) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "copy event");
+    }
+    upload_model(c, core, core_mask, const_cast<const double* const*>(factors), factor_masks);
+    // read-back staging for factors whose device rows are padded (ld != J)
+    uint64_t stage = 0;
+    for (int n = 0; n < c.N; ++n)
+      if (c.ld[n] != c.ranks[n]) stage += c.dims[n] * c.ranks[n];
+    if (stage) ensure(c, &c.d_xfer, &c.xfer_cap, stage);
+    sync_const_core(c);
+    uint64_t off = 0;
+    for (int n = 0; n < c.N; ++n) {
+      update_factor_mode(c, n, reg, lambda, true);
+      // factor n is final for this iteration: copy it out behind the next modes
+      const int J = c.ranks[n];
+      const size_t bytes = c.dims[n] * J * sizeof(double);
+      const double* src = c.d_factor[n];
+      if (c.ld[n] != J) {
+        k_restride<<<592, 256, 0, c.stream>>>(c.d_factor[n], c.ld[n], c.d_xfer + off, J, J, c.dims[n]);
+        count_launch();
+        check(cudaGetLastError(), "factor restride");
+        src = c.d_xfer + off;
+        off += c.dims[n] * J;
+      }
+      if (factors && factors[n]) {
+        check(cudaEventRecord(c.ev_copy[n], c.stream), "copy event");
+        check(cudaStreamWaitEvent(c.copy_stream, c.ev_copy[n], 0), "copy wait");
+        check(cudaMemcpyAsync(factors[n], src, bytes, cudaMemcpyDeviceToHost, c.copy_stream), "factor d2h");
+      }
+    }
+    core_sweep(c, reg, lambda);
+    c.table_valid = false;
+    if (core) check(cudaMemcpyAsync(core, c.d_core, c.G * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "core");
+    check(cudaStreamSynchronize(c.stream), "iteration");
+    check(cudaStreamSynchronize(c.copy_stream), "factor read-back");
     if (re) *re = c.re;
   });
 }

@@ -123,6 +123,8 @@ struct Ctx {
   double prof_ms[8] = {};
   uint64_t prof_n[8] = {};
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host read-back overlapped with compute
+  cudaEvent_t ev_copy[VEST_MAXN + 1] = {};
   int N = 0;
   uint64_t dims[VEST_MAXN] = {};
   int ranks[VEST_MAXN] = {};

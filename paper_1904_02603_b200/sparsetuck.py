@@ -289,6 +289,22 @@ class Device:
         check(self._L.vest_cd_iteration(self.h, int(reg), float(lam), C.byref(re)))
         return re.value
 
+    def cd_iteration_host(self, m: TuckerModel, reg: int, lam: float) -> float:
+        """One CD iteration on a host model, updated in place (vest_cd_iteration_host:
+        upload, iterate, factors streamed back as each mode finishes)."""
+        if list(m.dims) != self.dims or list(m.ranks) != self.ranks:
+            raise ValueError("model/tensor shape mismatch")
+        for a, dt in [(m.core, np.float64), (m.core_mask, np.uint8)] + [(f, np.float64) for f in m.factors] + \
+                [(k, np.uint8) for k in m.factor_masks]:
+            if a.dtype != dt or not a.flags.c_contiguous or not a.flags.writeable:
+                raise ValueError("host model arrays must be writeable C-contiguous float64/uint8")
+        fp = (f64p * self.order)(*[ptr(f, f64p) for f in m.factors])
+        mp = (u8p * self.order)(*[ptr(k, u8p) for k in m.factor_masks])
+        re = C.c_double()
+        check(self._L.vest_cd_iteration_host(self.h, ptr(m.core, f64p), ptr(m.core_mask, u8p), fp, mp, int(reg),
+                                              float(lam), C.byref(re)))
+        return re.value
+
     def compute_delta(self, at, mode: int) -> np.ndarray:
         a = np.ascontiguousarray(at, np.uint32).reshape(-1)
         out = np.zeros(self.ranks[mode])
