@@ -10,5 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 $CMD > gpurun_out/plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"${NCU_KERNELS:-k_rowpass|k_core_pass_s|k_core_gemm_tc|k_core_solve|k_pack_uw}" -s ${NCU_SKIP:-0} -c ${NCU_COUNT:-8} \
+    --metrics sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active \
+    -k regex:"${NCU_KERNELS:-k_rowpass|k_core_sall|k_sall_gemm|k_core_rpass|k_core_solve_g}" -s ${NCU_SKIP:-0} -c ${NCU_COUNT:-8} \
     -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
