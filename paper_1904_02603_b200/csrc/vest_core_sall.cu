@@ -86,7 +86,12 @@ __host__ __device__ constexpr int sall_ldr(int P, int F) {
 __host__ __device__ constexpr size_t h_stride(int nq) { return ((size_t)nq * nq + 1) & ~(size_t)1; }
 
 constexpr int kAllWarps = 4;    // k_core_sall warps per CTA
-constexpr int kRWarps = 8;      // k_core_rpass warps per CTA
+#ifndef VEST_RPASS_RE
+#define VEST_RPASS_RE 1  // RE=2: 14% fewer instructions but lower occupancy, measured no faster
+#endif
+constexpr int kRE = VEST_RPASS_RE;  // k_core_rpass entries per lane per round
+constexpr int kRRound = 32 * kRE;
+constexpr int kRWarps = kRE > 1 ? 4 : 8;  // k_core_rpass warps per CTA (staging smem)
 constexpr int kSgLd = 36;       // k_sall_gemm staging stride (== 4 mod 16)
 constexpr int kSolveK = 4;      // solve: cells per lane, F * J_m <= 128
 constexpr int kSolveSlack = 128;  // doubles after each H buffer (unconditional row reads)
@@ -417,12 +422,12 @@ struct RPassArgs {
 #define VEST_RPASS_MINB 2
 #endif
 template <int F, int Jm>
-struct RStage {  // one round's staged operands, per warp (doubles)
+struct RStage {  // one round's staged operands (kRRound entries), per warp (doubles)
   static constexpr int ld1 = (F + 1) & ~1, ld2 = (Jm + 1) & ~1;
-  static constexpr int U = 0;              // [32][ld1]
-  static constexpr int Wv = U + 32 * ld1;  // [4][32]: prev_a, prev_b, cur_a, cur_b
-  static constexpr int Rr = Wv + 4 * 32;   // [32]
-  static constexpr int A2 = Rr + 32;       // [ld2]
+  static constexpr int U = 0;                   // [kRRound][ld1]
+  static constexpr int Wv = U + kRRound * ld1;  // [4][kRRound]: prev_a, prev_b, cur_a, cur_b
+  static constexpr int Rr = Wv + 4 * kRRound;   // [kRRound]
+  static constexpr int A2 = Rr + kRRound;       // [ld2]
   static constexpr int size = (A2 + ld2 + 1) & ~1;
 };
 // v[i] summed over the warp, scattered: lane l returns with v[0] = sum of v[l]
@@ -487,23 +492,36 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
     return c;
   };
   auto next = [&](const Cur& c) {
-    if (c.base + 32 < c.end) return Cur{c.ci, c.beg, c.end, c.base + 32, c.row};
+    if (c.base + kRRound < c.end) return Cur{c.ci, c.beg, c.end, c.base + kRRound, c.row};
     return first(c.ci + stride);
   };
-  auto coord = [&](const Cur& c) -> uint32_t {
-    return (c.ci < a.csf.nchunks && c.base + lane < c.end) ? __ldg(a.csf.oc[1] + c.base + lane) : 0u;
+  struct Co {
+    uint32_t i[kRE];
   };
-  auto issue = [&](const Cur& c, int b, uint32_t i1) {
+  auto coord = [&](const Cur& c) {
+    Co o;
+#pragma unroll
+    for (int e = 0; e < kRE; ++e) {
+      const uint32_t pos = c.base + 32 * e + lane;
+      o.i[e] = (c.ci < a.csf.nchunks && pos < c.end) ? __ldg(a.csf.oc[1] + pos) : 0u;
+    }
+    return o;
+  };
+  auto issue = [&](const Cur& c, int b, const Co& co) {
     double* st = st0 + b * RS::size;
-    const uint32_t pos = c.base + lane;
-    if (c.ci < a.csf.nchunks && pos < c.end) {
-      const double* r1 = a.m.factor[1] + (size_t)i1 * ld1;
 #pragma unroll
-      for (int t = 0; t < ld1 / 2; ++t) cp_async16(st + RS::U + lane * ld1 + 2 * t, r1 + 2 * t);
+    for (int e = 0; e < kRE; ++e) {
+      const uint32_t pos = c.base + 32 * e + lane;
+      const int sl = 32 * e + lane;  // staged slot
+      if (c.ci < a.csf.nchunks && pos < c.end) {
+        const double* r1 = a.m.factor[1] + (size_t)co.i[e] * ld1;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (wrow[j] >= 0) cp_async8(st + RS::Wv + 32 * j + lane, a.W + (uint64_t)wrow[j] * a.wstride + pos);
-      cp_async8(st + RS::Rr + lane, a.r + pos);
+        for (int t = 0; t < ld1 / 2; ++t) cp_async16(st + RS::U + sl * ld1 + 2 * t, r1 + 2 * t);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (wrow[j] >= 0) cp_async8(st + RS::Wv + kRRound * j + sl, a.W + (uint64_t)wrow[j] * a.wstride + pos);
+        cp_async8(st + RS::Rr + sl, a.r + pos);
+      }
     }
     if (c.ci < a.csf.nchunks && c.base == c.beg && 2 * lane < ld2)
       cp_async16(st + RS::A2 + 2 * lane, a.m.factor[2] + (size_t)c.row * ld2 + 2 * lane);
@@ -513,7 +531,7 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
   if (cur.ci < a.csf.nchunks) {
     issue(cur, 0, coord(cur));
     Cur nxt = next(cur);
-    uint32_t n1 = coord(nxt);
+    Co n1 = coord(nxt);
     double R0[F], R1[F];
 #pragma unroll
     for (int f = 0; f < F; ++f) R0[f] = R1[f] = 0.0;
@@ -537,17 +555,21 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
       const bool more = nxt.ci < a.csf.nchunks;
       if (more) issue(nxt, buf ^ 1, n1);
       const Cur nn = more ? next(nxt) : nxt;
-      const uint32_t m1 = more ? coord(nn) : 0u;
-      const uint32_t pos = cur.base + lane;
+      Co m1;
+      if (more) m1 = coord(nn);
+#pragma unroll
+      for (int e = 0; e < kRE; ++e) {
+      const uint32_t pos = cur.base + 32 * e + lane;
+      const int sl = 32 * e + lane;
       if (pos < cur.end) {
         double u[ld1];
 #pragma unroll
         for (int t = 0; t < ld1 / 2; ++t) {
-          const double2 v = reinterpret_cast<const double2*>(st + RS::U + lane * ld1)[t];
+          const double2 v = reinterpret_cast<const double2*>(st + RS::U + sl * ld1)[t];
           u[2 * t] = v.x;
           u[2 * t + 1] = v.y;
         }
-        double r = st[RS::Rr + lane];
+        double r = st[RS::Rr + sl];
         if (np > 0) {
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
@@ -560,22 +582,23 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
                 t = fma(u[2 * f2], q.x, t);
                 if (2 * f2 + 1 < F) t = fma(u[2 * f2 + 1], q.y, t);
               }
-              r = fma(-st[RS::Wv + 32 * j + lane], t, r);
+              r = fma(-st[RS::Wv + kRRound * j + sl], t, r);
             }
           }
           a.r[pos] = r;
         }
         if (fin || a.want_sq) sq = fma(r, r, sq);
         if (nc > 0) {
-          const double w0 = st[RS::Wv + 64 + lane] * r;
+          const double w0 = st[RS::Wv + 2 * kRRound + sl] * r;
 #pragma unroll
           for (int f = 0; f < F; ++f) R0[f] = fma(w0, u[f], R0[f]);
           if (nc > 1) {
-            const double w1 = st[RS::Wv + 96 + lane] * r;
+            const double w1 = st[RS::Wv + 3 * kRRound + sl] * r;
 #pragma unroll
             for (int f = 0; f < F; ++f) R1[f] = fma(w1, u[f], R1[f]);
           }
         }
+      }
       }
       if (!more || nxt.ci != cur.ci) {  // chunk finished
         if (fin) {
@@ -914,7 +937,7 @@ const CoreAllOps kAllOps[] = {
 int rpass_grid(Ctx& c, const CoreAllOps* ops) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  return std::max(1, std::min(ops->rpass_occupancy(), VEST_RPASS_MINB)) * sms;
+  return std::max(1, std::min(ops->rpass_occupancy(), 4)) * sms;  // one resident wave (the last CTA sums the partials)
 }
 
 RPassArgs rpass_args(Ctx& c, const int (&prev)[2], const int (&cur)[2], double* cout, int want_sq) {
