@@ -204,7 +204,8 @@ def workload_config(n):
     return {"workload": "config2: 3-mode 100k^3, 10M uniform distinct entries, fp64 U[0,1), ranks 10x10x10, "
                         "lambda 0.01 LF; step = update_all_factors + update_core + RE",
             "nnz": CONFIG2["nnz"], "ranks": CONFIG2["ranks"], "dims": CONFIG2["dims"],
-            "parallelism": f"rows sharded x{n} (NCCL)" if n > 1 else "single",
+            "parallelism": (f"rows sharded x{n} (NCCL)" if n > 1 or os.environ.get("VEST_FORCE_SHARDED") == "1"
+                            else "single"),
             "l2": "inputs larger than L2 (per-mode CSF 600 MB vs 126 MB L2)"}
 
 
@@ -216,14 +217,17 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    # VEST_FORCE_SHARDED=1: the sharded driver + NCCL hooks even at world size 1
+    # (exercises the multi-GPU plumbing on a single GPU; diagnostic only)
+    sharded = world > 1 or os.environ.get("VEST_FORCE_SHARDED") == "1"
+    if sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     L = _lib.lib()
     cfg = CONFIG2
     coords, vals = synth(cfg["dims"], cfg["nnz"], cfg["data_seed"])
     x = st.SparseTensor(cfg["dims"], coords, vals)
-    if world > 1:
+    if sharded:
         # rows of every mode sharded by nnz-balanced ranges; NCCL exchanges
         # (paper_1904_02603_b200/sharded.py)
         from paper_1904_02603_b200 import sharded as sh
