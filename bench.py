@@ -87,6 +87,27 @@ def contraction_fmas(ranks, n):
     return ranks[0] * P(1)
 
 
+def step_flops_per_entry(ranks, core_unmasked=None):
+    """SURVEY.md 8(d) F_alg: reference-equivalent flops per entry x iteration,
+    sum_n [dense-factorised delta + J_n (J_n + 1) + 2 J_n] + |G_u| (N + 7) + 2,
+    dense-factorised delta = 2 (|G| + |G|/J_a + ...) over the N-1 contractions
+    (largest J first)."""
+    N = len(ranks)
+    G = 1
+    for J in ranks:
+        G *= J
+    Gu = G if core_unmasked is None else core_unmasked
+    total = 0
+    for n in range(N):
+        others = sorted((ranks[k] for k in range(N) if k != n), reverse=True)
+        d, size = 0, G
+        for Ja in others:
+            d += size
+            size //= Ja
+        total += 2 * d + ranks[n] * (ranks[n] + 1) + 2 * ranks[n]
+    return total + Gu * (N + 7) + 2
+
+
 def factor_launch_model(ranks, nnz, modes=None):
     """(flops, bytes) per launch of the dominant kernel: the factor-row update
     of one mode (k_rowpass<kStats>), averaged over modes 0..modes-1 (the last
@@ -344,6 +365,13 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "step_share": float(ms_arr[0] / ms) if ms > 0 else None,
     }
+    # whole-iteration FMA roof: reference-equivalent flops of one
+    # CD iteration over the whole job vs the measured FP64 peak of all GPUs
+    f_alg = step_flops_per_entry(cfg["ranks"])
+    step_tf = f_alg * value / 1e12
+    roofline["step"] = {"flops_per_entry": f_alg, "achieved": step_tf, "peak": peak.value * world,
+                        "unit": "TFLOP/s", "frac": step_tf / (peak.value * world),
+                        "note": "SURVEY.md 8(d) F_alg (reference-equivalent work) at the measured rate"}
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and not args.no_cpu:
