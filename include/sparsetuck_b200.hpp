@@ -634,4 +634,77 @@ inline double evaluate_test(const TuckerModel& m, const SparseTensor& test) {
   return re;
 }
 
+// ------------------------------------------------------------ data formats --
+// load_coo / save_coo (sparse_tensor.hpp:139-228), save_model / load_model
+// (model_io.hpp:22-104): vest_io.cpp, parallel, byte-compatible files and the
+// reference's exceptions and messages.
+namespace b200_detail {
+inline void io_check(int rc) {
+  if (rc == VEST_OK) return;
+  const std::string msg = vest_io_last_error();
+  if (rc == VEST_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+inline SparseTensor coo_take(vest_coo* h) {
+  std::unique_ptr<vest_coo, void (*)(vest_coo*)> g(h, vest_coo_free);
+  int order = 0;
+  std::uint64_t nnz = 0;
+  io_check(vest_coo_info(h, &order, &nnz, nullptr, nullptr, nullptr));
+  std::vector<std::uint64_t> d(order);
+  const std::uint32_t* c = nullptr;
+  const double* v = nullptr;
+  io_check(vest_coo_info(h, nullptr, nullptr, d.data(), &c, &v));
+  SparseTensor x;
+  x.dims.assign(d.begin(), d.end());
+  x.coords.assign(c, c + nnz * order);
+  x.values.assign(v, v + nnz);
+  return x;
+}
+}  // namespace b200_detail
+
+inline SparseTensor load_coo(const std::string& path, bool one_based = false) {
+  vest_coo* h = nullptr;
+  b200_detail::io_check(vest_coo_load(path.c_str(), one_based ? 1 : 0, 0, &h));
+  return b200_detail::coo_take(h);
+}
+
+inline void save_coo(const SparseTensor& x, const std::string& path) {
+  std::vector<std::uint64_t> d(x.dims.begin(), x.dims.end());
+  b200_detail::io_check(vest_coo_save(path.c_str(), (int)x.order(), d.data(), x.nnz(), x.coords.data(),
+                                      x.values.data()));
+}
+
+inline void save_model(const TuckerModel& m, const std::string& dir) {
+  std::vector<std::uint64_t> d(m.dims.begin(), m.dims.end()), r(m.ranks.begin(), m.ranks.end());
+  std::vector<const double*> f(m.order());
+  for (std::size_t n = 0; n < m.order(); ++n) f[n] = m.factors[n].data();
+  b200_detail::io_check(vest_model_save(dir.c_str(), (int)m.order(), d.data(), r.data(), m.core.data(), f.data()));
+}
+
+inline TuckerModel load_model(const std::string& dir) {
+  vest_model_file* h = nullptr;
+  b200_detail::io_check(vest_model_load(dir.c_str(), &h));
+  std::unique_ptr<vest_model_file, void (*)(vest_model_file*)> g(h, vest_model_file_free);
+  int order = 0;
+  b200_detail::io_check(vest_model_file_info(h, &order, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
+  std::vector<std::uint64_t> d(order), r(order);
+  const double* core = nullptr;
+  const std::uint8_t* cm = nullptr;
+  std::vector<const double*> f(order);
+  std::vector<const std::uint8_t*> k(order);
+  b200_detail::io_check(vest_model_file_info(h, nullptr, d.data(), r.data(), &core, &cm, f.data(), k.data()));
+  TuckerModel m;
+  m.dims.assign(d.begin(), d.end());
+  m.ranks.assign(r.begin(), r.end());
+  m.core.assign(core, core + m.core_size());
+  m.core_mask.assign(cm, cm + m.core_size());
+  m.factors.resize(order);
+  m.factor_masks.resize(order);
+  for (int n = 0; n < order; ++n) {
+    m.factors[n].assign(f[n], f[n] + m.dims[n] * m.ranks[n]);
+    m.factor_masks[n].assign(k[n], k[n] + m.dims[n] * m.ranks[n]);
+  }
+  return m;
+}
+
 }  // namespace sparsetuck

@@ -192,6 +192,40 @@ int vest_split_ids(uint64_t nnz, double test_fraction, uint64_t seed, uint64_t* 
  * bounds[0..world] with bounds[0] = 0, bounds[world] = rows. */
 int vest_partition_rows(const uint64_t* row_offsets, uint64_t rows, int world, uint64_t* bounds);
 
+/* --------------------------------------------------------- data formats --
+ * The formats either side of the path (host side, OpenMP), byte-compatible
+ * with the reference.  Errors: the reference's messages through
+ * vest_io_last_error(); VEST_EINVAL for tensor/model validation
+ * (std::invalid_argument), VEST_ERUNTIME for I/O and parse errors
+ * (std::runtime_error). */
+typedef struct vest_coo vest_coo;
+typedef struct vest_model_file vest_model_file;
+const char* vest_io_last_error(void);
+/* load_coo (sparse_tensor.hpp:139-209): whitespace-separated COO text, "#"
+ * comments, optional "# dims:" header, then make_tensor's validation (bounds,
+ * duplicates).  threads <= 0: all host threads.  Read the result with
+ * vest_coo_info (pointers stay valid until vest_coo_free). */
+int vest_coo_load(const char* path, int one_based, int threads, vest_coo** out);
+int vest_coo_info(const vest_coo* coo, int* order, uint64_t* nnz, uint64_t* dims, const uint32_t** coords,
+                  const double** values);
+void vest_coo_free(vest_coo* coo);
+/* save_coo (sparse_tensor.hpp:211-228): byte-identical "# dims:" + "%.17g" text. */
+int vest_coo_save(const char* path, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                  const double* values);
+/* Binary cache of a tensor (magic "VESTCOO1", order, nnz, dims, coords, values):
+ * a large input is parsed once. */
+int vest_coo_cache_save(const char* path, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                        const double* values);
+int vest_coo_cache_load(const char* path, vest_coo** out);
+/* save_model / load_model (model_io.hpp:22-104): factor_<n>.tsv + core.coo,
+ * byte-identical; a loaded model treats every zero as pruned. */
+int vest_model_save(const char* dir, int order, const uint64_t* dims, const uint64_t* ranks, const double* core,
+                    const double* const* factors);
+int vest_model_load(const char* dir, vest_model_file** out);
+int vest_model_file_info(const vest_model_file* mf, int* order, uint64_t* dims, uint64_t* ranks, const double** core,
+                         const uint8_t** core_mask, const double** factors, const uint8_t** factor_masks);
+void vest_model_file_free(vest_model_file* mf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,14 +8,17 @@
 //
 // Used for: (1) generating tests/golden fixtures (tests/golden/make_golden.py),
 // (2) pinning the C restatement (vest_oracle.c), (3) bench.py's CPU baseline
-// ("kind": "reference") and --impl reference arm.  The exported names mirror
-// vest_oracle.h with a vr_ prefix so both oracles share one Python binding.
+// ("kind": "reference") and --impl reference arm, (4) the byte-level parity of
+// the I/O row (load_coo / save_coo / save_model / load_model).  The exported
+// names mirror vest_oracle.h with a vr_ prefix so both oracles share one
+// Python binding.
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "sparsetuck/model_io.hpp"
 #include "sparsetuck/pruning.hpp"
 #include "sparsetuck/sparse_tensor.hpp"
 #include "sparsetuck/trainer.hpp"
@@ -299,6 +302,72 @@ int vr_fit(void* p, int reg, double lambda, int auto_mode, double target_sparsit
     *final_re = r.report.final_re;
     s->m = std::move(r.model);
     s->have_res = s->have_table = false;
+  });
+}
+
+// ------------------------------------------------------------------- I/O --
+// load_coo (sparse_tensor.hpp:143-209): two calls -- sizes (coords/values NULL),
+// then the data.
+int vr_load_coo(const char* path, int one_based, int* order, uint64_t* nnz, uint64_t* dims,
+                uint32_t* coords, double* values) {
+  return guard([&] {
+    const SparseTensor x = load_coo(path, one_based != 0);
+    *order = (int)x.order();
+    *nnz = x.nnz();
+    if (dims)
+      for (std::size_t k = 0; k < x.order(); ++k) dims[k] = x.dims[k];
+    if (coords) std::memcpy(coords, x.coords.data(), x.coords.size() * sizeof(Coord));
+    if (values) std::memcpy(values, x.values.data(), x.values.size() * sizeof(double));
+  });
+}
+
+// save_coo (sparse_tensor.hpp:211-228)
+int vr_save_coo(const char* path, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                const double* values) {
+  return guard([&] {
+    SparseTensor x;
+    x.dims.assign(dims, dims + order);
+    x.coords.assign(coords, coords + nnz * order);
+    x.values.assign(values, values + nnz);
+    save_coo(x, path);
+  });
+}
+
+// save_model (model_io.hpp:22-51)
+int vr_save_model(const char* dir, int order, const uint64_t* dims, const uint64_t* ranks, const double* core,
+                  const double* const* factors) {
+  return guard([&] {
+    TuckerModel m;
+    m.dims.assign(dims, dims + order);
+    m.ranks.assign(ranks, ranks + order);
+    m.core.assign(core, core + m.core_size());
+    m.core_mask.assign(m.core.size(), 0);
+    m.factors.resize(order);
+    m.factor_masks.resize(order);
+    for (int n = 0; n < order; ++n) {
+      m.factors[n].assign(factors[n], factors[n] + dims[n] * ranks[n]);
+      m.factor_masks[n].assign(m.factors[n].size(), 0);
+    }
+    save_model(m, dir);
+  });
+}
+
+// load_model (model_io.hpp:53-104): sizes first (core/factors NULL), then data
+int vr_load_model(const char* dir, int* order, uint64_t* dims, uint64_t* ranks, double* core,
+                  uint8_t* core_mask, double* const* factors, uint8_t* const* factor_masks) {
+  return guard([&] {
+    const TuckerModel m = load_model(dir);
+    *order = (int)m.order();
+    for (std::size_t n = 0; n < m.order(); ++n) {
+      if (dims) dims[n] = m.dims[n];
+      if (ranks) ranks[n] = m.ranks[n];
+    }
+    if (core) std::memcpy(core, m.core.data(), m.core.size() * sizeof(double));
+    if (core_mask) std::memcpy(core_mask, m.core_mask.data(), m.core_mask.size());
+    for (std::size_t n = 0; n < m.order(); ++n) {
+      if (factors && factors[n]) std::memcpy(factors[n], m.factors[n].data(), m.factors[n].size() * sizeof(double));
+      if (factor_masks && factor_masks[n]) std::memcpy(factor_masks[n], m.factor_masks[n].data(), m.factor_masks[n].size());
+    }
   });
 }
 

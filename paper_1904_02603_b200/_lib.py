@@ -64,6 +64,20 @@ SIGNATURES = {
     "vest_synth": (C.c_int, [C.c_int, u64p, C.c_uint64, f64p, C.c_int, C.c_uint64, u32p, f64p]),
     "vest_split_ids": (C.c_int, [C.c_uint64, C.c_double, C.c_uint64, u64p, u64p, u64p, u64p]),
     "vest_partition_rows": (C.c_int, [u64p, C.c_uint64, C.c_int, u64p]),
+    # data formats (vest_io.cpp)
+    "vest_io_last_error": (C.c_char_p, []),
+    "vest_coo_load": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]),
+    "vest_coo_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_uint64), u64p, C.POINTER(u32p),
+                                C.POINTER(f64p)]),
+    "vest_coo_free": (None, [vp]),
+    "vest_coo_save": (C.c_int, [C.c_char_p, C.c_int, u64p, C.c_uint64, u32p, f64p]),
+    "vest_coo_cache_save": (C.c_int, [C.c_char_p, C.c_int, u64p, C.c_uint64, u32p, f64p]),
+    "vest_coo_cache_load": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "vest_model_save": (C.c_int, [C.c_char_p, C.c_int, u64p, u64p, f64p, C.POINTER(f64p)]),
+    "vest_model_load": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "vest_model_file_info": (C.c_int, [vp, C.POINTER(C.c_int), u64p, u64p, C.POINTER(f64p), C.POINTER(u8p),
+                                       C.POINTER(f64p), C.POINTER(u8p)]),
+    "vest_model_file_free": (None, [vp]),
 }
 
 _lib = None
@@ -112,6 +126,18 @@ def check(rc: int) -> None:
     if rc == 3:
         raise CudaError(msg)
     raise VestError(msg)  # std::runtime_error
+
+
+def io_check(rc: int) -> None:
+    """Status of a data-format call (vest_io.cpp): the reference's exception
+    type and message (std::invalid_argument -> ValueError, std::runtime_error
+    -> VestError)."""
+    if rc == 0:
+        return
+    msg = lib().vest_io_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    raise VestError(msg)
 
 
 def ptr(a, t):

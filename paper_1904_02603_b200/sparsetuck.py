@@ -92,6 +92,56 @@ def make_tensor(dims: Sequence[int], coords, values) -> SparseTensor:
     return SparseTensor(dims, coords, values)
 
 
+# ---------------------------------------------------------------- data formats --
+def _coo_from_handle(h) -> SparseTensor:
+    L = _lib.lib()
+    try:
+        order, nnz = C.c_int(), C.c_uint64()
+        _lib.io_check(L.vest_coo_info(h, C.byref(order), C.byref(nnz), None, None, None))
+        dims = np.zeros(order.value, np.uint64)
+        cp, vp_ = u32p(), f64p()
+        _lib.io_check(L.vest_coo_info(h, None, None, ptr(dims, u64p), C.byref(cp), C.byref(vp_)))
+        n, k = int(nnz.value), int(order.value)
+        coords = np.ctypeslib.as_array(cp, shape=(max(n * k, 1),))[: n * k].copy().reshape(n, k) if n else \
+            np.zeros((0, k), np.uint32)
+        values = np.ctypeslib.as_array(vp_, shape=(max(n, 1),))[:n].copy() if n else np.zeros(0)
+        return SparseTensor([int(d) for d in dims], coords, values)
+    finally:
+        L.vest_coo_free(h)
+
+
+def load_coo(path, one_based: bool = False, threads: int = 0) -> SparseTensor:
+    """load_coo (sparse_tensor.hpp:139-209): parallel parse, the reference's
+    rules and messages, then make_tensor's validation."""
+    h = C.c_void_p()
+    _lib.io_check(_lib.lib().vest_coo_load(str(path).encode(), int(one_based), int(threads), C.byref(h)))
+    return _coo_from_handle(h)
+
+
+def save_coo(x: SparseTensor, path) -> None:
+    """save_coo (sparse_tensor.hpp:211-228): byte-identical text."""
+    d = np.asarray(x.dims, np.uint64)
+    c = np.ascontiguousarray(x.coords, np.uint32).reshape(-1)
+    v = np.ascontiguousarray(x.values, np.float64)
+    _lib.io_check(_lib.lib().vest_coo_save(str(path).encode(), x.order(), ptr(d, u64p), x.nnz(),
+                                           ptr(c, u32p), ptr(v, f64p)))
+
+
+def save_coo_cache(x: SparseTensor, path) -> None:
+    """Binary tensor cache (vest_coo_cache_save): parse a large input once."""
+    d = np.asarray(x.dims, np.uint64)
+    c = np.ascontiguousarray(x.coords, np.uint32).reshape(-1)
+    v = np.ascontiguousarray(x.values, np.float64)
+    _lib.io_check(_lib.lib().vest_coo_cache_save(str(path).encode(), x.order(), ptr(d, u64p), x.nnz(),
+                                                 ptr(c, u32p), ptr(v, f64p)))
+
+
+def load_coo_cache(path) -> SparseTensor:
+    h = C.c_void_p()
+    _lib.io_check(_lib.lib().vest_coo_cache_load(str(path).encode(), C.byref(h)))
+    return _coo_from_handle(h)
+
+
 @dataclass
 class ModeIndex:
     """Per-mode CSR (sparse_tensor.hpp:109-117): read back from the device CSF."""
@@ -517,6 +567,46 @@ def evaluate_test(m: TuckerModel, test: SparseTensor) -> float:
     dev = _model_device(m)
     dev.set_model(m)
     return dev.evaluate(test)
+
+
+def save_model(m: "TuckerModel", dir_path) -> None:
+    """save_model (model_io.hpp:22-51): factor_<n>.tsv + core.coo, byte-identical."""
+    d = np.asarray(m.dims, np.uint64)
+    r = np.asarray(m.ranks, np.uint64)
+    core = np.ascontiguousarray(m.core, np.float64).reshape(-1)
+    fs = [np.ascontiguousarray(f, np.float64).reshape(-1) for f in m.factors]
+    fp = (f64p * len(fs))(*[ptr(f, f64p) for f in fs])
+    _lib.io_check(_lib.lib().vest_model_save(str(dir_path).encode(), len(fs), ptr(d, u64p), ptr(r, u64p),
+                                             ptr(core, f64p), fp))
+
+
+def load_model(dir_path) -> "TuckerModel":
+    """load_model (model_io.hpp:53-104): every zero element is pruned."""
+    L = _lib.lib()
+    h = C.c_void_p()
+    _lib.io_check(L.vest_model_load(str(dir_path).encode(), C.byref(h)))
+    try:
+        order = C.c_int()
+        _lib.io_check(L.vest_model_file_info(h, C.byref(order), None, None, None, None, None, None))
+        n = order.value
+        dims = np.zeros(n, np.uint64)
+        ranks = np.zeros(n, np.uint64)
+        cp, cmp_ = f64p(), u8p()
+        fps = (f64p * n)()
+        mps = (u8p * n)()
+        _lib.io_check(L.vest_model_file_info(h, None, ptr(dims, u64p), ptr(ranks, u64p), C.byref(cp), C.byref(cmp_),
+                                             fps, mps))
+        dims_l, ranks_l = [int(v) for v in dims], [int(v) for v in ranks]
+        G = int(np.prod(ranks_l))
+        core = np.ctypeslib.as_array(cp, shape=(G,)).copy()
+        core_mask = np.ctypeslib.as_array(cmp_, shape=(G,)).copy()
+        factors = [np.ctypeslib.as_array(fps[k], shape=(dims_l[k] * ranks_l[k],)).copy().reshape(dims_l[k], ranks_l[k])
+                   for k in range(n)]
+        masks = [np.ctypeslib.as_array(mps[k], shape=(dims_l[k] * ranks_l[k],)).copy().reshape(dims_l[k], ranks_l[k])
+                 for k in range(n)]
+        return TuckerModel(dims_l, ranks_l, core, core_mask, factors, masks)
+    finally:
+        L.vest_model_file_free(h)
 
 
 def split_train_test(x: SparseTensor, test_fraction: float, seed: int):

@@ -143,6 +143,26 @@ int main() {
     }
     CHECK(std::abs(reconstruction_error(m, x) - r.report.iterations[5].re) <= 1e-9 * r.report.iterations[5].re);
   }
+  {  // data formats: model directory and COO text round trips (vest_io.cpp)
+    TuckerModel m = init_random({40, 30, 20}, {3, 2, 4}, 9);
+    m.core[1] = 0.0;
+    const std::string dir = "/tmp/vest_mirror_model";
+    save_model(m, dir);
+    const TuckerModel back = load_model(dir);
+    CHECK(back.dims == m.dims && back.ranks == m.ranks && back.core == m.core && back.factors == m.factors);
+    CHECK(back.core_mask[1] == 1 && back.core_mask[0] == 0);
+    SparseTensor x = make_tensor({5, 6}, {0, 1, 4, 5, 2, 2}, {0.25, -1e-300, 3.0});
+    save_coo(x, "/tmp/vest_mirror.coo");
+    const SparseTensor y = load_coo("/tmp/vest_mirror.coo");
+    CHECK(y.dims == x.dims && y.coords == x.coords && y.values == x.values);
+    bool threw = false;
+    try {
+      load_coo("/tmp/vest_mirror_absent.coo");
+    } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()).find("cannot open") != std::string::npos;
+    }
+    CHECK(threw);
+  }
   if (failures == 0) std::printf("ALL OK\n");
   return failures == 0 ? 0 : 1;
 }
