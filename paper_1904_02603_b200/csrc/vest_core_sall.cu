@@ -50,6 +50,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
+// factor-row gathers: through L1 (.ca) -- under skewed coordinates (Zipf) a
+// few hot rows take a large share of the gathers, which L2-only copies would
+// funnel into the same L2 slices
+__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_row(void* smem, const void* gmem, bool via_l1) {
+  if (via_l1) cp_async16_ca(smem, gmem);
+  else cp_async16(smem, gmem);
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
@@ -105,7 +115,7 @@ constexpr int kSolveSlack = 128;  // doubles after each H buffer (unconditional 
 // DMMA with B = u_i u_j formed from the staged u at fragment load.
 template <class S>
 __global__ void __launch_bounds__(kAllWarps * 32) k_core_sall(DevModel m, DevCSF csf, double* stats, double* W,
-                                                              uint64_t wstride) {
+                                                              uint64_t wstride, int hot) {
   static_assert(S::N == 3, "all-prefix statistics: 3-mode shapes");
   constexpr int P = S::J(0), F = S::J(1), NV = F * (F + 1) / 2;
   constexpr int X = P / 2, R = sall_rows(P), AR = sall_arow(P);
@@ -153,9 +163,9 @@ __global__ void __launch_bounds__(kAllWarps * 32) k_core_sall(DevModel m, DevCSF
       const double* r0 = m.factor[0] + (size_t)i0 * ld0;
       const double* r1 = m.factor[1] + (size_t)i1 * ld1;
 #pragma unroll
-      for (int t = 0; t < ld0 / 2; ++t) cp_async16(row + 2 * t, r0 + 2 * t);
+      for (int t = 0; t < ld0 / 2; ++t) cp_async16_row(row + 2 * t, r0 + 2 * t, hot & 1);
 #pragma unroll
-      for (int t = 0; t < ld1 / 2; ++t) cp_async16(row + AR + 2 * t, r1 + 2 * t);
+      for (int t = 0; t < ld1 / 2; ++t) cp_async16_row(row + AR + 2 * t, r1 + 2 * t, hot & 2);
     } else {
 #pragma unroll
       for (int t = 0; t < LDR; ++t) row[t] = 0.0;  // zero weights: no contribution
@@ -409,6 +419,7 @@ struct RPassArgs {
   const double* W;        // [P][wstride] block weights A_0[i_0, p] (k_core_sall)
   uint64_t wstride;
   int want_sq;            // also sum r^2 (after the previous group's update)
+  int hot;                // bit k: mode k is skewed (its row gathers go through L1)
 };
 
 // One pair group: r -= sum_prev w_p (u . q_p) (q_p = dg_p a per slice), then
@@ -516,7 +527,7 @@ __global__ void __launch_bounds__(kRWarps * 32, VEST_RPASS_MINB) k_core_rpass(RP
       if (c.ci < a.csf.nchunks && pos < c.end) {
         const double* r1 = a.m.factor[1] + (size_t)co.i[e] * ld1;
 #pragma unroll
-        for (int t = 0; t < ld1 / 2; ++t) cp_async16(st + RS::U + sl * ld1 + 2 * t, r1 + 2 * t);
+        for (int t = 0; t < ld1 / 2; ++t) cp_async16_row(st + RS::U + sl * ld1 + 2 * t, r1 + 2 * t, a.hot & 2);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (wrow[j] >= 0) cp_async8(st + RS::Wv + kRRound * j + sl, a.W + (uint64_t)wrow[j] * a.wstride + pos);
@@ -863,8 +874,8 @@ __global__ void __launch_bounds__(32) k_core_solve_g(const double* Ha, const dou
 // --------------------------------------------------------------- dispatch --
 struct CoreAllOps {
   int J[3];
-  cudaError_t (*sall)(const DevModel& m, const DevCSF& csf, double* stats, double* W, uint64_t wstride, int grid,
-                      cudaStream_t s);
+  cudaError_t (*sall)(const DevModel& m, const DevCSF& csf, double* stats, double* W, uint64_t wstride, int hot,
+                      int grid, cudaStream_t s);
   cudaError_t (*rpass)(const RPassArgs& a, int grid, cudaStream_t s);
   cudaError_t (*sgemm)(const double* stats, int LW, const Chunk* chunks, uint32_t nchunks, const double* A,
                        double* partial, int ksplit, cudaStream_t s);
@@ -873,11 +884,11 @@ struct CoreAllOps {
 
 template <class S>
 cudaError_t run_core_sall(const DevModel& m, const DevCSF& csf, double* stats, double* W, uint64_t wstride,
-                          int grid, cudaStream_t s) {
+                          int hot, int grid, cudaStream_t s) {
   if (csf.nchunks == 0) return cudaSuccess;
   const int smem = kAllWarps * 2 * 32 * sall_ldr(S::J(0), S::J(1)) * (int)sizeof(double);
   cudaFuncSetAttribute(k_core_sall<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_core_sall<S><<<grid, kAllWarps * 32, smem, s>>>(m, csf, stats, W, wstride);
+  k_core_sall<S><<<grid, kAllWarps * 32, smem, s>>>(m, csf, stats, W, wstride, hot);
   count_launch();
   return cudaGetLastError();
 }
@@ -934,6 +945,8 @@ const CoreAllOps kAllOps[] = {
     make_all_ops<10, 10, 5>(),
 };
 
+int hot_modes(const Ctx& c) { return (c.skewed[0] ? 1 : 0) | (c.skewed[1] ? 2 : 0); }
+
 int rpass_grid(Ctx& c, const CoreAllOps* ops) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
@@ -957,6 +970,7 @@ RPassArgs rpass_args(Ctx& c, const int (&prev)[2], const int (&cur)[2], double* 
   a.W = c.d_pack_w;
   a.wstride = c.nnz;
   a.want_sq = want_sq;
+  a.hot = hot_modes(c);
   return a;
 }
 
@@ -1004,7 +1018,8 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   double* Cb = Hd + nH;                                  // [C_a | C_b | sum r^2]
   {
     ProfScope ps(c, kProfCorePass);
-    check(ops->sall(mv, csf, c.d_chunk_stats, c.d_pack_w, c.nnz, 3 * sms, c.stream), "core all-prefix statistics");
+    check(ops->sall(mv, csf, c.d_chunk_stats, c.d_pack_w, c.nnz, hot_modes(c), 3 * sms, c.stream),
+          "core all-prefix statistics");
   }
   {
     ProfScope ps(c, kProfCoreGemm);

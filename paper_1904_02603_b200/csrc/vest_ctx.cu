@@ -277,6 +277,11 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
     std::vector<uint32_t> empty;
     uint32_t slot = 0;
     c.local_nnz[n] = md.h_offsets[c.row_hi[n]] - md.h_offsets[c.row_lo[n]];
+    {
+      uint64_t mx = 0;
+      for (uint64_t i = 0; i < c.dims[n]; ++i) mx = std::max(mx, md.h_offsets[i + 1] - md.h_offsets[i]);
+      c.skewed[n] = c.nnz > 0 && mx * 1000 > c.nnz;
+    }
     for (uint64_t i = c.row_lo[n]; i < c.row_hi[n]; ++i) {  // this context's rows
       const uint64_t b = md.h_offsets[i], e = md.h_offsets[i + 1], len = e - b;
       if (len == 0) {

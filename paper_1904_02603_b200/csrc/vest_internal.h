@@ -117,6 +117,7 @@ struct Ctx {
   int device = 0;
   uint64_t row_lo[VEST_MAXN] = {}, row_hi[VEST_MAXN] = {};  // owned rows per mode
   uint64_t local_nnz[VEST_MAXN] = {};
+  bool skewed[VEST_MAXN] = {};  // a row holds > 0.1 % of the entries (gathers of its row are hot)
   CommHooks comm;
   bool prof_on = false;
   std::vector<ProfEvent> prof_events;
