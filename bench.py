@@ -252,7 +252,8 @@ def run_ours(args, rank, world, local_rank):
         # rows of every mode sharded by nnz-balanced ranges; NCCL exchanges
         # (paper_1904_02603_b200/sharded.py)
         from paper_1904_02603_b200 import sharded as sh
-        dev = sh.ShardDevice(x, cfg["ranks"], rank, world, sh.TorchComm("cuda"), local_rank)
+        comm = sh.TorchComm("cuda") if os.environ.get("VEST_TORCH_COMM") == "1" else sh.NcclNative()
+        dev = sh.ShardDevice(x, cfg["ranks"], rank, world, comm, local_rank)
     else:
         dev = st.Device(x, cfg["ranks"], local_rank)
     assert dev.specialised(), "rank-specialised kernels expected for config 2"

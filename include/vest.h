@@ -93,6 +93,15 @@ int vest_ctx_create_shard(int order, const uint64_t* dims, uint64_t nnz, const u
                           const uint64_t* row_lo, const uint64_t* row_hi, vest_ctx** out);
 /* Install (or clear with NULL) the communication hooks. */
 int vest_ctx_set_comm(vest_ctx* ctx, const vest_comm* comm);
+/* Native NCCL exchanges for a shard context (instead of host callbacks): every
+ * rank passes the same 128-byte unique id (made once by vest_nccl_unique_id
+ * and distributed by the caller), its rank/world, and the row bounds of every
+ * mode, bounds[n * (world + 1) + r] (vest_partition_rows).  allreduce_sum and
+ * allgather_rows then run as ncclAllReduce / grouped ncclBroadcast on the
+ * context's stream.  NCCL is dlopen'ed (libnccl.so.2) on first use. */
+#define VEST_NCCL_ID_BYTES 128
+int vest_nccl_unique_id(void* id_out);
+int vest_ctx_set_nccl(vest_ctx* ctx, int rank, int world, const void* id, const uint64_t* bounds);
 /* Observed entries in this context's rows of `mode`. */
 uint64_t vest_ctx_local_nnz(vest_ctx* ctx, int mode);
 

@@ -64,6 +64,8 @@ SIGNATURES = {
     "vest_synth": (C.c_int, [C.c_int, u64p, C.c_uint64, f64p, C.c_int, C.c_uint64, u32p, f64p]),
     "vest_split_ids": (C.c_int, [C.c_uint64, C.c_double, C.c_uint64, u64p, u64p, u64p, u64p]),
     "vest_partition_rows": (C.c_int, [u64p, C.c_uint64, C.c_int, u64p]),
+    "vest_nccl_unique_id": (C.c_int, [vp]),
+    "vest_ctx_set_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp, u64p]),
     # data formats (vest_io.cpp)
     "vest_io_last_error": (C.c_char_p, []),
     "vest_coo_load": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]),

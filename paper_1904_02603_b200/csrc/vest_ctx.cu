@@ -681,6 +681,10 @@ int vest_ctx_create_shard(int order, const uint64_t* dims, uint64_t nnz, const u
 
 int vest_ctx_set_comm(vest_ctx* h, const vest_comm* comm) {
   Ctx& c = h->c;
+  if (c.comm_free) {
+    c.comm_free(c.comm.user);
+    c.comm_free = nullptr;
+  }
   c.comm = CommHooks{};
   if (comm) {
     c.comm.user = comm->user;
@@ -765,11 +769,27 @@ static int create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint
   return VEST_OK;
 }
 
+int vest_nccl_unique_id(void* id_out) {
+  return guard([&] { nccl_unique_id(id_out); });
+}
+
+int vest_ctx_set_nccl(vest_ctx* h, int rank, int world, const void* id, const uint64_t* bounds) {
+  Ctx& c = h->c;
+  return guard([&] {
+    set_dev(c);
+    ctx_set_nccl(c, rank, world, id, bounds);
+  });
+}
+
 int vest_ctx_destroy(vest_ctx* h) {
   if (!h) return VEST_OK;
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
+  if (c.comm_free) {
+    c.comm_free(c.comm.user);
+    c.comm_free = nullptr;
+  }
   for (int n = 0; n < VEST_MAXN; ++n) {
     ModeData& md = c.modes[n];
     cudaFree(md.d_offsets);

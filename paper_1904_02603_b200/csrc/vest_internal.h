@@ -115,6 +115,7 @@ struct CommHooks {
 
 struct Ctx {
   int device = 0;
+  void (*comm_free)(void*) = nullptr;  // owner of comm.user (native NCCL state)
   uint64_t row_lo[VEST_MAXN] = {}, row_hi[VEST_MAXN] = {};  // owned rows per mode
   uint64_t local_nnz[VEST_MAXN] = {};
   bool skewed[VEST_MAXN] = {};  // a row holds > 0.1 % of the entries (gathers of its row are hot)
@@ -218,6 +219,8 @@ void sparsity(Ctx& c, double* zero_frac, double* masked_frac);
 void normalize_columns(Ctx& c);
 double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n);
 void comm_allreduce(Ctx& c, double* p, uint64_t n);
+void ctx_set_nccl(Ctx& c, int rank, int world, const void* id, const uint64_t* bounds);  // vest_nccl.cpp
+void nccl_unique_id(void* out);
 void comm_allgather_rows(Ctx& c, int mode, double* base, uint64_t ld);
 
 // RAII timing scope for one kernel family (no-op unless profiling is on).

@@ -15,7 +15,10 @@ points of the CD sweep:
 Everything else (block solves, prune selection, sparsity) then runs
 identically on every rank on identical data, so the replicas stay consistent.
 
-`TorchComm` implements the hooks with torch.distributed (NCCL for device
+`NcclNative` (the production path, bench.py under torchrun) installs a native
+NCCL communicator in the library (vest_ctx_set_nccl): the collectives are
+issued by the library on its own stream, no Python per exchange.  `TorchComm`
+implements the hooks as host callbacks with torch.distributed (NCCL for device
 pointers, gloo for host pointers in the CPU tests); `LocalGroup` emulates W
 ranks as W threads of one process on one GPU (host-synchronised exchanges,
 no device-side waits) for single-GPU testing of the sharded path.
@@ -78,11 +81,35 @@ class ShardDevice(Device):
                                       ptr(r, u64p), device, ptr(lo, u64p), ptr(hi, u64p), C.byref(h)))
         self.h = h
         self.comm = comm
-        self._hooks = comm.hooks(self)  # keep the ctypes callbacks alive
-        check(L.vest_ctx_set_comm(self.h, C.cast(C.pointer(self._hooks), C.c_void_p)))
+        if isinstance(comm, NcclNative):
+            comm.install(self)
+        else:
+            self._hooks = comm.hooks(self)  # keep the ctypes callbacks alive
+            check(L.vest_ctx_set_comm(self.h, C.cast(C.pointer(self._hooks), C.c_void_p)))
 
     def local_nnz(self, mode: int) -> int:
         return int(self._L.vest_ctx_local_nnz(self.h, mode))
+
+
+# ----------------------------------------------------------- native NCCL --
+class NcclNative:
+    """The exchanges as native NCCL collectives on the library's stream
+    (vest_ctx_set_nccl): rank 0 makes the unique id, torch.distributed
+    distributes it (any backend), every rank installs the communicator with the
+    row bounds of every mode.  No host callback per exchange."""
+
+    def install(self, dev: "ShardDevice"):
+        import torch.distributed as dist
+
+        L = _lib.lib()
+        buf = (C.c_char * 128)()
+        if dev.rank == 0:
+            check(L.vest_nccl_unique_id(C.cast(buf, C.c_void_p)))
+        obj = [bytes(buf) if dev.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        bounds = np.concatenate([np.asarray(b, np.uint64) for b in dev.bounds])
+        check(L.vest_ctx_set_nccl(dev.h, dev.rank, dev.world, C.cast(uid, C.c_void_p), ptr(bounds, u64p)))
 
 
 # ------------------------------------------------------------- torch comm --
