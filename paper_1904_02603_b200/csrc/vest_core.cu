@@ -12,7 +12,7 @@
 //   H_(f,c),(f',c')    = sum_e p p           = sum_slices A_m[s,c]A_m[s,c'] * S^s_ff'
 // with R^s_f = sum_{e in s} s_ef r_e and S^s_ff' = sum_{e in s} s_ef s_ef'.
 // One pass over the entries (k_core_pass) produces (S, R) per slice chunk,
-// a small GEMM over the slices (k_core_gemm + k_colsum) produces (T, C), and one
+// a small GEMM over the slices (k_core_gemm_tc) produces (T, C), and one
 // warp solves the block's cells sequentially (k_core_solve):
 //   num_q = c_q - sum_{q' < q} dg_q' H_q'q + g_old H_qq ,  den_q = H_qq
 // which is exactly the reference's num/den (updates.hpp:211-217) for the
@@ -28,20 +28,33 @@
 
 namespace vest {
 
-constexpr int kFMax = 15;  // fibers per block (general pass: 15 s-columns + r on DMMA)
-constexpr int kPassWarps = 8;
+constexpr int kFMax = 31;       // fibers per block (31 s-columns + r: a 32-column DMMA Gram)
+constexpr int kSolveCells = 160;  // live cells per block (dense Gram of the block in shared memory)
+#ifndef VEST_PASS_WARPS
+#define VEST_PASS_WARPS 4
+#endif
+constexpr int kPassWarps = VEST_PASS_WARPS;
+
+// A block's fibers as the pass kernel reads them: the shared-memory stage row
+// of each fiber's factor values (compile-time fiber index in the unrolled
+// loops -> constant-bank operands).  Fibers are in row-major order, so
+// consecutive fibers usually share the prefix beta_0..beta_{m-2}; its product
+// w is recomputed only where the prefix changes (newp).
+struct FibTab {
+  int nf;
+  int last[kFMax];                 // stage row of beta_{m-1}(f)
+  int pre[kFMax][VEST_MAXN - 2];   // stage rows of beta_k(f), k < m-1
+  int newp[kFMax];
+};
 
 struct CorePassArgs {
   DevModel m;
   DevCSF csf;  // mode N-1
   double* r;
-  // block fibers: prefix lin index over modes 0..m-1
-  const uint32_t* prev_fib;
-  int prev_nf;
-  const double* prev_dg;  // [prev_nf][Jm]
-  const uint32_t* cur_fib;
-  int cur_nf;
+  const double* prev_dg;  // [prev.nf][Jm]
+  FibTab prev, cur;
   int kind;  // 0 sweep (S, R), 1 responsibility (R, D), 2 final (apply prev, sum r^2)
+  int tot;   // sum_{k<m} J_k (stage rows)
   double* stats;
   int stride;
   double* chunk_sq;
@@ -55,75 +68,90 @@ __device__ __forceinline__ void sfor(F&& f) {
   }
 }
 
-template <int V>
-__device__ __forceinline__ void treduce(double (&v)[V], int lane) {
-  sfor<0, 5>([&](auto sc) {
-    constexpr int s = decltype(sc)::value;
-    constexpr int H = (V >> s) / 2;
-    constexpr int off = 16 >> s;
-    const bool up = (lane & off) != 0;
+// Gram of the NT*8 staged columns of 32 entries on DMMA: upper tiles (I <= J)
+// of X^T X, tile t in row-major order over I <= J.
+template <int NT>
+__device__ __forceinline__ void gram_nt(const double* X, double (&d)[NT * (NT + 1) / 2][2], int lane) {
+  const int g = lane >> 2, tq = lane & 3;
 #pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const double keep = up ? v[i + H] : v[i];
-      const double send = up ? v[i] : v[i + H];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+  for (int kk = 0; kk < 8; ++kk) {
+    const int e = 4 * kk + tq;
+    double f[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) f[i] = X[(8 * i + g) * kXld + e];
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NT; ++I)
+#pragma unroll
+      for (int J = I; J < NT; ++J) {
+        dmma884(d[t][0], d[t][1], f[I], f[J]);
+        ++t;
+      }
+  }
+}
+
+// fiber product s_f = prod_{k<m} A_k[i_k, beta_k(f)] from the lane's staged
+// rows, reusing the running prefix product w
+template <int M>
+__device__ __forceinline__ double fiber_product(const FibTab& T, int f, const double* st, int lane, double& w) {
+  if constexpr (M > 1) {
+    if (T.newp[f]) {
+      w = st[T.pre[f][0] * 32 + lane];
+#pragma unroll
+      for (int k = 1; k < M - 1; ++k) w *= st[T.pre[f][k] * 32 + lane];
     }
-  });
+    return w * st[T.last[f] * 32 + lane];
+  } else {
+    return st[T.last[f] * 32 + lane];
+  }
 }
 
 // One warp per chunk of a last-mode slice (runtime ranks / sparse fiber
 // lists).  Per entry: the rows of modes < m are gathered once (vector loads,
 // all issued before use) into a lane-major shared-memory stage; the previous
-// block's residual update and the current block's fiber products
-// s_f = prod_k row_k[beta_k(f)] read it; the (s_0..s_{nf-1}, r) vectors are
-// staged transposed (r in column 15) and S = sum s s^T, R = sum s r are
-// accumulated on the FP64 tensor cores (DMMA), as in the structured pass.
-template <int M>
-__global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
+// block's residual update and the current block's fiber products read it;
+// the (s_0..s_{nf-1}, r) vectors are staged transposed (r in the last column)
+// and S = sum s s^T, R = sum s r are accumulated on the FP64 tensor cores
+// (DMMA).  NT = 2 (<= 15 fibers) or 4 (<= 31 fibers) column tiles.
+template <int M, int NT>
+__global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(const __grid_constant__ CorePassArgs a) {
   extern __shared__ double smem[];
-  __shared__ int sb[2][kFMax][M > 0 ? M : 1];  // beta of each fiber (prev, cur)
-  __shared__ double sdg[kFMax * VEST_MAXJ];
   __shared__ double sq_q[kPassWarps][kFMax];
+  constexpr int NC = NT * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Jm = a.m.J[M];
-  for (int t = threadIdx.x; t < 2 * kFMax * M; t += blockDim.x) {
-    const int which = t / (kFMax * M), rest = t % (kFMax * M), f = rest / M, k = rest % M;
-    const uint32_t* fl = which ? a.cur_fib : a.prev_fib;
-    const int nf = which ? a.cur_nf : a.prev_nf;
-    int b = 0;
-    if (f < nf) b = (a.m.cellbeta[fl[f] * Jm] >> (4 * k)) & 15u;
-    sb[which][f][k] = b;
-  }
-  for (int t = threadIdx.x; t < kFMax * Jm; t += blockDim.x)
-    sdg[t] = (a.prev_nf > 0 && t < a.prev_nf * Jm) ? a.prev_dg[t] : 0.0;
-  int offs[M > 0 ? M : 1];
-  int tot = 0;
+  int offs[M];
+  {
+    int tot = 0;
 #pragma unroll
-  for (int k = 0; k < M; ++k) {
-    offs[k] = tot;
-    tot += a.m.J[k];
+    for (int k = 0; k < M; ++k) {
+      offs[k] = tot;
+      tot += a.m.J[k];
+    }
   }
-  double* st = smem + (size_t)warp * (tot * 32 + 16 * kXld);
-  double* X = st + tot * 32;
-  for (int t = lane; t < 16 * kXld; t += 32) X[t] = 0.0;
-  __syncthreads();
+  double* st = smem + (size_t)warp * (a.tot * 32 + NC * kXld);
+  double* X = st + a.tot * 32;
   const uint32_t ci = blockIdx.x * kPassWarps + warp;
   if (ci >= a.csf.nchunks) return;
+  for (int t = lane; t < NC * kXld; t += 32) X[t] = 0.0;
   const Chunk ch = a.csf.chunks[ci];
 
   // q_f = sum_c A_m[s, c] dg_prev[f][c]
   const double* arow = a.m.factor[M] + (size_t)ch.row * a.m.ld[M];
   if (lane < kFMax) {
     double t = 0.0;
-    if (lane < a.prev_nf)
-      for (int c = 0; c < Jm; ++c) t = fma(__ldg(arow + c), sdg[lane * Jm + c], t);
+    if (lane < a.prev.nf)
+      for (int c = 0; c < Jm; ++c) t = fma(__ldg(arow + c), __ldg(a.prev_dg + lane * Jm + c), t);
     sq_q[warp][lane] = t;
   }
   __syncwarp();
 
-  double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  constexpr int NTT = NT * (NT + 1) / 2;
+  double d[NTT][2];
+#pragma unroll
+  for (int t = 0; t < NTT; ++t) d[t][0] = d[t][1] = 0.0;
   double sq = 0.0;
-  const int nf = a.cur_nf;
+  const int nf = a.cur.nf;
   const bool acc = a.kind != 2 && nf > 0;
 
   for (uint32_t base = ch.beg; base < ch.end; base += 32) {
@@ -131,7 +159,7 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
     const bool valid = pos < ch.end;
     double r = 0.0;
     if (valid) {
-      uint32_t idx[M > 0 ? M : 1];
+      uint32_t idx[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) idx[k] = __ldg(a.csf.oc[k] + pos);
       r = a.r[pos];
@@ -150,16 +178,11 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
       }
     }
     __syncwarp();
-    if (valid && a.prev_nf > 0) {
-      double t = 0.0;
+    if (valid && a.prev.nf > 0) {
+      double t = 0.0, w = 1.0;
 #pragma unroll
       for (int f = 0; f < kFMax; ++f) {
-        if (f < a.prev_nf) {
-          double s = 1.0;
-#pragma unroll
-          for (int k = 0; k < M; ++k) s *= st[(offs[k] + sb[0][f][k]) * 32 + lane];
-          t = fma(s, sq_q[warp][f], t);
-        }
+        if (f < a.prev.nf) t = fma(fiber_product<M>(a.prev, f, st, lane, w), sq_q[warp][f], t);
       }
       r -= t;
       if (a.kind != 1) a.r[pos] = r;
@@ -170,21 +193,17 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
       continue;
     }
     if (acc) {
+      double w = 1.0;
 #pragma unroll
-      for (int f = 0; f < kFMax; ++f) {
+      for (int f = 0; f < NC - 1 && f < kFMax; ++f) {
         if (f < nf) {
-          double v = 0.0;
-          if (valid) {
-            v = 1.0;
-#pragma unroll
-            for (int k = 0; k < M; ++k) v *= st[(offs[k] + sb[1][f][k]) * 32 + lane];
-          }
-          X[f * kXld + lane] = v;
+          const double v = fiber_product<M>(a.cur, f, st, lane, w);
+          X[f * kXld + lane] = valid ? v : 0.0;
         }
       }
-      X[15 * kXld + lane] = valid ? r : 0.0;
+      X[(NC - 1) * kXld + lane] = valid ? r : 0.0;
       __syncwarp();
-      gram_dmma<16>(X, d, lane);
+      gram_nt<NT>(X, d, lane);
     }
     __syncwarp();
   }
@@ -197,160 +216,27 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(CorePassArgs a) {
   if (!acc) return;
   double* out = a.stats + (size_t)ci * a.stride;
   const int NS = nf * (nf + 1) / 2;
+  const int g = lane >> 2, tq = lane & 3;
+  int t = 0;
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
+  for (int I = 0; I < NT; ++I) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      int row, col;
-      gram_coord(t, i, lane, row, col);
-      const double v = d[t][i];
-      if (a.kind == 0) {
-        if (row <= col && col < nf) out[row * nf - row * (row - 1) / 2 + (col - row)] = v;
-        else if (col == 15 && row < nf) out[NS + row] = v;
-      } else {
-        if (col == 15 && row < nf) out[row] = v;
-        else if (row == col && row < nf) out[nf + row] = v;
-      }
-    }
-  }
-}
-
-// T[pS][pA] = sum_chunks S[pS] * (a_c a_c')[pA], C[f][c] = sum R[f] a_c
-// (kind 0), or C = sum R a_c, D = sum D a_c^2 (kind 1).  Each CTA covers a
-// contiguous range of chunks and writes its partial sums; k_colsum adds the
-// partials in CTA order (deterministic).
-struct CoreGemmArgs {
-  const double* stats;
-  int stride;
-  const Chunk* chunks;
-  uint32_t nchunks;
-  const double* A;  // factor of the last mode
-  int ld, Jm, nf, kind;
-  int NS, NAm, nT, nout;
-  double* partial;
-};
-
-constexpr int kGemmThreads = 256;
-constexpr int kGemmBatch = 16;
-constexpr int kTileMax = 2;  // 4x4 tiles per thread
-
-__global__ void __launch_bounds__(kGemmThreads) k_core_gemm(CoreGemmArgs a) {
-  extern __shared__ double sm[];
-  const int NSp = (a.NS + 3) & ~3, NAp = (a.NAm + 3) & ~3;
-  double* sS = sm;                                  // [batch][NSp]
-  double* sA = sS + kGemmBatch * NSp;               // [batch][NAp]
-  double* sR = sA + kGemmBatch * NAp;               // [batch][nf] (R) and [batch][nf] (D)
-  double* sa = sR + kGemmBatch * 2 * kFMax;         // [batch][Jm]
-  const uint32_t per = (a.nchunks + gridDim.x - 1) / gridDim.x;
-  const uint32_t c0 = blockIdx.x * per;
-  const uint32_t c1 = min(a.nchunks, c0 + per);
-  const int tilesS = NSp / 4, tilesA = NAp / 4;
-  const int ntiles = a.kind == 0 ? tilesS * tilesA : 0;
-  double acc[kTileMax][16];
+    for (int J = I; J < NT; ++J) {
 #pragma unroll
-  for (int k = 0; k < kTileMax; ++k)
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[k][i] = 0.0;
-  double accC = 0.0, accD = 0.0;
-  const int nfj = a.nf * a.Jm;
-  for (uint32_t cb = c0; cb < c1; cb += kGemmBatch) {
-    const int nb = min((uint32_t)kGemmBatch, c1 - cb);
-    __syncthreads();
-    // stage the batch
-    for (int t = threadIdx.x; t < kGemmBatch * NSp; t += blockDim.x) {
-      const int b = t / NSp, p = t % NSp;
-      double v = 0.0;
-      if (b < nb && a.kind == 0 && p < a.NS) v = a.stats[(size_t)(cb + b) * a.stride + p];
-      sS[t] = v;
-    }
-    for (int t = threadIdx.x; t < kGemmBatch * 2 * kFMax; t += blockDim.x) {
-      const int b = t / (2 * kFMax), p = t % (2 * kFMax);
-      double v = 0.0;
-      if (b < nb) {
+      for (int i = 0; i < 2; ++i) {
+        const int row = 8 * I + g, col = 8 * J + 2 * tq + i;
+        const double v = d[t][i];
         if (a.kind == 0) {
-          if (p < a.nf) v = a.stats[(size_t)(cb + b) * a.stride + a.NS + p];
-        } else if (p < 2 * a.nf) {
-          v = a.stats[(size_t)(cb + b) * a.stride + p];
-        }
-      }
-      sR[t] = v;
-    }
-    for (int t = threadIdx.x; t < kGemmBatch * a.Jm; t += blockDim.x) {
-      const int b = t / a.Jm, c = t % a.Jm;
-      sa[t] = b < nb ? __ldg(a.A + (size_t)a.chunks[cb + b].row * a.ld + c) : 0.0;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < kGemmBatch * NAp; t += blockDim.x) {
-      const int b = t / NAp, p = t % NAp;
-      double v = 0.0;
-      if (p < a.NAm) {
-        int c = 0, rem = p;
-        while (rem >= a.Jm - c) {
-          rem -= a.Jm - c;
-          ++c;
-        }
-        v = sa[b * a.Jm + c] * sa[b * a.Jm + c + rem];
-      }
-      sA[t] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kTileMax; ++k) {
-      const int tile = threadIdx.x + k * blockDim.x;
-      if (tile < ntiles) {
-        const int ts = tile / tilesA, ta = tile % tilesA;
-        for (int b = 0; b < kGemmBatch; ++b) {
-          const double4 sv = *reinterpret_cast<const double4*>(sS + b * NSp + 4 * ts);
-          const double4 av = *reinterpret_cast<const double4*>(sA + b * NAp + 4 * ta);
-          const double s4[4] = {sv.x, sv.y, sv.z, sv.w};
-          const double a4[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[k][i * 4 + j] = fma(s4[i], a4[j], acc[k][i * 4 + j]);
-        }
-      }
-    }
-    if (threadIdx.x < nfj) {
-      const int f = threadIdx.x / a.Jm, c = threadIdx.x % a.Jm;
-      for (int b = 0; b < kGemmBatch; ++b) {
-        const double av = sa[b * a.Jm + c];
-        if (a.kind == 0) {
-          accC = fma(sR[b * 2 * kFMax + f], av, accC);
+          if (row <= col && col < nf) out[row * nf - row * (row - 1) / 2 + (col - row)] = v;
+          else if (col == NC - 1 && row < nf) out[NS + row] = v;
         } else {
-          accC = fma(sR[b * 2 * kFMax + f], av, accC);
-          accD = fma(sR[b * 2 * kFMax + a.nf + f], av * av, accD);
+          if (col == NC - 1 && row < nf) out[row] = v;
+          else if (row == col && row < nf) out[nf + row] = v;
         }
       }
+      ++t;
     }
   }
-  double* out = a.partial + (size_t)blockIdx.x * a.nout;
-#pragma unroll
-  for (int k = 0; k < kTileMax; ++k) {
-    const int tile = threadIdx.x + k * blockDim.x;
-    if (tile < ntiles) {
-      const int ts = tile / tilesA, ta = tile % tilesA;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int ps = 4 * ts + i, pa = 4 * ta + j;
-          if (ps < a.NS && pa < a.NAm) out[ps * a.NAm + pa] = acc[k][i * 4 + j];
-        }
-    }
-  }
-  if (threadIdx.x < nfj) {
-    out[a.nT + threadIdx.x] = accC;
-    if (a.kind == 1) out[a.nT + nfj + threadIdx.x] = accD;
-  }
-}
-
-__global__ void k_colsum(const double* partial, int nparts, int n, double* out) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= n) return;
-  double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += partial[(size_t)p * n + o];
-  out[o] = s;
 }
 
 __device__ __forceinline__ int tri(int i, int j, int n) {  // i <= j
@@ -372,6 +258,7 @@ struct GemmTcArgs {
   const double* A;
   int ld, Jm, nf, kind;
   int LW, RW, MT, NT;
+  int MTy;          // row tiles per CTA row (blockIdx.y): large blocks split the L rows
   double* partial;  // [gridDim.x][MT*NT][64]
 };
 
@@ -383,7 +270,7 @@ constexpr int kTcLd = 36;  // == 4 mod 16: conflict-free fragment loads
 __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
   extern __shared__ double sm[];
   double* Lt = sm;                           // [MT*8][kTcLd]
-  double* Rt = Lt + a.MT * 8 * kTcLd;        // [NT*8][kTcLd]
+  double* Rt = Lt + a.MTy * 8 * kTcLd;       // [NT*8][kTcLd]
   double* sa = Rt + a.NT * 8 * kTcLd;        // [32][Jm]
   int* rmap = reinterpret_cast<int*>(sa + 32 * a.Jm);  // Rt column -> (c, c') packed
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -407,7 +294,9 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
     rmap[col] = v;
   }
   const int g = lane >> 2, tq = lane & 3;
-  const int ntiles = a.MT * a.NT;
+  const int mt0 = blockIdx.y * a.MTy;
+  const int MTl = min(a.MTy, a.MT - mt0);
+  const int ntiles = MTl * a.NT;
   const uint32_t per = ((a.nchunks + gridDim.x - 1) / gridDim.x + 31) & ~31u;
   const uint32_t c0 = blockIdx.x * per;
   const uint32_t c1 = min(a.nchunks, c0 + per);
@@ -415,7 +304,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
 #pragma unroll
   for (int i = 0; i < kTcTilesPerWarp; ++i) acc[i][0] = acc[i][1] = 0.0;
   const int Jm = a.Jm;
-  const int LWp = a.MT * 8;
+  const int LWp = MTl * 8;
   // software pipeline: the next batch's statistics rows and last-mode factor
   // rows are loaded into registers while the current batch runs on DMMA
   constexpr int kLPer = kTcLPer, kAPer = 2;  // per-thread staging share (LWp*32 <= kTcLPer*256, 32*Jm <= 512)
@@ -426,7 +315,9 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
     for (int i = 0; i < kLPer; ++i) {
       const int t = threadIdx.x + i * blockDim.x;
       const int k = t / LWp, col = t - k * LWp;
-      lv[i] = (t < LWp * 32 && k < nb && col < a.LW) ? a.stats[(size_t)(cb + k) * a.stride + col] : 0.0;
+      lv[i] = (t < LWp * 32 && k < nb && mt0 * 8 + col < a.LW)
+                  ? a.stats[(size_t)(cb + k) * a.stride + mt0 * 8 + col]
+                  : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < kAPer; ++i) {
@@ -479,7 +370,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) k_core_gemm_tc(GemmTcArgs a) {
       }
     }
   }
-  double* out = a.partial + (size_t)blockIdx.x * ntiles * 64;
+  double* out = a.partial + (size_t)blockIdx.x * a.MT * a.NT * 64 + (size_t)mt0 * a.NT * 64;
 #pragma unroll
   for (int i = 0; i < kTcTilesPerWarp; ++i) {
     const int tile = warp + kTcWarps * i;
@@ -532,72 +423,87 @@ __global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, i
   out[o] = s;
 }
 
-// Sequential Gauss-Seidel over the block's cells.  The CTA loads [T | C],
-// the block's core values and masks into shared memory and expands the dense
-// cell Gram H (nq x nq, H_qq' = T[{f,f'}][{c,c'}]); then one warp runs the
-// nq sequential steps, each a handful of shared-memory reads plus one
-// coalesced row update of the remaining cells' c.
-__global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, int Jm, const uint32_t* fib,
+// Sequential Gauss-Seidel over the block's live cells.  The CTA compacts the
+// block's unmasked cells (ballot scan, row-major order), loads [T | C], their
+// core values into shared memory and expands the dense live-cell Gram H
+// (nl x nl, H_qq' = T[{f,f'}][{c,c'}]); then one warp runs the nl sequential
+// steps, each a handful of shared-memory reads plus one coalesced row update
+// of the remaining cells' c.  Masked cells keep dg = 0 (updates.hpp:199-202).
+__global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, int Jm, int nl, const uint32_t* fib,
                                                     double* core, const uint8_t* core_mask, int reg,
                                                     double lambda, double* dg_out) {
   extern __shared__ double sm[];
   const int NAm = Jm * (Jm + 1) / 2;
   const int nT = nf * (nf + 1) / 2 * NAm;
   const int nq = nf * Jm;
-  double* H = sm;             // nq x nq
-  double* cc = H + nq * nq;   // nq
-  double* gv = cc + nq;       // nq
-  double* mk = gv + nq;       // nq
-  double* rd = mk + nq;       // nq: 1 / (H_qq + lambda) (LF) or 1 / (2 H_qq) (L1)
-  for (int t = threadIdx.x; t < nq * nq; t += blockDim.x) {
-    const int q = t / nq, q2 = t % nq;
+  double* H = sm;             // nl x nl
+  double* cc = H + nl * nl;   // nl
+  double* gv = cc + nl;       // nl
+  double* rd = gv + nl;       // nl: 1 / (H_qq + lambda) (LF) or 1 / (2 H_qq) (L1)
+  int* lq = reinterpret_cast<int*>(rd + nl);  // live cell -> q
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) dg_out[q] = 0.0;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int n = 0;
+    for (int base = 0; base < nq; base += 32) {
+      const int q = base + lane;
+      const bool live = q < nq && !core_mask[(int)fib[q / Jm] * Jm + q % Jm];
+      const unsigned bal = __ballot_sync(0xffffffffu, live);
+      if (live) lq[n + __popc(bal & ((1u << lane) - 1u))] = q;
+      n += __popc(bal);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nl * nl; t += blockDim.x) {
+    const int q = lq[t / nl], q2 = lq[t % nl];
     const int f = q / Jm, c = q % Jm, f2 = q2 / Jm, c2 = q2 % Jm;
     const int ps = f <= f2 ? tri(f, f2, nf) : tri(f2, f, nf);
     const int pa = c <= c2 ? tri(c, c2, Jm) : tri(c2, c, Jm);
     H[t] = tc[ps * NAm + pa];
   }
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
-    cc[q] = tc[nT + q];
-    const int lin = (int)fib[q / Jm] * Jm + q % Jm;
-    gv[q] = core[lin];
-    mk[q] = core_mask[lin] ? 1.0 : 0.0;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const int q = lq[l];
+    cc[l] = tc[nT + q];
+    gv[l] = core[(int)fib[q / Jm] * Jm + q % Jm];
     // the denominators do not depend on the sweep state: invert them in
     // parallel, off the sequential critical path
     const int f = q / Jm, c = q % Jm;
     const double hqq = tc[tri(f, f, nf) * NAm + tri(c, c, Jm)];
     const double den = reg == 0 ? hqq + lambda : 2.0 * hqq;
-    rd[q] = den != 0.0 ? 1.0 / den : 0.0;
+    rd[l] = den != 0.0 ? 1.0 / den : 0.0;
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  for (int q = 0; q < nq; ++q) {
+  for (int l = 0; l < nl; ++l) {
     double dg = 0.0;
-    if (mk[q] == 0.0) {
-      const double hqq = H[q * nq + q];
-      const double g_old = gv[q];
-      const double num = cc[q] + g_old * hqq;
-      const double den = hqq;
-      double g_new = g_old;
-      const double r = rd[q];
-      if (reg == 0) {
-        if (den + lambda != 0.0) g_new = num * r;
-      } else {
-        const double g = -2.0 * num;
-        if (2.0 * den != 0.0) g_new = g > lambda ? (lambda - g) * r : (g < -lambda ? -(lambda + g) * r : 0.0);
-      }
-      if (g_new != g_old) dg = g_new - g_old;
-      if (lane == 0) gv[q] = g_new;
+    const double hqq = H[l * nl + l];
+    const double g_old = gv[l];
+    const double num = cc[l] + g_old * hqq;
+    const double den = hqq;
+    double g_new = g_old;
+    const double r = rd[l];
+    if (reg == 0) {
+      if (den + lambda != 0.0) g_new = num * r;
+    } else {
+      const double g = -2.0 * num;
+      if (2.0 * den != 0.0) g_new = g > lambda ? (lambda - g) * r : (g < -lambda ? -(lambda + g) * r : 0.0);
     }
-    if (lane == 0) dg_out[q] = dg;
+    if (g_new != g_old) dg = g_new - g_old;
+    if (lane == 0) {
+      gv[l] = g_new;
+      dg_out[lq[l]] = dg;
+    }
     if (dg != 0.0) {
-      const double* hr = H + q * nq;
-      for (int q2 = q + 1 + lane; q2 < nq; q2 += 32) cc[q2] = fma(-dg, hr[q2], cc[q2]);
+      const double* hr = H + l * nl;
+      for (int l2 = l + 1 + lane; l2 < nl; l2 += 32) cc[l2] = fma(-dg, hr[l2], cc[l2]);
     }
     __syncwarp();
   }
-  for (int q = lane; q < nq; q += 32)
-    if (mk[q] == 0.0) core[(int)fib[q / Jm] * Jm + q % Jm] = gv[q];
+  for (int l = lane; l < nl; l += 32) {
+    const int q = lq[l];
+    core[(int)fib[q / Jm] * Jm + q % Jm] = gv[l];
+  }
 }
 
 // Closed-form core responsibility (pruning.hpp:98-134): zeroing cell beta
@@ -652,24 +558,62 @@ bool legacy_block_passes() {
 struct Blocks {
   std::vector<uint32_t> fib;    // fibers of all blocks, row-major order
   std::vector<int> start, len;  // block ranges into fib
+  std::vector<int> nlive;       // general plan: unmasked cells of the block
   std::vector<int> prefix;      // structured plan: the block's prefix p
 };
 
-// General plan: runs of F consecutive live fibers.
+// General plan: runs of <= F consecutive live fibers (a fiber is live when
+// one of its cells is unmasked) holding <= kSolveCells unmasked cells.
 Blocks plan_blocks(const Ctx& c, int F) {
   Blocks b;
   const int Jm = c.ranks[c.N - 1];
   const int P = c.G / Jm;
+  std::vector<int> nl;
   for (int p = 0; p < P; ++p) {
-    bool live = false;
-    for (int q = 0; q < Jm && !live; ++q) live = !c.h_core_mask[(size_t)p * Jm + q];
-    if (live) b.fib.push_back(p);
+    int n = 0;
+    for (int q = 0; q < Jm; ++q) n += !c.h_core_mask[(size_t)p * Jm + q];
+    if (n > 0) {
+      b.fib.push_back(p);
+      nl.push_back(n);
+    }
   }
-  for (int s = 0; s < (int)b.fib.size(); s += F) {
+  for (int s = 0; s < (int)b.fib.size();) {
+    int len = 0, cells = 0;
+    while (s + len < (int)b.fib.size() && len < F && cells + nl[s + len] <= kSolveCells) cells += nl[s + len++];
     b.start.push_back(s);
-    b.len.push_back(std::min(F, (int)b.fib.size() - s));
+    b.len.push_back(len);
+    b.nlive.push_back(cells);
+    s += len;
   }
   return b;
+}
+
+// The pass kernel's view of a block's fibers (see FibTab).
+FibTab make_tab(const Ctx& c, const Blocks& b, int bi) {
+  FibTab t{};
+  if (bi < 0) return t;
+  const int m = c.N - 1;
+  int offs[VEST_MAXN] = {};
+  for (int k = 1; k < m; ++k) offs[k] = offs[k - 1] + c.ranks[k - 1];
+  t.nf = b.len[bi];
+  int prevb[VEST_MAXN] = {};
+  for (int f = 0; f < t.nf; ++f) {
+    uint32_t p = b.fib[b.start[bi] + f];  // row-major index over modes 0..m-1
+    int beta[VEST_MAXN] = {};
+    for (int k = m - 1; k >= 0; --k) {
+      beta[k] = (int)(p % (uint32_t)c.ranks[k]);
+      p /= (uint32_t)c.ranks[k];
+    }
+    t.last[f] = offs[m - 1] + beta[m - 1];
+    bool same = f > 0;
+    for (int k = 0; k < m - 1; ++k) {
+      t.pre[f][k] = offs[k] + beta[k];
+      same = same && beta[k] == prevb[k];
+      prevb[k] = beta[k];
+    }
+    t.newp[f] = same ? 0 : 1;
+  }
+  return t;
 }
 
 // Structured plan (compile-time ranks): one block per prefix over modes
@@ -690,55 +634,50 @@ Blocks plan_structured(const Ctx& c) {
   return b;
 }
 
-int pick_block(const Ctx& c) {
-  const int Jm = c.ranks[c.N - 1];
-  int F = c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax;
-  // keep the block within the solve's shared memory (dense H of (F*Jm)^2) and
-  // the tensor-core gemm's staging / tile capacity
-  while (F > 1) {
-    const int NS = F * (F + 1) / 2, NAm = Jm * (Jm + 1) / 2;
-    const int nq = F * Jm;
-    const int MT = (NS + F + 7) / 8, NT = (NAm + Jm + 7) / 8;
-    const bool solve_ok = (size_t)(nq * nq + 4 * nq) * 8 <= 200 * 1024;
-    const bool tc_ok = MT * NT <= kTcWarps * kTcTilesPerWarp && MT * 8 * 32 <= kTcLPer * 256 && 32 * Jm <= 512;
-    if (solve_ok && tc_ok) break;
-    --F;
-  }
-  return F;
-}
+// Fibers per block: up to kFMax (the live-cell cap of the solve is applied by
+// plan_blocks); the block GEMM splits its rows over CTA rows, so it imposes no
+// limit.
+int pick_block(const Ctx& c) { return c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax; }
 
 const void* structured_ops(const Ctx& c) {
   if (c.force_generic || c.N < 3 || c.core_block > 0) return nullptr;
   return find_core_ops(c.N, c.ranks);
 }
 
+template <int MM, int NT>
+void launch_pass_t(Ctx& c, const CorePassArgs& a, dim3 grid, size_t sm) {
+  check(cudaFuncSetAttribute(k_core_pass<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+        "pass smem");
+  k_core_pass<MM, NT><<<grid, kPassWarps * 32, sm, c.stream>>>(a);
+}
+
+template <int MM>
+void launch_pass_m(Ctx& c, const CorePassArgs& a, int NT) {
+  const size_t sm = (size_t)kPassWarps * (a.tot * 32 + NT * 8 * kXld) * sizeof(double);
+  const dim3 grid((a.csf.nchunks + kPassWarps - 1) / kPassWarps);
+  if (NT == 2) launch_pass_t<MM, 2>(c, a, grid, sm);
+  else if (NT == 3) launch_pass_t<MM, 3>(c, a, grid, sm);
+  else launch_pass_t<MM, 4>(c, a, grid, sm);
+}
+
 void launch_pass(Ctx& c, const CorePassArgs& a) {
   ProfScope ps(c, kProfCorePass);
   const int M = c.N - 1;
-  int tot = 0;
-  for (int k = 0; k < M; ++k) tot += c.ranks[k];
-  const size_t sm = (size_t)kPassWarps * (tot * 32 + 16 * kXld) * sizeof(double);
-  const dim3 grid((a.csf.nchunks + kPassWarps - 1) / kPassWarps);
   if (a.csf.nchunks == 0) return;
-#define VEST_PASS(MM)                                                                       \
-  case MM:                                                                                  \
-    check(cudaFuncSetAttribute(k_core_pass<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                               (int)sm),                                                    \
-          "pass smem");                                                                     \
-    k_core_pass<MM><<<grid, kPassWarps * 32, sm, c.stream>>>(a);                            \
-    break;
+  // column tiles: the block's fibers + the residual column
+  const int nf = a.kind == 2 ? 0 : a.cur.nf;
+  const int NT = nf <= 15 ? 2 : (nf <= 23 ? 3 : 4);
   switch (M) {
-    VEST_PASS(1)
-    VEST_PASS(2)
-    VEST_PASS(3)
-    VEST_PASS(4)
-    VEST_PASS(5)
-    VEST_PASS(6)
-    VEST_PASS(7)
+    case 1: launch_pass_m<1>(c, a, NT); break;
+    case 2: launch_pass_m<2>(c, a, NT); break;
+    case 3: launch_pass_m<3>(c, a, NT); break;
+    case 4: launch_pass_m<4>(c, a, NT); break;
+    case 5: launch_pass_m<5>(c, a, NT); break;
+    case 6: launch_pass_m<6>(c, a, NT); break;
+    case 7: launch_pass_m<7>(c, a, NT); break;
     default:
       throw ArgError{"unsupported order"};
   }
-#undef VEST_PASS
   count_launch();
   check(cudaGetLastError(), "core pass");
 }
@@ -764,78 +703,56 @@ void run_pass(Ctx& c, const void* sops, const Blocks& b, int prev, int cur, int 
   a.chunk_sq = c.d_chunk_sum;
   a.prev_dg = c.d_dg;
   a.kind = kind;
-  a.cur_fib = cur >= 0 ? c.d_fibers + b.start[cur] : c.d_fibers;
-  a.cur_nf = cur >= 0 ? b.len[cur] : 0;
-  a.prev_fib = prev >= 0 ? c.d_fibers + b.start[prev] : c.d_fibers;
-  a.prev_nf = prev >= 0 ? b.len[prev] : 0;
+  a.cur = make_tab(c, b, cur);
+  a.prev = make_tab(c, b, prev);
+  for (int k = 0; k < m; ++k) a.tot += c.ranks[k];
   launch_pass(c, a);
 }
 
 // (T, C) or (C, D) for one block into c.d_gemm_out; returns nout.
 int block_gemm(Ctx& c, int nf, int kind, int stride) {
   const int m = c.N - 1, Jm = c.ranks[m];
-  CoreGemmArgs g{};
-  g.stats = c.d_chunk_stats;
-  g.stride = stride;
-  g.chunks = c.modes[m].d_chunks;
-  g.nchunks = c.modes[m].nchunks;
-  g.A = c.d_factor[m];
-  g.ld = c.ld[m];
-  g.Jm = Jm;
-  g.nf = nf;
-  g.kind = kind;
-  g.NS = kind == 0 ? nf * (nf + 1) / 2 : 0;
-  g.NAm = Jm * (Jm + 1) / 2;
-  g.nT = kind == 0 ? g.NS * g.NAm : 0;
-  g.nout = g.nT + (kind == 0 ? 1 : 2) * nf * Jm;
-  int nblocks = 0;
-  cudaDeviceGetAttribute(&nblocks, cudaDevAttrMultiProcessorCount, c.device);
-  nblocks = std::max(1, std::min<int>(2 * nblocks, (g.nchunks + kGemmBatch - 1) / kGemmBatch));
-  ensure(c, &c.d_gemm_part, &c.gemm_part_cap, (size_t)nblocks * g.nout);
-  ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)g.nout);
-  g.partial = c.d_gemm_part;
+  const int NS = kind == 0 ? nf * (nf + 1) / 2 : 0;
+  const int NAm = Jm * (Jm + 1) / 2;
+  const int nout = (kind == 0 ? NS * NAm : 0) + (kind == 0 ? 1 : 2) * nf * Jm;
+  ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)nout);
   ProfScope ps(c, kProfCoreGemm);
   GemmTcArgs t{};
-  t.stats = g.stats;
+  t.stats = c.d_chunk_stats;
   t.stride = stride;
-  t.chunks = g.chunks;
-  t.nchunks = g.nchunks;
-  t.A = g.A;
-  t.ld = g.ld;
+  t.chunks = c.modes[m].d_chunks;
+  t.nchunks = c.modes[m].nchunks;
+  t.A = c.d_factor[m];
+  t.ld = c.ld[m];
   t.Jm = Jm;
   t.nf = nf;
   t.kind = kind;
-  t.LW = kind == 0 ? g.NS + nf : 2 * nf;
-  t.RW = kind == 0 ? g.NAm + Jm : 2 * Jm;
+  t.LW = kind == 0 ? NS + nf : 2 * nf;
+  t.RW = kind == 0 ? NAm + Jm : 2 * Jm;
   t.MT = (t.LW + 7) / 8;
   t.NT = (t.RW + 7) / 8;
+  // row tiles per CTA row: the staging (kTcLPer per thread) and the warps'
+  // tile slots bound it
+  t.MTy = std::min({t.MT, kTcLPer * 256 / 256, kTcWarps * kTcTilesPerWarp / t.NT});
+  const int ysplit = (t.MT + t.MTy - 1) / t.MTy;
   const int ntiles = t.MT * t.NT;
-  if (ntiles <= kTcWarps * kTcTilesPerWarp && t.MT * 8 * 32 <= kTcLPer * 256 && 32 * Jm <= 2 * 256) {
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    const int nparts = std::max(1, std::min<int>(2 * sms, (g.nchunks + 31) / 32));
-    const int n = ntiles * 64;
-    const int groups = 16;
-    ensure(c, &c.d_gemm_part, &c.gemm_part_cap, (size_t)nparts * n + (size_t)groups * n);
-    t.partial = c.d_gemm_part;
-    double* raw = c.d_gemm_part + (size_t)nparts * n;
-    const size_t sm = ((size_t)(t.MT + t.NT) * 8 * kTcLd + 32 * Jm) * sizeof(double) + (size_t)t.NT * 8 * sizeof(int);
-    check(cudaFuncSetAttribute(k_core_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gemm smem");
-    k_core_gemm_tc<<<nparts, kTcWarps * 32, sm, c.stream>>>(t);
-    k_gemm_reduce1<<<dim3((n + 255) / 256, groups), 256, 0, c.stream>>>(t.partial, nparts, n, groups, raw);
-    k_gemm_reduce2<<<(g.nout + 255) / 256, 256, 0, c.stream>>>(raw, n, groups, kind, nf, Jm, t.NT, c.d_gemm_out);
-    count_launch(3);
-    check(cudaGetLastError(), "core gemm (tensor cores)");
-    return g.nout;
-  }
-  const int NSp = (g.NS + 3) & ~3, NAp = (g.NAm + 3) & ~3;
-  const size_t sm = (size_t)kGemmBatch * (NSp + NAp + 2 * kFMax + Jm) * sizeof(double);
-  check(cudaFuncSetAttribute(k_core_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gemm smem");
-  k_core_gemm<<<nblocks, kGemmThreads, sm, c.stream>>>(g);
-  k_colsum<<<(g.nout + 255) / 256, 256, 0, c.stream>>>(c.d_gemm_part, nblocks, g.nout, c.d_gemm_out);
-  count_launch(2);
-  check(cudaGetLastError(), "core gemm");
-  return g.nout;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  const int nparts = std::max(1, std::min<int>(2 * sms, (t.nchunks + 31) / 32));
+  const int n = ntiles * 64;
+  const int groups = 16;
+  ensure(c, &c.d_gemm_part, &c.gemm_part_cap, (size_t)nparts * n + (size_t)groups * n);
+  t.partial = c.d_gemm_part;
+  double* raw = c.d_gemm_part + (size_t)nparts * n;
+  const size_t sm =
+      ((size_t)(t.MTy + t.NT) * 8 * kTcLd + 32 * Jm) * sizeof(double) + (size_t)t.NT * 8 * sizeof(int);
+  check(cudaFuncSetAttribute(k_core_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gemm smem");
+  k_core_gemm_tc<<<dim3(nparts, ysplit), kTcWarps * 32, sm, c.stream>>>(t);
+  k_gemm_reduce1<<<dim3((n + 255) / 256, groups), 256, 0, c.stream>>>(t.partial, nparts, n, groups, raw);
+  k_gemm_reduce2<<<(nout + 255) / 256, 256, 0, c.stream>>>(raw, n, groups, kind, nf, Jm, t.NT, c.d_gemm_out);
+  count_launch(3);
+  check(cudaGetLastError(), "core gemm (tensor cores)");
+  return nout;
 }
 
 void upload_fibers(Ctx& c, const Blocks& b) {
@@ -882,7 +799,7 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   if (sops) pack_operands(c, sops);
   const int stride = F * (F + 1) / 2 + F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
-  ensure(c, &c.d_dg, &c.dg_cap, (size_t)16 * VEST_MAXJ);
+  ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
   ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);
   const int nb = (int)b.start.size();
   for (int bi = 0; bi <= nb; ++bi) {
@@ -893,10 +810,10 @@ void core_sweep(Ctx& c, int reg, double lambda) {
     const int nout = block_gemm(c, nf, 0, stride);
     comm_allreduce(c, c.d_gemm_out, (uint64_t)nout);  // block statistics over the shards
     ProfScope ps(c, kProfCoreSolve);
-    const size_t nq = (size_t)nf * Jm;
-    const size_t sm = (nq * nq + 4 * nq) * sizeof(double);
+    const size_t nq = (size_t)nf * Jm, nl = (size_t)b.nlive[bi];
+    const size_t sm = (nl * nl + 3 * nl) * sizeof(double) + nq * sizeof(int);
     check(cudaFuncSetAttribute(k_core_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "solve smem");
-    k_core_solve<<<1, 256, sm, c.stream>>>(c.d_gemm_out, nf, Jm, c.d_fibers + b.start[bi], c.d_core,
+    k_core_solve<<<1, 256, sm, c.stream>>>(c.d_gemm_out, nf, Jm, (int)nl, c.d_fibers + b.start[bi], c.d_core,
                                            c.d_core_mask, reg, lambda, c.d_dg);
     count_launch();
     check(cudaGetLastError(), "core solve");
@@ -921,7 +838,7 @@ void core_responsibilities(Ctx& c) {
   if (sops) pack_operands(c, sops);
   const int stride = 2 * F;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
-  ensure(c, &c.d_dg, &c.dg_cap, (size_t)16 * VEST_MAXJ);
+  ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
   for (int bi = 0; bi < (int)b.start.size(); ++bi) {
     run_pass(c, sops, b, -1, bi, 1, stride);
     const int nf = b.len[bi];

@@ -57,6 +57,29 @@ __device__ __forceinline__ void load_row(const double* __restrict__ row, double 
 // ------------------------------------------------------------------ policies --
 // A policy computes delta for NE entries per lane: the CSF positions pos[e]
 // (clamped into the chunk by the caller), rows of the other modes gathered.
+#ifndef VEST_ROW_NE
+#define VEST_ROW_NE 2
+#endif
+#ifndef VEST_ROW_MINB
+#define VEST_ROW_MINB 2
+#endif
+// Shapes with N >= 4 (configs 4-5): NE = 2 entries per lane spills 100-500 B
+// per thread at the 128-register budget of 2 CTAs/SM, but measured 2-3x faster
+// than NE = 1 (one uniform constant load per DFMA is issue-bound) and than
+// NE = 2 at 1 CTA/SM (configs 4/5: 1.17/0.59 s vs 2.34/1.23 s and 1.20/0.66 s
+// per iteration).
+#ifndef VEST_ROW_NE_HI
+#define VEST_ROW_NE_HI 2
+#endif
+#ifndef VEST_ROW_MINB_HI
+#define VEST_ROW_MINB_HI 2
+#endif
+template <class S>
+struct RowTune {
+  static constexpr int NE = S::N <= 3 ? VEST_ROW_NE : VEST_ROW_NE_HI;
+  static constexpr int MINB = S::N <= 3 ? VEST_ROW_MINB : VEST_ROW_MINB_HI;
+};
+
 template <class S, int MODE>
 #ifndef VEST_ROW_TAIL1
 #define VEST_ROW_TAIL1 0  // measured slower (larger kernel body): 1.36 vs 1.27 ms per mode
@@ -71,10 +94,8 @@ struct StaticPolicy {
   static constexpr int MAXJ = S::MAXJ;
   static constexpr int JN = S::J(MODE);
   static constexpr bool kStatic = true;
-#ifndef VEST_ROW_NE
-#define VEST_ROW_NE 2
-#endif
-  static constexpr int NE = VEST_ROW_NE;  // entries per lane per round
+  static constexpr int NE = RowTune<S>::NE;  // entries per lane per round
+  static constexpr int kMinB = RowTune<S>::MINB;
   static constexpr int K0 = (MODE == 0) ? 1 : 0;
   int jn;  // unused, keeps the interface uniform
   __device__ __forceinline__ int J() const { return JN; }
@@ -132,6 +153,7 @@ struct DynPolicy {
   static constexpr int MAXJ = VEST_MAXJ;
   static constexpr bool kStatic = false;
   static constexpr int NE = 1;
+  static constexpr int kMinB = VEST_ROW_MINB;
   static constexpr int JN = VEST_MAXJ;
   int md;
   int jn;
@@ -233,6 +255,16 @@ struct TensorGram {
 };
 
 template <class P>
+constexpr int fused_resid_words() {
+  if constexpr (P::kStatic) {
+    using S = typename P::Shape;
+    return S::N >= 3 ? 128 + S::G() / S::J(S::N - 1) : 0;
+  } else {
+    return 0;
+  }
+}
+
+template <class P>
 constexpr int stage_words() {
   // per-warp shared memory: the transposed DMMA stage (16 x kXldN(NE)), or
   // 32 staged rows of (J + 1) doubles (odd stride), or the row solve area
@@ -242,7 +274,10 @@ constexpr int stage_words() {
   constexpr int sv = J * J + J;
   constexpr int tcw = 16 * kXldN(P::NE);
   constexpr int m1 = st > sv ? st : sv;
-  return m1 > tcw ? m1 : tcw;
+  constexpr int m2 = m1 > tcw ? m1 : tcw;
+  // the fused residual's v = G x_m a_row lives at offset 128 (after the solve area)
+  constexpr int fr = fused_resid_words<P>();
+  return m2 > fr ? m2 : fr;
 }
 
 // Statistics of the row's entries: on the tensor pipe for static ranks (the
@@ -293,12 +328,8 @@ __device__ __forceinline__ void fused_residual(const RowPassArgs& a, const Chunk
   }
 }
 
-#ifndef VEST_ROW_MINB
-#define VEST_ROW_MINB 2
-#endif
-
 template <class P, int KIND>
-__global__ void __launch_bounds__(kRowWarps * 32, VEST_ROW_MINB) k_rowpass(RowPassArgs a, P pol) {
+__global__ void __launch_bounds__(kRowWarps * 32, P::kMinB) k_rowpass(RowPassArgs a, P pol) {
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
