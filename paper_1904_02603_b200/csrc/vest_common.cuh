@@ -226,7 +226,7 @@ constexpr int kFullUnrollN = VEST_FULL_UNROLL;
 #endif
 constexpr int kK0Unroll = VEST_K0_UNROLL;  // unroll of the rolled k0 loop
 
-template <class S, int n, int NE, class GA>
+template <class S, int n, int NE, class GA, int K0U = kK0Unroll>
 __device__ __forceinline__ void delta_staticN(const GA& g, const double (&u)[NE][S::N][S::MAXJ],
                                               const double* const (&rows0)[NE], double (&delta)[NE][S::MAXJ]) {
   constexpr int k0 = (n == 0) ? 1 : 0;
@@ -253,7 +253,7 @@ __device__ __forceinline__ void delta_staticN(const GA& g, const double (&u)[NE]
     }
     return;
   }
-#pragma unroll kK0Unroll
+#pragma unroll K0U
   for (int a = 0; a < S::J(k0); ++a) {
     double w0[NE];
 #pragma unroll

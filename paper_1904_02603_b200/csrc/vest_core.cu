@@ -47,14 +47,33 @@ struct FibTab {
   int newp[kFMax];
 };
 
+// Prefix blocks for a compile-time last-fiber rank JL: the block is np <=
+// 31 / JL whole prefixes (beta_0..beta_{m-2}) -- all JL fibers of each, the
+// masked cells included (the solve skips them) -- so fiber (slot p, b) is
+// Gram column p * JL + b at compile time; the lane's A_{m-1} row sits in
+// registers and each prefix's product w is formed once.
+constexpr int kPreMax = 8;
+struct PreTab {
+  int nf;
+  int np;
+  int pre[kPreMax][VEST_MAXN - 2];  // stage offsets of beta_k(p), k < m-1
+};
+union BlockTab {
+  FibTab fib;
+  PreTab pre;  // nf is the common first member
+};
+
 struct CorePassArgs {
   DevModel m;
   DevCSF csf;  // mode N-1
   double* r;
   const double* prev_dg;  // [prev.nf][Jm]
-  FibTab prev, cur;
+  BlockTab prev, cur;
   int kind;  // 0 sweep (S, R), 1 responsibility (R, D), 2 final (apply prev, sum r^2)
-  int tot;   // sum_{k<m} J_k (stage rows)
+  int soff[VEST_MAXN];  // per-lane stage offset of mode k's factor row (k < m, even)
+  int rslot;            // per-lane stage slot of r
+  int prefix_plan;      // blocks are whole prefixes (PreTab)
+  int ldr;              // per-lane stage stride (== 2 mod 4: 16-byte copies, 2-way read conflicts)
   double* stats;
   int stride;
   double* chunk_sq;
@@ -91,114 +110,201 @@ __device__ __forceinline__ void gram_nt(const double* X, double (&d)[NT * (NT + 
 }
 
 // fiber product s_f = prod_{k<m} A_k[i_k, beta_k(f)] from the lane's staged
-// rows, reusing the running prefix product w
+// rows (st = the lane's stage row), reusing the running prefix product w
 template <int M>
-__device__ __forceinline__ double fiber_product(const FibTab& T, int f, const double* st, int lane, double& w) {
+__device__ __forceinline__ double fiber_product(const FibTab& T, int f, const double* st, double& w) {
   if constexpr (M > 1) {
     if (T.newp[f]) {
-      w = st[T.pre[f][0] * 32 + lane];
+      w = st[T.pre[f][0]];
 #pragma unroll
-      for (int k = 1; k < M - 1; ++k) w *= st[T.pre[f][k] * 32 + lane];
+      for (int k = 1; k < M - 1; ++k) w *= st[T.pre[f][k]];
     }
-    return w * st[T.last[f] * 32 + lane];
+    return w * st[T.last[f]];
   } else {
-    return st[T.last[f] * 32 + lane];
+    return st[T.last[f]];
   }
 }
 
-// One warp per chunk of a last-mode slice (runtime ranks / sparse fiber
-// lists).  Per entry: the rows of modes < m are gathered once (vector loads,
-// all issued before use) into a lane-major shared-memory stage; the previous
-// block's residual update and the current block's fiber products read it;
-// the (s_0..s_{nf-1}, r) vectors are staged transposed (r in the last column)
-// and S = sum s s^T, R = sum s r are accumulated on the FP64 tensor cores
-// (DMMA).  NT = 2 (<= 15 fibers) or 4 (<= 31 fibers) column tiles.
-template <int M, int NT>
+// prefix product w_p = prod_{k<m-1} A_k[i_k, beta_k(p)] (1 for m = 1)
+template <int M>
+__device__ __forceinline__ double prefix_weight(const PreTab& T, int pi, const double* st) {
+  double w = 1.0;
+  if constexpr (M > 1) {
+    w = st[T.pre[pi][0]];
+#pragma unroll
+    for (int k = 1; k < M - 1; ++k) w *= st[T.pre[pi][k]];
+  }
+  return w;
+}
+
+__device__ __forceinline__ uint32_t cp_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async8_s(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_s(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+
+// Persistent, one warp per chunk of a last-mode slice at a time (runtime
+// ranks / sparse fiber lists).  Rounds of 32 entries (one per lane): the rows
+// of modes < m and r are copied global -> shared by cp.async one round ahead
+// (coordinates two rounds ahead) into a per-lane, odd-strided stage, so the
+// gathers of the next round overlap this round's arithmetic.  Per entry: the
+// previous block's residual update and the current block's fiber products
+// read the stage; the (s_0..s_{nf-1}, r) vectors are staged transposed (r in
+// the last column) and S = sum s s^T, R = sum s r are accumulated on the FP64
+// tensor cores (DMMA).  NT = 2/3/4 column tiles (<= 15/23/31 fibers).
+template <int M, int NT, int JL, int JALL>
 __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(const __grid_constant__ CorePassArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   __shared__ double sq_q[kPassWarps][kFMax];
   constexpr int NC = NT * 8;
+  constexpr int NTT = NT * (NT + 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Jm = a.m.J[M];
-  int offs[M];
-  {
-    int tot = 0;
-#pragma unroll
-    for (int k = 0; k < M; ++k) {
-      offs[k] = tot;
-      tot += a.m.J[k];
+  const int ldr = a.ldr;
+  double* const stage = smem + (size_t)warp * (2 * 32 * ldr + NC * kXld);  // [2][32][ldr]
+  double* const X = stage + 2 * 32 * ldr;
+  for (int t = lane; t < NC * kXld; t += 32) X[t] = 0.0;  // columns >= nf stay zero
+  const int nf = a.cur.fib.nf;
+  const int pnf = a.prev.fib.nf;
+  const bool acc = a.kind != 2 && nf > 0;
+  const uint32_t wstride = gridDim.x * kPassWarps;
+
+  struct Cur {
+    uint32_t ci, beg, end, base, row;
+  };
+  auto first = [&](uint32_t ci) {
+    Cur c{ci, 0, 0, 0, 0};
+    if (ci < a.csf.nchunks) {
+      const Chunk ch = a.csf.chunks[ci];
+      c.beg = ch.beg;
+      c.end = ch.end;
+      c.base = ch.beg;
+      c.row = ch.row;
     }
-  }
-  double* st = smem + (size_t)warp * (a.tot * 32 + NC * kXld);
-  double* X = st + a.tot * 32;
-  const uint32_t ci = blockIdx.x * kPassWarps + warp;
-  if (ci >= a.csf.nchunks) return;
-  for (int t = lane; t < NC * kXld; t += 32) X[t] = 0.0;
-  const Chunk ch = a.csf.chunks[ci];
+    return c;
+  };
+  auto next = [&](const Cur& c) {
+    if (c.base + 32 < c.end) return Cur{c.ci, c.beg, c.end, c.base + 32, c.row};
+    return first(c.ci + wstride);
+  };
+  auto coords = [&](const Cur& c, uint32_t (&idx)[M]) {
+    const bool v = c.ci < a.csf.nchunks && c.base + lane < c.end;
+#pragma unroll
+    for (int k = 0; k < M; ++k) idx[k] = v ? __ldg(a.csf.oc[k] + c.base + lane) : 0u;
+  };
+  const uint32_t sbase = cp_smem_u32(stage);
+  auto issue = [&](const Cur& c, int b, const uint32_t (&idx)[M]) {
+    if (c.ci < a.csf.nchunks && c.base + lane < c.end) {
+      const uint32_t st = sbase + (uint32_t)((b * 32 + lane) * ldr) * 8u;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        // rows are ld_k (even) doubles: 16-byte copies, the padding included
+        const int ldk = JALL > 0 ? ((JALL + 1) & ~1) : a.m.ld[k];
+        const double* row = a.m.factor[k] + (size_t)idx[k] * ldk;
+#pragma unroll
+        for (int t = 0; t < (JALL > 0 ? (JALL + 1) / 2 : VEST_MAXJ / 2); ++t)
+          if (JALL > 0 || 2 * t < ldk) cp_async16_s(st + (uint32_t)(a.soff[k] + 2 * t) * 8u, row + 2 * t);
+      }
+      cp_async8_s(st + (uint32_t)a.rslot * 8u, a.r + c.base + lane);
+    }
+    cp_async_commit();
+  };
+  // chunk prologue: q_f = sum_c A_m[s, c] dg_prev[f][c]
+  auto prologue = [&](const Cur& c) {
+    if (lane < kFMax) {
+      double t = 0.0;
+      if (lane < pnf) {
+        const double* arow = a.m.factor[M] + (size_t)c.row * a.m.ld[M];
+        for (int q = 0; q < Jm; ++q) t = fma(__ldg(arow + q), __ldg(a.prev_dg + lane * Jm + q), t);
+      }
+      sq_q[warp][lane] = t;
+    }
+    __syncwarp();
+  };
 
-  // q_f = sum_c A_m[s, c] dg_prev[f][c]
-  const double* arow = a.m.factor[M] + (size_t)ch.row * a.m.ld[M];
-  if (lane < kFMax) {
-    double t = 0.0;
-    if (lane < a.prev.nf)
-      for (int c = 0; c < Jm; ++c) t = fma(__ldg(arow + c), __ldg(a.prev_dg + lane * Jm + c), t);
-    sq_q[warp][lane] = t;
+  Cur cur = first(blockIdx.x * kPassWarps + warp);
+  if (cur.ci >= a.csf.nchunks) return;
+  {
+    uint32_t i0[M];
+    coords(cur, i0);
+    issue(cur, 0, i0);
   }
-  __syncwarp();
+  Cur nxt = next(cur);
+  uint32_t inx[M];
+  coords(nxt, inx);
+  prologue(cur);
 
-  constexpr int NTT = NT * (NT + 1) / 2;
   double d[NTT][2];
 #pragma unroll
   for (int t = 0; t < NTT; ++t) d[t][0] = d[t][1] = 0.0;
   double sq = 0.0;
-  const int nf = a.cur.nf;
-  const bool acc = a.kind != 2 && nf > 0;
-
-  for (uint32_t base = ch.beg; base < ch.end; base += 32) {
-    const uint32_t pos = base + lane;
-    const bool valid = pos < ch.end;
-    double r = 0.0;
-    if (valid) {
-      uint32_t idx[M];
+  int buf = 0;
+  while (true) {
+    // next round's gathers into the other buffer, the round after's coordinates
+    issue(nxt, buf ^ 1, inx);
+    const Cur nn = next(nxt);
+    coords(nn, inx);
+    cp_async_wait<1>();
+    __syncwarp();
+    const double* st = stage + (size_t)(buf * 32 + lane) * ldr;
+    const uint32_t pos = cur.base + lane;
+    const bool valid = pos < cur.end;
+    double r = valid ? st[a.rslot] : 0.0;
+    double ul[JL > 0 ? JL : 1];
+    if constexpr (JL > 0) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) idx[k] = __ldg(a.csf.oc[k] + pos);
-      r = a.r[pos];
+      for (int b = 0; b < JL; ++b) ul[b] = valid ? st[a.soff[M - 1] + b] : 0.0;  // stale stage: no NaN
+    }
+    if (valid && pnf > 0) {
+      double t = 0.0;
+      if constexpr (JL > 0) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        const double* row = a.m.factor[k] + (size_t)idx[k] * a.m.ld[k];
-        const int Jk = a.m.J[k];
+        for (int pi = 0; pi < kFMax / JL; ++pi) {
+          if (pi < a.prev.pre.np) {
+            const double w = prefix_weight<M>(a.prev.pre, pi, st);
+            double s = ul[0] * sq_q[warp][pi * JL];
 #pragma unroll
-        for (int b = 0; b < VEST_MAXJ; b += 2) {
-          if (b < Jk) {
-            const double2 v = __ldg(reinterpret_cast<const double2*>(row + b));
-            st[(offs[k] + b) * 32 + lane] = v.x;
-            if (b + 1 < Jk) st[(offs[k] + b + 1) * 32 + lane] = v.y;
+            for (int b = 1; b < JL; ++b) s = fma(ul[b], sq_q[warp][pi * JL + b], s);
+            t = fma(w, s, t);
           }
         }
-      }
-    }
-    __syncwarp();
-    if (valid && a.prev.nf > 0) {
-      double t = 0.0, w = 1.0;
+      } else {
+        double w = 1.0;
 #pragma unroll
-      for (int f = 0; f < kFMax; ++f) {
-        if (f < a.prev.nf) t = fma(fiber_product<M>(a.prev, f, st, lane, w), sq_q[warp][f], t);
+        for (int f = 0; f < kFMax; ++f) {
+          if (f < pnf) t = fma(fiber_product<M>(a.prev.fib, f, st, w), sq_q[warp][f], t);
+        }
       }
       r -= t;
       if (a.kind != 1) a.r[pos] = r;
     }
     if (a.kind == 2) {
       sq = fma(r, r, sq);
-      __syncwarp();
-      continue;
-    }
-    if (acc) {
-      double w = 1.0;
+    } else if (acc) {
+      if constexpr (JL > 0) {
 #pragma unroll
-      for (int f = 0; f < NC - 1 && f < kFMax; ++f) {
-        if (f < nf) {
-          const double v = fiber_product<M>(a.cur, f, st, lane, w);
-          X[f * kXld + lane] = valid ? v : 0.0;
+        for (int pi = 0; pi < kFMax / JL; ++pi) {
+          if (pi < a.cur.pre.np) {
+            const double w = valid ? prefix_weight<M>(a.cur.pre, pi, st) : 0.0;
+#pragma unroll
+            for (int b = 0; b < JL; ++b) X[(pi * JL + b) * kXld + lane] = w * ul[b];
+          }
+        }
+      } else {
+        double w = 1.0;
+#pragma unroll
+        for (int f = 0; f < NC - 1 && f < kFMax; ++f) {
+          if (f < nf) {
+            const double v = fiber_product<M>(a.cur.fib, f, st, w);
+            X[f * kXld + lane] = valid ? v : 0.0;
+          }
         }
       }
       X[(NC - 1) * kXld + lane] = valid ? r : 0.0;
@@ -206,37 +312,47 @@ __global__ void __launch_bounds__(kPassWarps * 32) k_core_pass(const __grid_cons
       gram_nt<NT>(X, d, lane);
     }
     __syncwarp();
-  }
 
-  if (a.kind == 2) {
-    sq = warp_sum(sq);
-    if (lane == 0) a.chunk_sq[ci] = sq;
-    return;
-  }
-  if (!acc) return;
-  double* out = a.stats + (size_t)ci * a.stride;
-  const int NS = nf * (nf + 1) / 2;
-  const int g = lane >> 2, tq = lane & 3;
-  int t = 0;
+    if (nxt.ci != cur.ci) {  // chunk epilogue
+      const uint32_t ci = cur.ci;
+      if (a.kind == 2) {
+        sq = warp_sum(sq);
+        if (lane == 0) a.chunk_sq[ci] = sq;
+        sq = 0.0;
+      } else if (acc) {
+        double* out = a.stats + (size_t)ci * a.stride;
+        const int NS = nf * (nf + 1) / 2;
+        const int g = lane >> 2, tq = lane & 3;
+        int t = 0;
 #pragma unroll
-  for (int I = 0; I < NT; ++I) {
+        for (int I = 0; I < NT; ++I) {
 #pragma unroll
-    for (int J = I; J < NT; ++J) {
+          for (int J = I; J < NT; ++J) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int row = 8 * I + g, col = 8 * J + 2 * tq + i;
-        const double v = d[t][i];
-        if (a.kind == 0) {
-          if (row <= col && col < nf) out[row * nf - row * (row - 1) / 2 + (col - row)] = v;
-          else if (col == NC - 1 && row < nf) out[NS + row] = v;
-        } else {
-          if (col == NC - 1 && row < nf) out[row] = v;
-          else if (row == col && row < nf) out[nf + row] = v;
+            for (int i = 0; i < 2; ++i) {
+              const int row = 8 * I + g, col = 8 * J + 2 * tq + i;
+              const double v = d[t][i];
+              if (a.kind == 0) {
+                if (row <= col && col < nf) out[row * nf - row * (row - 1) / 2 + (col - row)] = v;
+                else if (col == NC - 1 && row < nf) out[NS + row] = v;
+              } else {
+                if (col == NC - 1 && row < nf) out[row] = v;
+                else if (row == col && row < nf) out[nf + row] = v;
+              }
+              d[t][i] = 0.0;
+            }
+            ++t;
+          }
         }
       }
-      ++t;
+      if (nxt.ci >= a.csf.nchunks) break;
+      prologue(nxt);
     }
+    cur = nxt;
+    nxt = nn;
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 __device__ __forceinline__ int tri(int i, int j, int n) {  // i <= j
@@ -560,6 +676,7 @@ struct Blocks {
   std::vector<int> start, len;  // block ranges into fib
   std::vector<int> nlive;       // general plan: unmasked cells of the block
   std::vector<int> prefix;      // structured plan: the block's prefix p
+  bool pre = false;             // prefix plan (whole prefixes, PreTab)
 };
 
 // General plan: runs of <= F consecutive live fibers (a fiber is live when
@@ -588,13 +705,66 @@ Blocks plan_blocks(const Ctx& c, int F) {
   return b;
 }
 
+// Per-lane stage row of the pass kernel: mode k's factor row (ld_k values,
+// even) at offs[k], then r; stride == 2 mod 4 doubles (16-byte aligned rows,
+// at most 2-way bank conflicts on the 64-bit reads).  16-byte cp.async
+// halves the L1 wavefronts of the random-row gathers against 8-byte copies.
+void stage_layout(const Ctx& c, int* offs, int* rslot, int* ldr) {
+  const int m = c.N - 1;
+  int o = 0;
+  for (int k = 0; k < m; ++k) {
+    offs[k] = o;
+    o += c.ld[k];
+  }
+  if (rslot) *rslot = o;
+  ++o;
+  while (o % 4 != 2) ++o;
+  if (ldr) *ldr = o;
+}
+
+// compile-time last-fiber rank of the prefix-grouped pass kernel (0: per-fiber kernel)
+int pass_jl(const Ctx& c) {
+  if (c.force_generic || c.core_block > 0) return 0;
+  const int M = c.N - 1, JL = c.ranks[c.N - 2];
+  if ((M == 2 && (JL == 5 || JL == 10)) || (M == 3 && (JL == 5 || JL == 8)) || (M == 4 && JL == 5)) return JL;
+  return 0;
+}
+
+// The pass kernel's view of a block's fibers grouped by prefix (see PreTab).
+PreTab make_pretab(const Ctx& c, const Blocks& b, int bi) {
+  PreTab t{};
+  if (bi < 0) return t;
+  const int m = c.N - 1, JL = c.ranks[m - 1];
+  int offs[VEST_MAXN] = {};
+  stage_layout(c, offs, nullptr, nullptr);
+  t.nf = b.len[bi];
+  int64_t last_p = -1;
+  for (int f = 0; f < t.nf; ++f) {
+    const uint32_t fib = b.fib[b.start[bi] + f];
+    const uint32_t pfx = fib / (uint32_t)JL;
+    if ((int64_t)pfx != last_p) {
+      if (t.np == kPreMax) throw RtError{"core block spans too many prefixes"};
+      uint32_t p = pfx;
+      for (int k = m - 2; k >= 0; --k) {
+        t.pre[t.np][k] = offs[k] + (int)(p % (uint32_t)c.ranks[k]);
+        p /= (uint32_t)c.ranks[k];
+      }
+      ++t.np;
+      last_p = pfx;
+    }
+  }
+  return t;
+}
+
+BlockTab block_tab(const Ctx& c, const Blocks& b, int bi);
+
 // The pass kernel's view of a block's fibers (see FibTab).
 FibTab make_tab(const Ctx& c, const Blocks& b, int bi) {
   FibTab t{};
   if (bi < 0) return t;
   const int m = c.N - 1;
   int offs[VEST_MAXN] = {};
-  for (int k = 1; k < m; ++k) offs[k] = offs[k - 1] + c.ranks[k - 1];
+  stage_layout(c, offs, nullptr, nullptr);
   t.nf = b.len[bi];
   int prevb[VEST_MAXN] = {};
   for (int f = 0; f < t.nf; ++f) {
@@ -613,6 +783,13 @@ FibTab make_tab(const Ctx& c, const Blocks& b, int bi) {
     }
     t.newp[f] = same ? 0 : 1;
   }
+  return t;
+}
+
+BlockTab block_tab(const Ctx& c, const Blocks& b, int bi) {
+  BlockTab t{};
+  if (b.pre) t.pre = make_pretab(c, b, bi);
+  else t.fib = make_tab(c, b, bi);
   return t;
 }
 
@@ -637,6 +814,62 @@ Blocks plan_structured(const Ctx& c) {
 // Fibers per block: up to kFMax (the live-cell cap of the solve is applied by
 // plan_blocks); the block GEMM splits its rows over CTA rows, so it imposes no
 // limit.
+int pass_jl(const Ctx& c);
+
+// Prefix plan (pass_jl > 0): runs of <= 31 / JL consecutive prefixes
+// (beta_0..beta_{m-2}) with an unmasked cell, all JL fibers of each, holding
+// <= kSolveCells unmasked cells.
+Blocks plan_prefix_blocks(const Ctx& c) {
+  Blocks b;
+  const int Jm = c.ranks[c.N - 1], JL = c.ranks[c.N - 2];
+  const int P = c.G / (JL * Jm), per = kFMax / JL;
+  std::vector<int> live;
+  std::vector<int> pf;
+  for (int p = 0; p < P; ++p) {
+    int n = 0;
+    for (int q = 0; q < JL * Jm; ++q) n += !c.h_core_mask[(size_t)p * JL * Jm + q];
+    if (n > 0) {
+      pf.push_back(p);
+      live.push_back(n);
+    }
+  }
+  for (int s = 0; s < (int)pf.size();) {
+    int np = 0, cells = 0;
+    while (s + np < (int)pf.size() && np < per && (np == 0 || cells + live[s + np] <= kSolveCells))
+      cells += live[s + np++];
+    b.pre = true;
+    b.start.push_back((int)b.fib.size());
+    b.len.push_back(np * JL);
+    b.nlive.push_back(cells);
+    for (int i = 0; i < np; ++i)
+      for (int f = 0; f < JL; ++f) b.fib.push_back((uint32_t)pf[s + i] * JL + f);
+    s += np;
+  }
+  return b;
+}
+
+// Prefix blocks carry their prefixes' masked fibers as Gram columns; use them
+// while most fibers of the live prefixes are live (dense cores), runs of live
+// fibers otherwise (e.g. config 4's 10 %-dense core: 11 passes instead of 23).
+Blocks plan_general(const Ctx& c, int F) {
+  if (pass_jl(c) > 0) {
+    const int Jm = c.ranks[c.N - 1], JL = c.ranks[c.N - 2];
+    const int P = c.G / (JL * Jm);
+    long live_f = 0, tot_f = 0;
+    for (int p = 0; p < P; ++p) {
+      int lf = 0;
+      for (int f = 0; f < JL; ++f) {
+        bool live = false;
+        for (int q = 0; q < Jm && !live; ++q) live = !c.h_core_mask[((size_t)p * JL + f) * Jm + q];
+        lf += live;
+      }
+      if (lf > 0) live_f += lf, tot_f += JL;
+    }
+    if (tot_f > 0 && 4 * live_f >= 3 * tot_f) return plan_prefix_blocks(c);
+  }
+  return plan_blocks(c, F);
+}
+
 int pick_block(const Ctx& c) { return c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax; }
 
 const void* structured_ops(const Ctx& c) {
@@ -644,20 +877,47 @@ const void* structured_ops(const Ctx& c) {
   return find_core_ops(c.N, c.ranks);
 }
 
-template <int MM, int NT>
-void launch_pass_t(Ctx& c, const CorePassArgs& a, dim3 grid, size_t sm) {
-  check(cudaFuncSetAttribute(k_core_pass<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+template <int MM, int NT, int JL, int JALL>
+void launch_pass_nt(Ctx& c, const CorePassArgs& a) {
+  const size_t sm = (size_t)kPassWarps * (2 * 32 * a.ldr + NT * 8 * kXld) * sizeof(double);
+  check(cudaFuncSetAttribute(k_core_pass<MM, NT, JL, JALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
         "pass smem");
-  k_core_pass<MM, NT><<<grid, kPassWarps * 32, sm, c.stream>>>(a);
+  // persistent: as many CTAs as are resident, each warp strides over the chunks
+  int per_sm = 0, sms = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_core_pass<MM, NT, JL, JALL>, kPassWarps * 32, sm),
+        "pass occupancy");
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  const uint32_t need = (a.csf.nchunks + kPassWarps - 1) / kPassWarps;
+  const dim3 grid(std::max(1u, std::min<uint32_t>(need, (uint32_t)std::max(1, per_sm) * sms)));
+  k_core_pass<MM, NT, JL, JALL><<<grid, kPassWarps * 32, sm, c.stream>>>(a);
+}
+
+template <int MM, int JL, int JALL = 0>
+void launch_pass_j(Ctx& c, const CorePassArgs& a, int NT) {
+  if (NT == 2) launch_pass_nt<MM, 2, JL, JALL>(c, a);
+  else if (NT == 3) launch_pass_nt<MM, 3, JL, JALL>(c, a);
+  else launch_pass_nt<MM, 4, JL, JALL>(c, a);
 }
 
 template <int MM>
 void launch_pass_m(Ctx& c, const CorePassArgs& a, int NT) {
-  const size_t sm = (size_t)kPassWarps * (a.tot * 32 + NT * 8 * kXld) * sizeof(double);
-  const dim3 grid((a.csf.nchunks + kPassWarps - 1) / kPassWarps);
-  if (NT == 2) launch_pass_t<MM, 2>(c, a, grid, sm);
-  else if (NT == 3) launch_pass_t<MM, 3>(c, a, grid, sm);
-  else launch_pass_t<MM, 4>(c, a, grid, sm);
+  const int jl = a.prefix_plan ? pass_jl(c) : 0;
+  // uniform ranks over the staged modes: compile-time row copies
+  bool uni = true;
+  for (int k = 0; k < MM; ++k) uni = uni && c.ranks[k] == c.ranks[0];
+  const int ja = uni ? c.ranks[0] : 0;
+  if constexpr (MM == 2) {
+    if (jl == 5) return ja == 5 ? launch_pass_j<2, 5, 5>(c, a, NT) : launch_pass_j<2, 5>(c, a, NT);
+    if (jl == 10) return ja == 10 ? launch_pass_j<2, 10, 10>(c, a, NT) : launch_pass_j<2, 10>(c, a, NT);
+  } else if constexpr (MM == 3) {
+    if (jl == 5) return ja == 5 ? launch_pass_j<3, 5, 5>(c, a, NT) : launch_pass_j<3, 5>(c, a, NT);
+    if (jl == 8) return ja == 8 ? launch_pass_j<3, 8, 8>(c, a, NT) : launch_pass_j<3, 8>(c, a, NT);
+    if (ja == 8) return launch_pass_j<3, 0, 8>(c, a, NT);
+  } else if constexpr (MM == 4) {
+    if (jl == 5) return ja == 5 ? launch_pass_j<4, 5, 5>(c, a, NT) : launch_pass_j<4, 5>(c, a, NT);
+    if (ja == 5) return launch_pass_j<4, 0, 5>(c, a, NT);
+  }
+  launch_pass_j<MM, 0>(c, a, NT);
 }
 
 void launch_pass(Ctx& c, const CorePassArgs& a) {
@@ -665,7 +925,7 @@ void launch_pass(Ctx& c, const CorePassArgs& a) {
   const int M = c.N - 1;
   if (a.csf.nchunks == 0) return;
   // column tiles: the block's fibers + the residual column
-  const int nf = a.kind == 2 ? 0 : a.cur.nf;
+  const int nf = a.kind == 2 ? 0 : a.cur.fib.nf;
   const int NT = nf <= 15 ? 2 : (nf <= 23 ? 3 : 4);
   switch (M) {
     case 1: launch_pass_m<1>(c, a, NT); break;
@@ -703,9 +963,10 @@ void run_pass(Ctx& c, const void* sops, const Blocks& b, int prev, int cur, int 
   a.chunk_sq = c.d_chunk_sum;
   a.prev_dg = c.d_dg;
   a.kind = kind;
-  a.cur = make_tab(c, b, cur);
-  a.prev = make_tab(c, b, prev);
-  for (int k = 0; k < m; ++k) a.tot += c.ranks[k];
+  a.prefix_plan = b.pre ? 1 : 0;
+  a.cur = block_tab(c, b, cur);
+  a.prev = block_tab(c, b, prev);
+  stage_layout(c, a.soff, &a.rslot, &a.ldr);
   launch_pass(c, a);
 }
 
@@ -787,7 +1048,7 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   if (!c.r_fresh) compute_residual(c);
   const void* sops = structured_ops(c);
   const int F = sops ? c.ranks[c.N - 2] : pick_block(c);
-  const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
+  const Blocks b = sops ? plan_structured(c) : plan_general(c, F);
   if (b.fib.empty()) return;  // fully pruned core: nothing to update
   upload_fibers(c, b);
   if (sops && !legacy_block_passes()) {
@@ -832,7 +1093,7 @@ void core_responsibilities(Ctx& c) {
   if (c.re == 0.0) return;  // perfect fit: everything +inf (pruning.hpp:102-103)
   const void* sops = structured_ops(c);
   const int F = sops ? c.ranks[c.N - 2] : pick_block(c);
-  const Blocks b = sops ? plan_structured(c) : plan_blocks(c, F);
+  const Blocks b = sops ? plan_structured(c) : plan_general(c, F);
   if (b.fib.empty()) return;
   upload_fibers(c, b);
   if (sops) pack_operands(c, sops);

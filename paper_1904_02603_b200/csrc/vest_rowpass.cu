@@ -74,10 +74,16 @@ __device__ __forceinline__ void load_row(const double* __restrict__ row, double 
 #ifndef VEST_ROW_MINB_HI
 #define VEST_ROW_MINB_HI 2
 #endif
+// ... and unroll the rolled outer-mode loop once (K0U = 1): the 2-way unroll
+// of the 3-mode shapes spills at N >= 4.
+#ifndef VEST_K0_UNROLL_HI
+#define VEST_K0_UNROLL_HI 2
+#endif
 template <class S>
 struct RowTune {
   static constexpr int NE = S::N <= 3 ? VEST_ROW_NE : VEST_ROW_NE_HI;
   static constexpr int MINB = S::N <= 3 ? VEST_ROW_MINB : VEST_ROW_MINB_HI;
+  static constexpr int K0U = S::N <= 3 ? kK0Unroll : VEST_K0_UNROLL_HI;
 };
 
 template <class S, int MODE>
@@ -121,7 +127,7 @@ struct StaticPolicy {
 #if VEST_CORE_SMEM
     delta_staticN<S, MODE, NE>(SmemCore{score}, u, rows0, d);
 #else
-    delta_staticN<S, MODE, NE>(ConstCore{}, u, rows0, d);
+    delta_staticN<S, MODE, NE, ConstCore, RowTune<S>::K0U>(ConstCore{}, u, rows0, d);
 #endif
   }
   const double* score = nullptr;
