@@ -69,6 +69,16 @@ int vest_ctx_specialised(const vest_ctx* ctx);
 int vest_ctx_force_generic(vest_ctx* ctx, int on);
 /* Tuning: fibers per core-sweep block (0 = default). */
 int vest_ctx_set_core_block(vest_ctx* ctx, int fibers);
+/* Mask-specialised delta contraction for pruned cores (NVRTC-compiled for the
+ * current core mask, recompiled after prunes; replaces the dense contraction
+ * of the factor-row update, updates.hpp:35-52 skipping zero cells):
+ * -1 auto (unmasked cells < |G| / 4 on rank-specialised shapes), 0 off, 1 on.
+ * vest_ctx_sparse_delta_active reports whether the next update uses it. */
+int vest_ctx_set_sparse_delta(vest_ctx* ctx, int mode);
+int vest_ctx_sparse_delta_active(const vest_ctx* ctx);
+/* Host-only: generate and NVRTC-compile that contraction for ranks and a core
+ * mask (no GPU needed); *cubin_bytes = size of the sm_100a cubin. */
+int vest_sparse_compile_check(int order, const uint64_t* ranks, const uint8_t* core_mask, uint64_t* cubin_bytes);
 
 /* ---------------------------------------------------------------- sharding --
  * Multi-GPU (one process per GPU): a shard context owns the rows

@@ -352,6 +352,41 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
   const bool fuse = fuse_resid && mode == c.N - 1 && c.ops && !c.force_generic;
   a.fuse_resid = fuse ? 1 : 0;
   a.r_out = c.d_r;
+  const ModeData& mdd = c.modes[mode];
+  const uint64_t p0 = mdd.h_offsets[c.row_lo[mode]], p1 = mdd.h_offsets[c.row_hi[mode]];
+  if (sparse_delta_enabled(c)) {
+    // mask-specialised contraction (vest_sparse.cu), then the statistics,
+    // solves and fused residual from the materialised delta
+    const bool fuse_d = fuse_resid && mode == c.N - 1;
+    a.fuse_resid = fuse_d ? 1 : 0;
+    ensure(c, &c.d_delta, &c.delta_cap, (size_t)J * (p1 - p0) + 1);
+    {
+      ProfScope ps(c, fuse_d ? kProfFactorFused : kProfFactor);
+      sparse_delta(c, mode, p0, p1 - p0, c.d_delta);
+      check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream), "factor update (delta)");
+      if (reg == 1) l1_empty_rows(c, mode, lambda);
+    }
+    c.r_valid = false;
+    c.r_pending[0] = c.r_pending[1] = -1;
+    c.r_fresh = false;
+    c.table_valid = false;
+    if (fuse_d) {
+      if (mdd.nheavy_chunks > 0) {
+        RowPassArgs b = row_args(c, mode);
+        b.csf.chunks = mdd.d_heavy_chunks;
+        b.csf.nchunks = mdd.nheavy_chunks;
+        b.csf.nheavy = 0;
+        b.r_out = c.d_r;
+        ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, mdd.nchunks + 1);
+        b.chunk_out = c.d_chunk_sum;
+        ProfScope ps(c, kProfResid);
+        check(launch_rowpass_delta(b, kResid, b.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream), "heavy-row residual");
+      }
+      c.r_fresh = true;
+    }
+    comm_allgather_rows(c, mode, c.d_factor[mode], (uint64_t)c.ld[mode]);
+    return;
+  }
   {
     ProfScope ps(c, fuse ? kProfFactorFused : kProfFactor);
     check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
@@ -817,6 +852,8 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_small);
   cudaFree(c.d_fibers);
   cudaFree(c.d_dg);
+  cudaFree(c.d_delta);
+  sparse_free(c);
   cudaFree(c.d_pack_u);
   cudaFree(c.d_pack_w);
   cudaFree(c.d_counter);
@@ -842,6 +879,20 @@ int vest_ctx_force_generic(vest_ctx* h, int on) {
 int vest_ctx_set_core_block(vest_ctx* h, int fibers) {
   h->c.core_block = fibers;
   return VEST_OK;
+}
+int vest_ctx_set_sparse_delta(vest_ctx* h, int mode) {
+  h->c.sparse_delta = mode < 0 ? -1 : (mode ? 1 : 0);
+  return VEST_OK;
+}
+int vest_ctx_sparse_delta_active(const vest_ctx* h) { return h && sparse_delta_enabled(h->c) ? 1 : 0; }
+int vest_sparse_compile_check(int order, const uint64_t* ranks, const uint8_t* core_mask, uint64_t* cubin_bytes) {
+  return guard([&] {
+    if (order < 2 || order > VEST_MAXN) throw ArgError{"order must be in [2, 8]"};
+    int r[VEST_MAXN];
+    for (int k = 0; k < order; ++k) r[k] = (int)ranks[k];
+    std::string err;
+    if (sparse_compile_check(order, r, core_mask, cubin_bytes, &err)) throw RtError{err};
+  });
 }
 
 int vest_init_random(vest_ctx* h, uint64_t seed) {

@@ -92,6 +92,7 @@ struct ModeData {
 };
 
 struct Ctx;
+struct SparseState;  // vest_sparse.cu: NVRTC module of the mask-specialised delta contraction
 
 // Kernel families instantiated for compile-time rank tuples.
 struct ShapeOps {
@@ -173,6 +174,9 @@ struct Ctx {
   unsigned long long* d_counts = nullptr;  // prune / sparsity counters
   void* d_sel = nullptr;           // radix-select state
 
+  SparseState* sparse = nullptr;
+  int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
+  double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
   bool force_generic = false;
   int core_block = 0;  // fibers per block (0 = auto)
   const ShapeOps* ops = nullptr;
@@ -207,6 +211,12 @@ cudaError_t launch_rowpass_generic(const RowPassArgs& a, int kind, uint32_t nchu
 cudaError_t launch_coo_recon_generic(const DevModel& m, const uint32_t* coords, const double* values,
                                      uint64_t n, double* out, double* partial, int nblocks, cudaStream_t s);
 void sync_const_core(Ctx& c);  // copy d_core into every TU's constant-bank core
+cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
+                                 uint64_t dstride, uint64_t p0, cudaStream_t s);
+bool sparse_delta_enabled(const Ctx& c);
+void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out);
+void sparse_free(Ctx& c);
+int sparse_compile_check(int N, const int* ranks, const uint8_t* core_mask, uint64_t* bytes, std::string* err);
 
 void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values);
 void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resid);

@@ -611,6 +611,128 @@ __global__ void __launch_bounds__(256) k_heavy(RowPassArgs a, int kind) {
             a.m.fmask[mode] + (size_t)h.row * J, lane);
 }
 
+// --------------------------------------------- statistics from a given delta --
+// The row pass when delta was produced elsewhere (the mask-specialised
+// contraction of vest_sparse.cu): delta[j][pos - p0] SoA.  One warp per
+// chunk; kStats stages (delta, x) transposed and accumulates the Gram on DMMA
+// exactly as k_rowpass, solves light rows in-kernel (heavy rows: partials for
+// k_heavy) and, for the last mode, writes the fused residual
+// r = x - delta . a_row of the solved row (tucker_model.hpp:168-183: B(alpha)
+// = delta_n(alpha) . a_n[i_n]); kResid does the same for rows k_heavy solved.
+template <int JN, int KIND>
+__global__ void __launch_bounds__(kRowWarps * 32, 2) k_rowpass_delta(RowPassArgs a, const double* __restrict__ delta,
+                                                                     uint64_t dstride, uint64_t p0) {
+  static_assert(JN + 1 <= 16, "DMMA tile: J <= 15");
+  __shared__ double smem_d[kRowWarps][16 * kXld];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ci = blockIdx.x * kRowWarps + warp;
+  if (ci >= a.csf.nchunks) return;
+  const Chunk ch = a.csf.chunks[ci];
+  const int mode = a.mode;
+  double* wsm = smem_d[warp];
+  double* arow_p = a.m.factor[mode] + (size_t)ch.row * a.m.ld[mode];
+  if constexpr (KIND == kResid) {
+    double arow[JN];
+#pragma unroll
+    for (int j = 0; j < JN; ++j) arow[j] = __ldg(arow_p + j);
+    double sq = 0.0;
+    for (uint32_t pos = ch.beg + lane; pos < ch.end; pos += 32) {
+      double rec = 0.0;
+#pragma unroll
+      for (int j = 0; j < JN; ++j) rec = fma(__ldg(delta + j * dstride + (pos - p0)), arow[j], rec);
+      const double r = __ldg(a.csf.val + pos) - rec;
+      a.r_out[pos] = r;
+      sq = fma(r, r, sq);
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) a.chunk_out[ci] = sq;
+    return;
+  } else {
+    for (int t = lane; t < 16 * kXld; t += 32) wsm[t] = 0.0;
+    __syncwarp();
+    double tc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (uint32_t base = ch.beg; base < ch.end; base += 32) {
+      const uint32_t pos = base + lane;
+      const bool valid = pos < ch.end;
+#pragma unroll
+      for (int j = 0; j < JN; ++j) wsm[j * kXld + lane] = valid ? __ldg(delta + j * dstride + (pos - p0)) : 0.0;
+      wsm[JN * kXld + lane] = valid ? __ldg(a.csf.val + pos) : 0.0;
+      __syncwarp();
+      gram_dmma<JN + 1, 1>(wsm, tc, lane);
+      __syncwarp();
+    }
+    constexpr int J = JN;
+    constexpr int NG = J * (J + 1) / 2;
+    double* Gs = wsm;          // J x J
+    double* xd = wsm + J * J;  // J
+#pragma unroll
+    for (int t = 0; t < (JN + 1 > 8 ? 3 : 1); ++t) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        int row, col;
+        gram_coord(t, i, lane, row, col);
+        const double v = tc[t][i];
+        int slot = -1;
+        if (row <= col && col < J) slot = row * J - row * (row - 1) / 2 + (col - row);
+        else if (col == J && row < J) slot = NG + row;
+        if (slot < 0) continue;
+        if (ch.slot != kLight) {
+          a.heavy_out[(size_t)ch.slot * a.stride_na + slot] = v;
+        } else if (col == J) {
+          xd[row] = v;
+        } else {
+          Gs[row * J + col] = v;
+          Gs[col * J + row] = v;
+        }
+      }
+    }
+    if (ch.slot != kLight) return;
+    __syncwarp();
+    solve_row(J, a.reg, a.lambda, Gs, xd, arow_p, a.m.fmask[mode] + (size_t)ch.row * J, lane);
+    if (!a.fuse_resid) return;
+    __syncwarp();  // the solved row (global) is visible to the warp
+    double arow[JN];
+#pragma unroll
+    for (int j = 0; j < JN; ++j) arow[j] = arow_p[j];
+    for (uint32_t pos = ch.beg + lane; pos < ch.end; pos += 32) {
+      double rec = 0.0;
+#pragma unroll
+      for (int j = 0; j < JN; ++j) rec = fma(__ldg(delta + j * dstride + (pos - p0)), arow[j], rec);
+      a.r_out[pos] = __ldg(a.csf.val + pos) - rec;
+    }
+  }
+}
+
+template <int JN>
+cudaError_t launch_delta_j(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta, uint64_t dstride,
+                           uint64_t p0, cudaStream_t s) {
+  const dim3 grid((nchunks + kRowWarps - 1) / kRowWarps);
+  if (nchunks > 0) {
+    if (kind == kStats) k_rowpass_delta<JN, kStats><<<grid, kRowWarps * 32, 0, s>>>(a, delta, dstride, p0);
+    else k_rowpass_delta<JN, kResid><<<grid, kRowWarps * 32, 0, s>>>(a, delta, dstride, p0);
+    count_launch();
+  }
+  if (kind == kStats && a.csf.nheavy > 0) {
+    k_heavy<<<(a.csf.nheavy + 7) / 8, 256, 0, s>>>(a, kStats);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
+                                 uint64_t dstride, uint64_t p0, cudaStream_t s) {
+  switch (a.m.J[a.mode]) {
+#define VEST_DJ(JJ) \
+  case JJ:          \
+    return launch_delta_j<JJ>(a, kind, nchunks, delta, dstride, p0, s);
+    VEST_DJ(1) VEST_DJ(2) VEST_DJ(3) VEST_DJ(4) VEST_DJ(5) VEST_DJ(6) VEST_DJ(7) VEST_DJ(8)
+    VEST_DJ(9) VEST_DJ(10) VEST_DJ(11) VEST_DJ(12) VEST_DJ(13) VEST_DJ(14) VEST_DJ(15)
+#undef VEST_DJ
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 // ------------------------------------------------------- COO reconstruction --
 // predict / evaluate_test (trainer.hpp:172-190) on entry-major coordinates.
 template <class S>

@@ -283,6 +283,13 @@ class Device:
     def force_generic(self, on: bool = True):
         check(self._L.vest_ctx_force_generic(self.h, 1 if on else 0))
 
+    def set_sparse_delta(self, mode: int):
+        """Mask-specialised delta contraction: -1 auto, 0 off, 1 on."""
+        check(self._L.vest_ctx_set_sparse_delta(self.h, int(mode)))
+
+    def sparse_delta_active(self) -> bool:
+        return bool(self._L.vest_ctx_sparse_delta_active(self.h))
+
     def set_core_block(self, fibers: int):
         check(self._L.vest_ctx_set_core_block(self.h, fibers))
 

@@ -37,6 +37,20 @@ def test_version_and_counter(L):
     assert L.vest_launch_count() == 0  # nothing launched without a device
 
 
+@pytest.mark.parametrize("ranks,keep", [([8, 8, 8, 8], 0.1), ([5, 5, 5], 1.0), ([3, 4], 0.5), ([2, 2, 3, 2, 2], 0.3)])
+def test_sparse_delta_source_compiles_for_sm100a(L, ranks, keep):
+    """The mask-specialised delta contraction (vest_sparse.cu) is generated and
+    NVRTC-compiled for sm_100a on the host -- no GPU involved."""
+    g = int(np.prod(ranks))
+    mask = (np.random.default_rng(44).random(g) >= keep).astype(np.uint8)
+    r = np.asarray(ranks, np.uint64)
+    out = np.zeros(1, np.uint64)
+    rc = L.vest_sparse_compile_check(len(ranks), _lib.ptr(r, _lib.u64p), _lib.ptr(mask, _lib.u8p),
+                                     _lib.ptr(out, _lib.u64p))
+    assert rc == 0, L.vest_last_error()
+    assert out[0] > 1000  # a cubin
+
+
 def test_init_random_host_matches_reference(L):
     g = golden("init_random")
     for k in range(int(g["ncases"])):

@@ -50,12 +50,15 @@ def model_of(s, dims, ranks):
     return st.TuckerModel(list(dims), list(ranks), core, cm, fs, ms)
 
 
-def phases(dims, ranks, nnz, seed, reg, lam, iters=2, pr=0.3, generic=False, **kw):
+def phases(dims, ranks, nnz, seed, reg, lam, iters=2, pr=0.3, generic=False, sparse=None, **kw):
     coords, values, m = random_instance(dims, ranks, nnz, seed, **kw)
     x = st.make_tensor(dims, coords, values)
     dev = st.Device(x, ranks)
     if generic:
         dev.force_generic(True)
+    if sparse is not None:
+        dev.set_sparse_delta(sparse)
+        assert dev.sparse_delta_active() == bool(sparse)
     s = oracle_session(dims, ranks, coords, values, m)
     N = len(dims)
     for t in range(iters):
@@ -106,6 +109,34 @@ def test_config23_ranks(ranks):
 
 def test_config4_ranks_sparse_core():
     phases([20, 18, 16, 14], [8, 8, 8, 8], 5000, 14, 0, 0.01, iters=1, mask_frac=0.9)
+    phases([20, 18, 16, 14], [8, 8, 8, 8], 5000, 14, 0, 0.01, iters=1, mask_frac=0.9, sparse=0)
+
+
+def test_sparse_delta_auto_selection():
+    coords, values, m = random_instance([20, 18, 16, 14], [8, 8, 8, 8], 3000, 3, mask_frac=0.9)
+    dev = st.Device(st.make_tensor([20, 18, 16, 14], coords, values), [8, 8, 8, 8])
+    dev.set_model(m)
+    assert dev.sparse_delta_active()  # 10 %-dense core: mask-specialised contraction
+    coords, values, m = random_instance([20, 18, 16], [8, 8, 8], 3000, 3)
+    dev = st.Device(st.make_tensor([20, 18, 16], coords, values), [8, 8, 8])
+    dev.set_model(m)
+    assert not dev.sparse_delta_active()  # dense core: factorised kernels
+
+
+# the mask-specialised (NVRTC) contraction forced on: every order, L1/LF,
+# masks, heavy split rows; recompiled when a prune changes the mask
+@pytest.mark.parametrize("dims,ranks,mf", [([20, 18, 16, 14], [8, 8, 8, 8], 0.9), ([60, 50, 40], [5, 5, 5], 0.3),
+                                           ([30, 25], [4, 3], 0.2), ([7, 6, 5, 4, 3], [2, 2, 3, 2, 2], 0.2),
+                                           ([9, 8, 8, 7, 7], [5, 5, 5, 5, 5], 0.5)])
+@pytest.mark.parametrize("reg,lam", [(0, 0.01), (1, 0.1)])
+def test_sparse_delta_forced(dims, ranks, mf, reg, lam):
+    nnz = min(int(np.prod(dims)) // 3, 4000)
+    phases(dims, ranks, nnz, 31, reg, lam, iters=2, mask_frac=mf, sparse=1)
+
+
+def test_sparse_delta_heavy_rows():
+    phases([3, 60, 60], [5, 5, 5], 9000, 18, 0, 0.01, iters=1, sparse=1)
+    phases([12, 40, 30], [5, 5, 5], 8000, 20, 1, 0.05, iters=1, skew=1.6, sparse=1)
 
 
 def test_config5_ranks():
