@@ -76,6 +76,10 @@ int vest_ctx_set_core_block(vest_ctx* ctx, int fibers);
  * vest_ctx_sparse_delta_active reports whether the next update uses it. */
 int vest_ctx_set_sparse_delta(vest_ctx* ctx, int mode);
 int vest_ctx_sparse_delta_active(const vest_ctx* ctx);
+/* Plan-specialised core-sweep passes for the general block plans (straight-line
+ * passes generated per core mask, NVRTC-compiled): -1 auto (rank-specialised
+ * shapes), 0 off (table-driven kernel), 1 on. */
+int vest_ctx_set_core_gen(vest_ctx* ctx, int mode);
 /* Host-only: generate and NVRTC-compile that contraction for ranks and a core
  * mask (no GPU needed); *cubin_bytes = size of the sm_100a cubin. */
 int vest_sparse_compile_check(int order, const uint64_t* ranks, const uint8_t* core_mask, uint64_t* cubin_bytes);

@@ -35,6 +35,7 @@ SIGNATURES = {
     "vest_ctx_set_core_block": (C.c_int, [vp, C.c_int]),
     "vest_ctx_set_sparse_delta": (C.c_int, [vp, C.c_int]),
     "vest_ctx_sparse_delta_active": (C.c_int, [vp]),
+    "vest_ctx_set_core_gen": (C.c_int, [vp, C.c_int]),
     "vest_sparse_compile_check": (C.c_int, [C.c_int, u64p, u8p, u64p]),
     "vest_init_random": (C.c_int, [vp, C.c_uint64]),
     "vest_init_random_host": (C.c_int, [C.c_int, u64p, u64p, C.c_uint64, f64p, C.POINTER(f64p)]),

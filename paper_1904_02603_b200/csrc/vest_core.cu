@@ -870,6 +870,33 @@ Blocks plan_general(const Ctx& c, int F) {
   return plan_blocks(c, F);
 }
 
+bool use_core_gen(const Ctx& c) {
+  if (c.core_gen_mode >= 0) return c.core_gen_mode == 1;
+  return c.ops && !c.force_generic && c.core_block == 0;
+}
+
+std::vector<std::vector<uint32_t>> block_lists(const Blocks& b) {
+  std::vector<std::vector<uint32_t>> out(b.start.size());
+  for (size_t i = 0; i < b.start.size(); ++i)
+    out[i].assign(b.fib.begin() + b.start[i], b.fib.begin() + b.start[i] + b.len[i]);
+  return out;
+}
+
+uint64_t plan_key(const Ctx& c, const Blocks& b, int F) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    h ^= v;
+    h *= 1099511628211ull;
+  };
+  mix((uint64_t)c.N);
+  for (int k = 0; k < c.N; ++k) mix((uint64_t)c.ranks[k] << 8 | (uint64_t)c.ld[k]);
+  mix((uint64_t)F);
+  mix(b.pre ? 1 : 0);
+  for (size_t i = 0; i < b.start.size(); ++i) mix((uint64_t)b.start[i] << 20 | (uint64_t)b.len[i]);
+  for (uint32_t f : b.fib) mix(f);
+  return h;
+}
+
 int pick_block(const Ctx& c) { return c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax; }
 
 const void* structured_ops(const Ctx& c) {
@@ -1040,6 +1067,9 @@ void pack_operands(Ctx& c, const void* sops) {
 
 }  // namespace
 
+// the general plan's blocks (host-only compile check of the generated passes)
+std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c) { return block_lists(plan_general(c, pick_block(c))); }
+
 void core_sweep(Ctx& c, int reg, double lambda) {
   const int m = c.N - 1, Jm = c.ranks[m];
   // r = x - B(alpha) for the model after the factor updates
@@ -1063,9 +1093,17 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
   ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);
   const int nb = (int)b.start.size();
+  // plan-specialised passes (vest_core_gen.cu) for the general plans
+  const bool gen = !sops && use_core_gen(c);
+  if (gen) core_gen_prepare(c, block_lists(b), plan_key(c, b, F));
   for (int bi = 0; bi <= nb; ++bi) {
     const bool last = bi == nb;
-    run_pass(c, sops, b, bi - 1, last ? -1 : bi, last ? 2 : 0, stride);
+    if (gen) {
+      ProfScope ps(c, kProfCorePass);
+      core_gen_pass(c, bi, c.d_dg, c.d_chunk_stats, stride, c.d_chunk_sum);
+    } else {
+      run_pass(c, sops, b, bi - 1, last ? -1 : bi, last ? 2 : 0, stride);
+    }
     if (last) break;
     const int nf = b.len[bi];
     const int nout = block_gemm(c, nf, 0, stride);

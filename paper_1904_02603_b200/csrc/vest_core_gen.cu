@@ -1,0 +1,390 @@
+// SPDX-License-Identifier: Apache-2.0
+// vest_core_gen.cu -- the generic core-sweep passes (vest_core.cu
+// k_core_pass) generated per block plan and NVRTC-compiled for sm_100a.
+//
+// A block is a runtime list of live fibers (beta_0..beta_{m-1}); the
+// table-driven pass kernel spends most of its instructions on the tables
+// (per-fiber guards, constant loads, address arithmetic: ~1570 instructions
+// per 32-entry round at config 4).  The plan depends on the core mask only,
+// so every pass (previous block's residual update + current block's
+// statistics, and the final sum of squares) is emitted as straight-line code:
+// the lane's staged factor rows are loaded into registers once per round and
+// each fiber product is 1-2 DMUL with compile-time register operands, each
+// Gram column store a compile-time shared-memory offset.  Everything else --
+// persistent warps over the last mode's chunks, cp.async staging one round
+// ahead, the DMMA Gram, the per-chunk statistics layout -- is the table-driven
+// kernel's, so its block GEMM and solve consume the output unchanged.  One
+// NVRTC program holds all passes of a plan; it is rebuilt only when a prune
+// changes the mask.
+#include <algorithm>
+#include <functional>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "vest_internal.h"
+
+namespace vest {
+
+
+struct CoreGenArgs {
+  const uint32_t* oc[VEST_MAXN];
+  const double* f[VEST_MAXN];
+  double* r;
+  const double* prev_dg;
+  double* stats;
+  double* chunk_sq;
+  const Chunk* chunks;
+  uint32_t nchunks;
+  int stride;
+};
+
+struct CoreGenState {
+  uint64_t key = 0;
+  cudaLibrary_t lib = nullptr;
+  std::vector<cudaKernel_t> k;  // pass i: prev = i - 1, cur = i (i < nb); pass nb: final
+  std::vector<int> nt;
+  int ldr = 0;
+};
+
+namespace {
+
+// device prelude shared by every generated pass
+const char* kPrelude = R"CUDA(
+struct Chunk { unsigned row, beg, end, slot; };
+struct CoreGenArgs {
+  const unsigned* oc[8]; const double* f[8]; double* r; const double* prev_dg; double* stats;
+  double* chunk_sq; const Chunk* chunks; unsigned nchunks; int stride;
+};
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp16(unsigned s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp8(unsigned s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int NT>
+__device__ __forceinline__ void gram_nt(const double* X, double (&d)[NT * (NT + 1) / 2][2], int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int e = 4 * kk + tq;
+    double f[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) f[i] = X[(8 * i + g) * 36 + e];
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NT; ++I)
+#pragma unroll
+      for (int J = I; J < NT; ++J) { dmma884(d[t][0], d[t][1], f[I], f[J]); ++t; }
+  }
+}
+)CUDA";
+
+// one pass: KIND 0 (prev update + cur statistics) or 2 (prev update + r^2)
+const char* kPass = R"CUDA(
+extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
+  constexpr int M = @M@, LDR = @LDR@, NT = @NT@, NC = NT * 8, NTT = NT * (NT + 1) / 2;
+  constexpr int NF = @NF@, PNF = @PNF@, KIND = @KIND@, JM = @JM@, RSLOT = @RSLOT@;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double sq_q[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* const stage = smem + (unsigned long long)warp * (2 * 32 * LDR + NC * 36);
+  double* const X = stage + 2 * 32 * LDR;
+  for (int t = lane; t < NC * 36; t += 32) X[t] = 0.0;
+  const unsigned wstride = gridDim.x * 4;
+  struct Cur { unsigned ci, end, base, row; };
+  auto first = [&](unsigned ci) {
+    Cur c{ci, 0, 0, 0};
+    if (ci < a.nchunks) { const Chunk ch = a.chunks[ci]; c.end = ch.end; c.base = ch.beg; c.row = ch.row; }
+    return c;
+  };
+  auto next = [&](const Cur& c) {
+    if (c.base + 32 < c.end) return Cur{c.ci, c.end, c.base + 32, c.row};
+    return first(c.ci + wstride);
+  };
+  auto coords = [&](const Cur& c, unsigned (&idx)[M]) {
+    const bool v = c.ci < a.nchunks && c.base + lane < c.end;
+#pragma unroll
+    for (int k = 0; k < M; ++k) idx[k] = v ? __ldg(a.oc[k] + c.base + lane) : 0u;
+  };
+  const unsigned sbase = su32(stage);
+  auto issue = [&](const Cur& c, int b, const unsigned (&idx)[M]) {
+    if (c.ci < a.nchunks && c.base + lane < c.end) {
+      const unsigned st = sbase + (unsigned)((b * 32 + lane) * LDR) * 8u;
+@ISSUE@
+      cp8(st + RSLOT * 8u, a.r + c.base + lane);
+    } else {
+      double* sp = stage + (b * 32 + lane) * LDR;  // finite zeros: products of idle lanes vanish
+#pragma unroll
+      for (int t = 0; t < LDR; ++t) sp[t] = 0.0;
+    }
+    cp_commit();
+  };
+  auto prologue = [&](const Cur& c) {
+    if (PNF > 0) {
+      double t = 0.0;
+      if (lane < PNF) {
+        const double* arow = a.f[M] + (unsigned long long)c.row * @LDM@;
+#pragma unroll
+        for (int q = 0; q < JM; ++q) t = fma(__ldg(arow + q), __ldg(a.prev_dg + lane * JM + q), t);
+      }
+      sq_q[warp][lane] = t;
+      __syncwarp();
+    }
+  };
+  Cur cur = first(blockIdx.x * 4 + warp);
+  if (cur.ci >= a.nchunks) return;
+  { unsigned i0[M]; coords(cur, i0); issue(cur, 0, i0); }
+  Cur nxt = next(cur);
+  unsigned inx[M];
+  coords(nxt, inx);
+  prologue(cur);
+  double d[NTT][2];
+#pragma unroll
+  for (int t = 0; t < NTT; ++t) d[t][0] = d[t][1] = 0.0;
+  double sq = 0.0;
+  int buf = 0;
+  while (true) {
+    issue(nxt, buf ^ 1, inx);
+    const Cur nn = next(nxt);
+    coords(nn, inx);
+    cp_wait1();
+    __syncwarp();
+    const double* st = stage + (buf * 32 + lane) * LDR;
+    const unsigned pos = cur.base + lane;
+    const bool valid = pos < cur.end;
+    double r = st[RSLOT];
+@LOADU@
+    if (PNF > 0 && valid) {
+      double t = 0.0;
+@PREV@
+      r -= t;
+      a.r[pos] = r;
+    }
+    if (KIND == 2) {
+      sq = fma(r, r, sq);
+    } else {
+@CUR@
+      X[(NC - 1) * 36 + lane] = r;
+      __syncwarp();
+      gram_nt<NT>(X, d, lane);
+    }
+    __syncwarp();
+    if (nxt.ci != cur.ci) {
+      const unsigned ci = cur.ci;
+      if (KIND == 2) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) a.chunk_sq[ci] = sq;
+        sq = 0.0;
+      } else {
+        double* out = a.stats + (unsigned long long)ci * a.stride;
+        constexpr int NS = NF * (NF + 1) / 2;
+        const int g = lane >> 2, tq = lane & 3;
+        int t = 0;
+#pragma unroll
+        for (int I = 0; I < NT; ++I) {
+#pragma unroll
+          for (int J = I; J < NT; ++J) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int row = 8 * I + g, col = 8 * J + 2 * tq + i;
+              if (row <= col && col < NF) out[row * NF - row * (row - 1) / 2 + (col - row)] = d[t][i];
+              else if (col == NC - 1 && row < NF) out[NS + row] = d[t][i];
+              d[t][i] = 0.0;
+            }
+            ++t;
+          }
+        }
+      }
+      if (nxt.ci >= a.nchunks) break;
+      prologue(nxt);
+    }
+    cur = nxt;
+    nxt = nn;
+    buf ^= 1;
+  }
+  cp_wait0();
+}
+)CUDA";
+
+void replace_all(std::string& s, const std::string& from, const std::string& to) {
+  for (size_t p = 0; (p = s.find(from, p)) != std::string::npos; p += to.size()) s.replace(p, from.size(), to);
+}
+
+std::string uname(int k, int b) { return "u" + std::to_string(k) + "_" + std::to_string(b); }
+
+// fiber p (row-major over modes 0..m-1) -> betas
+void fiber_beta(const Ctx& c, uint32_t p, int* beta) {
+  const int m = c.N - 1;
+  for (int k = m - 1; k >= 0; --k) {
+    beta[k] = (int)(p % (uint32_t)c.ranks[k]);
+    p /= (uint32_t)c.ranks[k];
+  }
+}
+
+// straight-line products of a block's fibers; emit(f, expr) consumes each
+void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream& o,
+              const std::function<std::string(int, const std::string&)>& emit, std::vector<bool>& used) {
+  const int M = c.N - 1;
+  int prev[VEST_MAXN];
+  bool open = false;
+  for (size_t f = 0; f < fib.size(); ++f) {
+    int beta[VEST_MAXN];
+    fiber_beta(c, fib[f], beta);
+    bool same = open;
+    for (int k = 0; k + 1 < M && same; ++k) same = beta[k] == prev[k];
+    if (!same) {
+      if (open) o << "      }\n";
+      o << "      { const double w = ";
+      if (M == 1) {
+        o << "1.0";
+      } else {
+        for (int k = 0; k + 1 < M; ++k) {
+          o << (k ? " * " : "") << uname(k, beta[k]);
+          used[k * 16 + beta[k]] = true;
+        }
+      }
+      o << ";\n";
+      open = true;
+    }
+    for (int k = 0; k < M; ++k) prev[k] = beta[k];
+    used[(M - 1) * 16 + beta[M - 1]] = true;
+    o << "        " << emit((int)f, "w * " + uname(M - 1, beta[M - 1])) << "\n";
+  }
+  if (open) o << "      }\n";
+}
+
+}  // namespace
+
+void core_gen_free(Ctx& c) {
+  if (!c.core_gen) return;
+  if (c.core_gen->lib) cudaLibraryUnload(c.core_gen->lib);
+  delete c.core_gen;
+  c.core_gen = nullptr;
+}
+
+// CUDA source of every pass of a plan (blocks as fiber lists); NT per pass
+std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, std::vector<int>& nts,
+                            int& ldr_out) {
+  const int M = c.N - 1;
+  int soff[VEST_MAXN] = {}, o = 0;
+  for (int k = 0; k < M; ++k) {
+    soff[k] = o;
+    o += c.ld[k];
+  }
+  const int rslot = o++;
+  while (o % 4 != 2) ++o;
+  const int ldr = o;
+  std::ostringstream src;
+  src << kPrelude;
+  const int nb = (int)blocks.size();
+  for (int i = 0; i <= nb; ++i) {
+    const std::vector<uint32_t> none;
+    const auto& prev = i > 0 ? blocks[i - 1] : none;
+    const auto& cur = i < nb ? blocks[i] : none;
+    const int nf = (int)cur.size(), pnf = (int)prev.size();
+    const int NT = i == nb ? 2 : (nf <= 15 ? 2 : (nf <= 23 ? 3 : 4));
+    nts.push_back(NT);
+    std::vector<bool> used(VEST_MAXN * 16, false);
+    std::ostringstream pv, cv;
+    products(c, prev, pv, [](int f, const std::string& e) {
+      return "t = fma(" + e + ", sq_q[warp][" + std::to_string(f) + "], t);";
+    }, used);
+    products(c, cur, cv, [](int f, const std::string& e) {
+      return "X[" + std::to_string(f * 36) + " + lane] = " + e + ";";
+    }, used);
+    std::ostringstream iss, lu;
+    for (int k = 0; k < M; ++k) {
+      iss << "      { const double* row = a.f[" << k << "] + (unsigned long long)idx[" << k << "] * " << c.ld[k] << ";\n";
+      for (int t = 0; t < c.ld[k] / 2; ++t)
+        iss << "        cp16(st + " << (soff[k] + 2 * t) * 8 << "u, row + " << 2 * t << ");\n";
+      iss << "      }\n";
+      for (int b = 0; b < c.ranks[k]; ++b)
+        if (used[k * 16 + b]) lu << "    const double " << uname(k, b) << " = st[" << soff[k] + b << "];\n";
+    }
+    std::string p = kPass;
+    replace_all(p, "@NAME@", "vest_cp_" + std::to_string(i));
+    replace_all(p, "@M@", std::to_string(M));
+    replace_all(p, "@LDR@", std::to_string(ldr));
+    replace_all(p, "@NT@", std::to_string(NT));
+    replace_all(p, "@NF@", std::to_string(nf));
+    replace_all(p, "@PNF@", std::to_string(pnf));
+    replace_all(p, "@KIND@", i == nb ? "2" : "0");
+    replace_all(p, "@JM@", std::to_string(c.ranks[M]));
+    replace_all(p, "@LDM@", std::to_string(c.ld[M]));
+    replace_all(p, "@RSLOT@", std::to_string(rslot));
+    replace_all(p, "@ISSUE@", iss.str());
+    replace_all(p, "@LOADU@", lu.str());
+    replace_all(p, "@PREV@", pv.str());
+    replace_all(p, "@CUR@", cv.str());
+    src << p;
+  }
+  ldr_out = ldr;
+  return src.str();
+}
+
+// Build (or reuse) the generated passes for a plan.
+bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, uint64_t plan_key) {
+  if (c.core_gen && c.core_gen->key == plan_key) return true;
+  core_gen_free(c);
+  std::vector<int> nts;
+  int ldr = 0;
+  const std::vector<char> cubin = nvrtc_compile(core_gen_source(c, blocks, nts, ldr), "vest_core_gen.cu");
+  const int nb = (int)blocks.size();
+  auto* s = new CoreGenState;
+  s->key = plan_key;
+  s->ldr = ldr;
+  s->nt = nts;
+  check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "core gen load");
+  s->k.resize(nb + 1);
+  for (int i = 0; i <= nb; ++i) {
+    const std::string nm = "vest_cp_" + std::to_string(i);
+    check(cudaLibraryGetKernel(&s->k[i], s->lib, nm.c_str()), "core gen kernel");
+  }
+  c.core_gen = s;
+  return true;
+}
+
+// pass i of the prepared plan (i < nb: statistics of block i after applying
+// block i-1; i == nb: apply the last block, per-chunk sums of r^2)
+void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stride, double* chunk_sq) {
+  CoreGenState& s = *c.core_gen;
+  const int m = c.N - 1;
+  const DevCSF csf = c.csf_view(m);
+  if (csf.nchunks == 0) return;
+  CoreGenArgs a{};
+  for (int k = 0; k < c.N; ++k) {
+    a.oc[k] = csf.oc[k];
+    a.f[k] = c.d_factor[k];
+  }
+  a.r = c.d_r;
+  a.prev_dg = prev_dg;
+  a.stats = stats;
+  a.chunk_sq = chunk_sq;
+  a.chunks = csf.chunks;
+  a.nchunks = csf.nchunks;
+  a.stride = stride;
+  const int NT = s.nt[i];
+  const size_t sm = (unsigned long long)4 * (2 * 32 * s.ldr + NT * 8 * 36) * sizeof(double);
+  const void* fn = reinterpret_cast<const void*>(s.k[i]);
+  check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "core gen smem");
+  int per_sm = 0, sms = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 128, sm), "core gen occupancy");
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  const uint32_t need = (csf.nchunks + 3) / 4;
+  const unsigned grid = std::max(1u, std::min<uint32_t>(need, (uint32_t)std::max(1, per_sm) * sms));
+  void* args[] = {&a};
+  check(cudaLaunchKernel(fn, dim3(grid), dim3(128), args, sm, c.stream), "core gen launch");
+  count_launch();
+}
+
+}  // namespace vest

@@ -854,6 +854,7 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_dg);
   cudaFree(c.d_delta);
   sparse_free(c);
+  core_gen_free(c);
   cudaFree(c.d_pack_u);
   cudaFree(c.d_pack_w);
   cudaFree(c.d_counter);
@@ -882,6 +883,10 @@ int vest_ctx_set_core_block(vest_ctx* h, int fibers) {
 }
 int vest_ctx_set_sparse_delta(vest_ctx* h, int mode) {
   h->c.sparse_delta = mode < 0 ? -1 : (mode ? 1 : 0);
+  return VEST_OK;
+}
+int vest_ctx_set_core_gen(vest_ctx* h, int mode) {
+  h->c.core_gen_mode = mode < 0 ? -1 : (mode ? 1 : 0);
   return VEST_OK;
 }
 int vest_ctx_sparse_delta_active(const vest_ctx* h) { return h && sparse_delta_enabled(h->c) ? 1 : 0; }

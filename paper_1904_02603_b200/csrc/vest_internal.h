@@ -93,6 +93,7 @@ struct ModeData {
 
 struct Ctx;
 struct SparseState;  // vest_sparse.cu: NVRTC module of the mask-specialised delta contraction
+struct CoreGenState;  // vest_core_gen.cu: NVRTC module of the plan-specialised core passes
 
 // Kernel families instantiated for compile-time rank tuples.
 struct ShapeOps {
@@ -175,6 +176,8 @@ struct Ctx {
   void* d_sel = nullptr;           // radix-select state
 
   SparseState* sparse = nullptr;
+  CoreGenState* core_gen = nullptr;
+  int core_gen_mode = -1;          // plan-specialised core passes: -1 auto, 0 off, 1 on
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
   double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
   bool force_generic = false;
@@ -216,6 +219,13 @@ cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunk
 bool sparse_delta_enabled(const Ctx& c);
 void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out);
 void sparse_free(Ctx& c);
+std::vector<char> nvrtc_compile(const std::string& src, const char* name);
+void core_gen_free(Ctx& c);
+bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, uint64_t plan_key);
+void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stride, double* chunk_sq);
+std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, std::vector<int>& nts,
+                            int& ldr);
+std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c);
 int sparse_compile_check(int N, const int* ranks, const uint8_t* core_mask, uint64_t* bytes, std::string* err);
 
 void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values);

@@ -224,12 +224,12 @@ bool sparse_delta_enabled(const Ctx& c) {
   return 4 * live < c.G;
 }
 
-static std::vector<char> compile_cubin(const std::string& src) {
+std::vector<char> nvrtc_compile(const std::string& src, const char* name) {
   const Nvrtc& nv = nvrtc();
-  if (!nv.h || !nv.create || !nv.compile || !nv.cubin) throw RtError{"sparse delta: libnvrtc not found"};
+  if (!nv.h || !nv.create || !nv.compile || !nv.cubin) throw RtError{"libnvrtc not found (mask-specialised kernels)"};
   void* prog = nullptr;
-  if (nv.create(&prog, src.c_str(), "vest_sparse_delta.cu", 0, nullptr, nullptr) != 0)
-    throw RtError{"sparse delta: nvrtcCreateProgram failed"};
+  if (nv.create(&prog, src.c_str(), name, 0, nullptr, nullptr) != 0)
+    throw RtError{"nvrtcCreateProgram failed"};
   const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
   const int rc = nv.compile(prog, 3, opts);
   if (rc != 0) {
@@ -238,7 +238,7 @@ static std::vector<char> compile_cubin(const std::string& src) {
     std::string log(ls, '\0');
     nv.log(prog, &log[0]);
     nv.destroy(&prog);
-    throw RtError{"sparse delta: NVRTC compile failed: " + log.substr(0, 2000)};
+    throw RtError{std::string("NVRTC compile failed (") + name + "): " + log.substr(0, 2000)};
   }
   size_t sz = 0;
   nv.cubin_size(prog, &sz);
@@ -252,7 +252,7 @@ static void ensure_module(Ctx& c) {
   const uint64_t key = mask_key(c);
   if (c.sparse && c.sparse->key == key) return;
   sparse_free(c);
-  const std::vector<char> cubin = compile_cubin(gen_source(c));
+  const std::vector<char> cubin = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu");
   auto* s = new SparseState;
   s->key = key;
   check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "sparse delta load");
@@ -303,7 +303,12 @@ int sparse_compile_check(int N, const int* ranks, const uint8_t* core_mask, uint
       c.G *= ranks[k];
     }
     c.h_core_mask.assign(core_mask, core_mask + c.G);
-    *bytes = compile_cubin(gen_source(c)).size();
+    *bytes = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu").size();
+    if (N >= 2) {  // the plan-specialised core passes of the same mask
+      std::vector<int> nts;
+      int ldr = 0;
+      *bytes += nvrtc_compile(core_gen_source(c, core_gen_plan(c), nts, ldr), "vest_core_gen.cu").size();
+    }
     return 0;
   } catch (const RtError& e) {
     *err = e.msg;

@@ -287,6 +287,10 @@ class Device:
         """Mask-specialised delta contraction: -1 auto, 0 off, 1 on."""
         check(self._L.vest_ctx_set_sparse_delta(self.h, int(mode)))
 
+    def set_core_gen(self, mode: int):
+        """Plan-specialised core-sweep passes: -1 auto, 0 off, 1 on."""
+        check(self._L.vest_ctx_set_core_gen(self.h, int(mode)))
+
     def sparse_delta_active(self) -> bool:
         return bool(self._L.vest_ctx_sparse_delta_active(self.h))
 

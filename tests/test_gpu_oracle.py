@@ -50,12 +50,14 @@ def model_of(s, dims, ranks):
     return st.TuckerModel(list(dims), list(ranks), core, cm, fs, ms)
 
 
-def phases(dims, ranks, nnz, seed, reg, lam, iters=2, pr=0.3, generic=False, sparse=None, **kw):
+def phases(dims, ranks, nnz, seed, reg, lam, iters=2, pr=0.3, generic=False, sparse=None, core_gen=None, **kw):
     coords, values, m = random_instance(dims, ranks, nnz, seed, **kw)
     x = st.make_tensor(dims, coords, values)
     dev = st.Device(x, ranks)
     if generic:
         dev.force_generic(True)
+    if core_gen is not None:
+        dev.set_core_gen(core_gen)
     if sparse is not None:
         dev.set_sparse_delta(sparse)
         assert dev.sparse_delta_active() == bool(sparse)
@@ -132,6 +134,18 @@ def test_sparse_delta_auto_selection():
 def test_sparse_delta_forced(dims, ranks, mf, reg, lam):
     nnz = min(int(np.prod(dims)) // 3, 4000)
     phases(dims, ranks, nnz, 31, reg, lam, iters=2, mask_frac=mf, sparse=1)
+
+
+# plan-specialised (NVRTC) core passes forced on/off across orders, plans and
+# masks (prefix blocks for dense cores, live-fiber runs for sparse ones)
+@pytest.mark.parametrize("dims,ranks,mf", [([20, 18, 16, 14], [8, 8, 8, 8], 0.9), ([9, 8, 8, 7, 7], [5, 5, 5, 5, 5], 0.0),
+                                           ([30, 25], [4, 3], 0.2), ([7, 6, 5, 4, 3], [2, 2, 3, 2, 2], 0.2),
+                                           ([40, 30, 20], [3, 5, 4], 0.3)])
+@pytest.mark.parametrize("gen", [0, 1])
+def test_core_gen_passes(dims, ranks, mf, gen):
+    nnz = min(int(np.prod(dims)) // 3, 4000)
+    phases(dims, ranks, nnz, 41, 0, 0.01, iters=2, mask_frac=mf, core_gen=gen)
+    phases(dims, ranks, nnz, 42, 1, 0.1, iters=1, mask_frac=mf, core_gen=gen)
 
 
 def test_sparse_delta_heavy_rows():
