@@ -296,8 +296,12 @@ constexpr int stage_words() {
 // where v = G x_m a (|G| / J_m values, computed once per row into shared
 // memory), so each entry costs the (N-1)-mode contraction instead of a full
 // reconstruction.  Writes r (CSF order of mode m) for the chunk's entries.
+// Returns the lane's partial sum of r^2.  Also the residual pass (kResid) of
+// rank-specialised shapes: |G| / J_m + ... FMA per entry instead of the full
+// delta contraction.
 template <class P>
-__device__ __forceinline__ void fused_residual(const RowPassArgs& a, const Chunk& ch, double* v, int lane) {
+__device__ __forceinline__ double fused_residual(const RowPassArgs& a, const Chunk& ch, double* v, int lane) {
+  double sq = 0.0;
   if constexpr (P::kStatic) {
     using S = typename P::Shape;
     if constexpr (S::N >= 3) {
@@ -328,10 +332,13 @@ __device__ __forceinline__ void fused_residual(const RowPassArgs& a, const Chunk
         });
         double rec[1];
         trailingN<Q, 0, 1>(gv, u, 0, rec);
-        a.r_out[pos] = __ldg(a.csf.val + pos) - rec[0];
+        const double r = __ldg(a.csf.val + pos) - rec[0];
+        a.r_out[pos] = r;
+        sq = fma(r, r, sq);
       }
     }
   }
+  return sq;
 }
 
 template <class P, int KIND>
@@ -348,6 +355,13 @@ __global__ void __launch_bounds__(kRowWarps * 32, P::kMinB) k_rowpass(RowPassArg
   const uint32_t ci = blockIdx.x * kRowWarps + warp;
   if (ci >= a.csf.nchunks) return;
   const Chunk ch = a.csf.chunks[ci];
+  if constexpr (KIND == kResid && P::kStatic) {
+    if constexpr (P::Shape::N >= 3) {  // kResid runs on the last mode: v = G x_m a_row
+      const double sq = warp_sum(fused_residual<P>(a, ch, smem + warp * stage_words<P>() + 128, lane));
+      if (lane == 0) a.chunk_out[ci] = sq;
+      return;
+    }
+  }
   constexpr int NE = P::NE;
   const int J = pol.J();
   const int mode = pol.mode();

@@ -214,10 +214,15 @@ void sparse_free(Ctx& c) {
 // Live-cell threshold: the generated contraction costs ~2 FMA per unmasked
 // cell against >= |G| for the dense factorised one.
 bool sparse_delta_enabled(const Ctx& c) {
-  if (c.sparse_delta == 0 || c.N < 2) return false;
+  static const int env = [] {  // VEST_SPARSE_DELTA=0/1 overrides "auto" (A/B timing)
+    const char* e = getenv("VEST_SPARSE_DELTA");
+    return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+  }();
+  const int mode = c.sparse_delta >= 0 ? c.sparse_delta : env;
+  if (mode == 0 || c.N < 2) return false;
   for (int k = 0; k < c.N; ++k)
     if (c.ranks[k] > 15) return false;  // the statistics kernel's DMMA tile
-  if (c.sparse_delta == 1) return true;
+  if (mode == 1) return true;
   if (!c.ops || c.force_generic) return false;
   long live = 0;
   for (uint8_t m : c.h_core_mask) live += !m;

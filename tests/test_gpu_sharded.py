@@ -91,3 +91,37 @@ def test_sharded_skewed_rows():
         for a, b in zip(res, ref_res):
             assert abs(a - b) <= 1e-9 * b
         assert_close(m.core, ref_m.core, "core", tol=1e-9)
+
+
+# 4- and 5-mode shapes: the general core sweep with plan-specialised passes and,
+# for the 90 %-masked core, the mask-specialised delta (both NVRTC-compiled),
+# through the shard exchange points
+@pytest.mark.parametrize("dims,ranks,mf", [([30, 28, 26, 24], [8, 8, 8, 8], 0.9), ([9, 9, 8, 8, 7], [5, 5, 5, 5, 5], 0.0)])
+def test_sharded_generated_kernels(dims, ranks, mf):
+    x = _instance(dims, ranks, 8000, 5)
+    m = st.init_random(dims, ranks, 9)
+    if mf > 0:
+        cm = (np.random.default_rng(3).random(m.core.shape) < mf).astype(np.uint8)
+        m.core[cm == 1] = 0.0
+        m.core_mask = cm
+    dev = st.Device(x, ranks)
+    dev.set_model(m)
+    assert dev.sparse_delta_active() == (mf > 0)
+    ref_res = [dev.cd_iteration(0, 0.01) for _ in range(3)]
+    ref_m = dev.get_model()
+    group = sh.LocalGroup(2)
+    bounds = sh.partition(x, 2)
+    devs = [sh.ShardDevice(x, ranks, r, 2, group.hooks_for(r), bounds=bounds) for r in range(2)]
+
+    def body(r):
+        devs[r].set_model(m)
+        return [devs[r].cd_iteration(0, 0.01) for _ in range(3)], devs[r].get_model()
+
+    outs = group.run([lambda r=r: body(r) for r in range(2)])
+    for res, mm in outs:
+        for a, b in zip(res, ref_res):
+            assert abs(a - b) <= 1e-9 * b
+        assert_close(mm.core, ref_m.core, "core", tol=1e-9)
+        for n in range(len(dims)):
+            assert_close(mm.factors[n], ref_m.factors[n], f"factor{n}", tol=1e-9)
+    assert np.array_equal(outs[0][1].core, outs[1][1].core)
