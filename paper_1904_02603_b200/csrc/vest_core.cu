@@ -539,6 +539,71 @@ __global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, i
   out[o] = s;
 }
 
+// Live-cell block Gram without the dense GEMM: for a sparse block (config 4:
+// ~43 live cells of 31 fibers x 8) the GEMM over [S | R] x [a a^T | a] forms
+// every (fiber pair, c pair) -- ~20x the entries the solve reads.  Each thread
+// owns up to kHsPer entries of H (upper triangle over the live cells) or C,
+// tab[e] = s-index | c << 16 | c' << 24 (c' = 255: a C entry, R x a_c), and
+// accumulates s * a_c * a_c' over its CTA's chunks in order (batches of chunk
+// statistics rows staged in shared memory); CTA partials are summed in a
+// fixed order afterwards (deterministic).
+constexpr int kHsBatch = 8, kHsPer = 8, kHsThreads = 256;
+__global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __restrict__ stats, int stride, int width,
+                                                             const Chunk* __restrict__ chunks, uint32_t nchunks,
+                                                             const double* __restrict__ A, int ld, int Jm,
+                                                             const uint32_t* __restrict__ tab, int E,
+                                                             double* __restrict__ partial) {
+  extern __shared__ double hs[];
+  double* ss = hs;                     // [kHsBatch][width]
+  double* sa = hs + kHsBatch * width;  // [kHsBatch][Jm]
+  const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
+  uint32_t my[kHsPer];
+  double acc[kHsPer];
+#pragma unroll
+  for (int j = 0; j < kHsPer; ++j) {
+    const int e = threadIdx.x + kHsThreads * j;
+    my[j] = e < E ? __ldg(tab + e) : 0xffffffffu;
+    acc[j] = 0.0;
+  }
+  for (uint32_t cb = c0; cb < c1; cb += kHsBatch) {
+    const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb * width; t += kHsThreads) {
+      const int b = t / width, w = t - b * width;
+      ss[t] = __ldg(stats + (size_t)(cb + b) * stride + w);
+    }
+    for (int t = threadIdx.x; t < nb * Jm; t += kHsThreads) {
+      const int b = t / Jm, q = t - b * Jm;
+      sa[t] = __ldg(A + (size_t)chunks[cb + b].row * ld + q);
+    }
+    __syncthreads();
+    for (int b = 0; b < nb; ++b) {
+#pragma unroll
+      for (int j = 0; j < kHsPer; ++j) {
+        if (my[j] == 0xffffffffu) continue;
+        const uint32_t cj = my[j] >> 24;
+        double v = ss[b * width + (my[j] & 0xffffu)] * sa[b * Jm + ((my[j] >> 16) & 255u)];
+        if (cj != 255u) v *= sa[b * Jm + cj];
+        acc[j] += v;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kHsPer; ++j) {
+    const int e = threadIdx.x + kHsThreads * j;
+    if (e < E) partial[(size_t)blockIdx.x * E + e] = acc[j];
+  }
+}
+
+__global__ void k_sum_groups(const double* raw, int n, int groups, double* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int g = 0; g < groups; ++g) s += raw[(size_t)g * n + j];
+  out[j] = s;
+}
+
 // Sequential Gauss-Seidel over the block's live cells.  The CTA compacts the
 // block's unmasked cells (ballot scan, row-major order), loads [T | C], their
 // core values into shared memory and expands the dense live-cell Gram H
@@ -547,7 +612,7 @@ __global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, i
 // of the remaining cells' c.  Masked cells keep dg = 0 (updates.hpp:199-202).
 __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, int Jm, int nl, const uint32_t* fib,
                                                     double* core, const uint8_t* core_mask, int reg,
-                                                    double lambda, double* dg_out) {
+                                                    double lambda, double* dg_out, int packed) {
   extern __shared__ double sm[];
   const int NAm = Jm * (Jm + 1) / 2;
   const int nT = nf * (nf + 1) / 2 * NAm;
@@ -570,7 +635,15 @@ __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, in
     }
   }
   __syncthreads();
+  // packed: tc = [H (upper triangle over the live cells, row-major) | C (live)]
+  // (k_core_hsample); else [T | C] of the block GEMM
+  const int nh = nl * (nl + 1) / 2;
   for (int t = threadIdx.x; t < nl * nl; t += blockDim.x) {
+    if (packed) {
+      const int i = t / nl, j = t % nl;
+      H[t] = tc[i <= j ? tri(i, j, nl) : tri(j, i, nl)];
+      continue;
+    }
     const int q = lq[t / nl], q2 = lq[t % nl];
     const int f = q / Jm, c = q % Jm, f2 = q2 / Jm, c2 = q2 % Jm;
     const int ps = f <= f2 ? tri(f, f2, nf) : tri(f2, f, nf);
@@ -579,12 +652,12 @@ __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, in
   }
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
     const int q = lq[l];
-    cc[l] = tc[nT + q];
+    cc[l] = packed ? tc[nh + l] : tc[nT + q];
     gv[l] = core[(int)fib[q / Jm] * Jm + q % Jm];
     // the denominators do not depend on the sweep state: invert them in
     // parallel, off the sequential critical path
     const int f = q / Jm, c = q % Jm;
-    const double hqq = tc[tri(f, f, nf) * NAm + tri(c, c, Jm)];
+    const double hqq = packed ? tc[tri(l, l, nl)] : tc[tri(f, f, nf) * NAm + tri(c, c, Jm)];
     const double den = reg == 0 ? hqq + lambda : 2.0 * hqq;
     rd[l] = den != 0.0 ? 1.0 / den : 0.0;
   }
@@ -872,7 +945,7 @@ Blocks plan_general(const Ctx& c, int F) {
 
 bool use_core_gen(const Ctx& c) {
   if (c.core_gen_mode >= 0) return c.core_gen_mode == 1;
-  return c.ops && !c.force_generic && c.core_block == 0;
+  return c.ops && !c.force_generic && c.core_block == 0 && nvrtc_available();
 }
 
 std::vector<std::vector<uint32_t>> block_lists(const Blocks& b) {
@@ -1043,6 +1116,52 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
   return nout;
 }
 
+// The sampled live-cell Gram (k_core_hsample) for block bi of a general plan,
+// into c.d_gemm_out as [H packed | C]; returns its length, or -1 when the
+// dense block GEMM is cheaper (dense blocks) or the block is too wide.
+int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
+  const int m = c.N - 1, Jm = c.ranks[m];
+  const int nf = b.len[bi], nl = b.nlive[bi];
+  const int E = nl * (nl + 1) / 2 + nl;
+  const int NS = nf * (nf + 1) / 2, NAm = Jm * (Jm + 1) / 2;
+  if (E > kHsPer * kHsThreads || 4 * E >= (NS + nf) * (NAm + Jm)) return -1;
+  std::vector<int> lq;
+  for (int f = 0; f < nf; ++f)
+    for (int q = 0; q < Jm; ++q)
+      if (!c.h_core_mask[(size_t)b.fib[b.start[bi] + f] * Jm + q]) lq.push_back(f * Jm + q);
+  std::vector<uint32_t> tab(E);
+  auto tri_h = [](int i, int j, int n) { return i * n - i * (i - 1) / 2 + (j - i); };
+  for (int i = 0; i < nl; ++i) {
+    const int fi = lq[i] / Jm, ci = lq[i] % Jm;
+    for (int j = i; j < nl; ++j) {
+      const int fj = lq[j] / Jm, cj = lq[j] % Jm;  // fi <= fj (row-major live order)
+      tab[tri_h(i, j, nl)] = (uint32_t)tri_h(fi, fj, nf) | (uint32_t)ci << 16 | (uint32_t)cj << 24;
+    }
+    tab[nl * (nl + 1) / 2 + i] = (uint32_t)(NS + fi) | (uint32_t)ci << 16 | 255u << 24;
+  }
+  ensure(c, reinterpret_cast<double**>(&c.d_hstab), &c.hstab_cap, (size_t)(E + 1) / 2 + 1);
+  check(cudaMemcpyAsync(c.d_hstab, tab.data(), (size_t)E * 4, cudaMemcpyHostToDevice, c.stream), "hsample table");
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  const ModeData& md = c.modes[m];
+  const int nparts = std::max(1, std::min<int>(4 * sms, (int)((md.nchunks + kHsBatch - 1) / kHsBatch)));
+  const int groups = 16;
+  ensure(c, &c.d_gemm_part, &c.gemm_part_cap, (size_t)nparts * E + (size_t)groups * E);
+  ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)E);
+  double* raw = c.d_gemm_part + (size_t)nparts * E;
+  const int width = NS + nf;
+  const size_t sm = (size_t)kHsBatch * (width + Jm) * sizeof(double);
+  ProfScope ps(c, kProfCoreGemm);
+  check(cudaFuncSetAttribute(k_core_hsample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "hsample smem");
+  k_core_hsample<<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks, md.nchunks,
+                                                        c.d_factor[m], c.ld[m], Jm, c.d_hstab, E, c.d_gemm_part);
+  k_gemm_reduce1<<<dim3((E + 255) / 256, groups), 256, 0, c.stream>>>(c.d_gemm_part, nparts, E, groups, raw);
+  k_sum_groups<<<(E + 255) / 256, 256, 0, c.stream>>>(raw, E, groups, c.d_gemm_out);
+  count_launch(3);
+  check(cudaGetLastError(), "hsample");
+  return E;
+}
+
 void upload_fibers(Ctx& c, const Blocks& b) {
   ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
   check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
@@ -1106,14 +1225,16 @@ void core_sweep(Ctx& c, int reg, double lambda) {
     }
     if (last) break;
     const int nf = b.len[bi];
-    const int nout = block_gemm(c, nf, 0, stride);
+    int nout = sops ? -1 : block_hsample(c, b, bi, stride);
+    const int packed = nout >= 0 ? 1 : 0;
+    if (nout < 0) nout = block_gemm(c, nf, 0, stride);
     comm_allreduce(c, c.d_gemm_out, (uint64_t)nout);  // block statistics over the shards
     ProfScope ps(c, kProfCoreSolve);
     const size_t nq = (size_t)nf * Jm, nl = (size_t)b.nlive[bi];
     const size_t sm = (nl * nl + 3 * nl) * sizeof(double) + nq * sizeof(int);
     check(cudaFuncSetAttribute(k_core_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "solve smem");
     k_core_solve<<<1, 256, sm, c.stream>>>(c.d_gemm_out, nf, Jm, (int)nl, c.d_fibers + b.start[bi], c.d_core,
-                                           c.d_core_mask, reg, lambda, c.d_dg);
+                                           c.d_core_mask, reg, lambda, c.d_dg, packed);
     count_launch();
     check(cudaGetLastError(), "core solve");
   }

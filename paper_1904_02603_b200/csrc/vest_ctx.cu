@@ -853,6 +853,7 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_fibers);
   cudaFree(c.d_dg);
   cudaFree(c.d_delta);
+  cudaFree(c.d_hstab);
   sparse_free(c);
   core_gen_free(c);
   cudaFree(c.d_pack_u);

@@ -180,6 +180,7 @@ struct Ctx {
   int core_gen_mode = -1;          // plan-specialised core passes: -1 auto, 0 off, 1 on
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
   double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
+  uint32_t* d_hstab = nullptr;     size_t hstab_cap = 0;    // live-cell Gram entry table (k_core_hsample)
   bool force_generic = false;
   int core_block = 0;  // fibers per block (0 = auto)
   const ShapeOps* ops = nullptr;
@@ -220,6 +221,7 @@ bool sparse_delta_enabled(const Ctx& c);
 void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out);
 void sparse_free(Ctx& c);
 std::vector<char> nvrtc_compile(const std::string& src, const char* name);
+bool nvrtc_available();
 void core_gen_free(Ctx& c);
 bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, uint64_t plan_key);
 void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stride, double* chunk_sq);

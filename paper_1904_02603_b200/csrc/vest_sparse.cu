@@ -211,6 +211,11 @@ void sparse_free(Ctx& c) {
   c.sparse = nullptr;
 }
 
+bool nvrtc_available() {
+  const Nvrtc& nv = nvrtc();
+  return nv.h && nv.create && nv.compile && nv.cubin;
+}
+
 // Live-cell threshold: the generated contraction costs ~2 FMA per unmasked
 // cell against >= |G| for the dense factorised one.
 bool sparse_delta_enabled(const Ctx& c) {
@@ -223,7 +228,7 @@ bool sparse_delta_enabled(const Ctx& c) {
   for (int k = 0; k < c.N; ++k)
     if (c.ranks[k] > 15) return false;  // the statistics kernel's DMMA tile
   if (mode == 1) return true;
-  if (!c.ops || c.force_generic) return false;
+  if (!c.ops || c.force_generic || !nvrtc_available()) return false;
   long live = 0;
   for (uint8_t m : c.h_core_mask) live += !m;
   return 4 * live < c.G;
