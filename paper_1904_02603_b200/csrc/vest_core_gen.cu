@@ -96,8 +96,8 @@ extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double sq_q[4][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* const stage = smem + (unsigned long long)warp * (2 * 32 * LDR + NC * 36);
-  double* const X = stage + 2 * 32 * LDR;
+  double* const stage = smem + (unsigned long long)warp * (32 * LDR + NC * 36);  // one round's rows
+  double* const X = stage + 32 * LDR;
   for (int t = lane; t < NC * 36; t += 32) X[t] = 0.0;
   const unsigned wstride = gridDim.x * 4;
   struct Cur { unsigned ci, end, base, row; };
@@ -151,18 +151,21 @@ extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
 #pragma unroll
   for (int t = 0; t < NTT; ++t) d[t][0] = d[t][1] = 0.0;
   double sq = 0.0;
-  int buf = 0;
   while (true) {
-    issue(nxt, buf ^ 1, inx);
-    const Cur nn = next(nxt);
-    coords(nn, inx);
-    cp_wait1();
+    // this round's rows -> registers, then the next round's gathers into the
+    // same (single) stage while this round computes: half the shared memory
+    // of a double buffer, 12 instead of 8 resident warps per SM
+    cp_wait0();
     __syncwarp();
-    const double* st = stage + (buf * 32 + lane) * LDR;
+    const double* st = stage + lane * LDR;
     const unsigned pos = cur.base + lane;
     const bool valid = pos < cur.end;
     double r = st[RSLOT];
 @LOADU@
+    __syncwarp();
+    issue(nxt, 0, inx);
+    const Cur nn = next(nxt);
+    coords(nn, inx);
     if (PNF > 0 && valid) {
       double t = 0.0;
 @PREV@
@@ -210,7 +213,6 @@ extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
     }
     cur = nxt;
     nxt = nn;
-    buf ^= 1;
   }
   cp_wait0();
 }
@@ -374,7 +376,7 @@ void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stri
   a.nchunks = csf.nchunks;
   a.stride = stride;
   const int NT = s.nt[i];
-  const size_t sm = (unsigned long long)4 * (2 * 32 * s.ldr + NT * 8 * 36) * sizeof(double);
+  const size_t sm = (unsigned long long)4 * (32 * s.ldr + NT * 8 * 36) * sizeof(double);
   const void* fn = reinterpret_cast<const void*>(s.k[i]);
   check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "core gen smem");
   int per_sm = 0, sms = 0;

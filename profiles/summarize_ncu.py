@@ -6,7 +6,10 @@ import subprocess
 import sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-rows = list(csv.reader(open("gpurun_out/launches.csv")))
+launches = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/launches.csv"
+rep = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/prof_full.ncu-rep"
+cmd = sys.argv[4] if len(sys.argv) > 4 else "python bench.py --steps 1 --warmup 1 --no-cpu"
+rows = list(csv.reader(open(launches)))
 hdr, data = None, []
 for r in rows:
     if "Kernel Name" in r:
@@ -24,7 +27,7 @@ for d in data:
     agg[k][0] += v
     agg[k][1] += 1
 tot = sum(v[0] for v in agg.values())
-lines = [f"# ncu launch list ({tag}): `python bench.py --steps 1 --warmup 1 --no-cpu`", "",
+lines = [f"# ncu launch list ({tag}): `{cmd}`", "",
          "Cold-cache, serialised per-launch device times (ncu --metrics gpu__time_duration.sum); the run includes",
          "context build, warm-up, one timed step, the prune event and the e2e step, so compare SHARES.", "",
          "| kernel | launches | total us | share |", "|---|---|---|---|"]
@@ -32,7 +35,7 @@ for k, v in sorted(agg.items(), key=lambda x: -x[1][0]):
     lines.append(f"| `{k}` | {v[1]} | {v[0] / 1e3:.1f} | {100 * v[0] / tot:.1f}% |")
 open(f"profiles/{tag}_ncu_launches.md", "w").write("\n".join(lines) + "\n")
 
-raw = subprocess.run(["ncu", "-i", "gpurun_out/prof_full.ncu-rep", "--page", "raw", "--csv"],
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 h, units, body = rows[0], rows[1], rows[2:]
@@ -55,7 +58,7 @@ json.dump(out, open(f"profiles/{tag}_ncu_full.json", "w"), indent=1)
 # traffic of the dominant kernel (factor-row update, mode 0) per launch
 for d in body:
     name = d[h.index("Kernel Name")]
-    if "k_rowpass" in name and "0>,0>" in name.replace(" ", ""):
+    if tag == "r1" and "k_rowpass" in name and "0>,0>" in name.replace(" ", ""):
         rd = float(d[h.index("dram__bytes_read.sum")])
         wr = float(d[h.index("dram__bytes_write.sum")])
         u = units[h.index("dram__bytes_read.sum")]
