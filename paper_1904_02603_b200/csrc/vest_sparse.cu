@@ -25,6 +25,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
@@ -118,59 +119,75 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
   };
   std::sort(cells.begin(), cells.end(), key);
 
-  o << "extern \"C\" __global__ void __launch_bounds__(256) vest_sd_" << n << "(const SparseDeltaArgs a) {\n"
-    << "  for (unsigned long long t = blockIdx.x * 256ull + threadIdx.x; t < a.n; t += gridDim.x * 256ull) {\n"
-    << "    const unsigned long long pos = a.p0 + t;\n";
-  for (int k : oth) {
-    const int ld = c.ld[k];
-    o << "    const double* r" << k << " = a.f[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + pos) * "
-      << ld << "ull;\n";
-    for (int b = 0; b < c.ranks[k]; b += 2) {
-      if (b + 1 < c.ranks[k]) {
-        o << "    const double2 v" << k << "_" << b << " = __ldg(reinterpret_cast<const double2*>(r" << k << " + " << b
-          << "));\n"
-          << "    const double " << u(k, b) << " = v" << k << "_" << b << ".x, " << u(k, b + 1) << " = v" << k << "_"
-          << b << ".y;\n";
-      } else {
-        o << "    const double " << u(k, b) << " = __ldg(r" << k << " + " << b << ");\n";
+  // two entries per thread (E = 0, 1: t and t + 256 of the block's stride
+  // window): every core value is loaded once (uniform constant load) and
+  // feeds both entries' FMAs
+  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) vest_sd_" << n << "(const SparseDeltaArgs a) {\n"
+    << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
+    << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
+  for (int e = 0; e < 2; ++e) {
+    const std::string E = std::to_string(e);
+    for (int k : oth) {
+      const int ld = c.ld[k];
+      const std::string rk = "r" + std::to_string(k) + "e" + E;
+      o << "    const double* " << rk << " = a.f[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + a.p0 + t"
+        << E << ") * " << ld << "ull;\n";
+      for (int b = 0; b < c.ranks[k]; b += 2) {
+        const std::string ua = u(k, b) + "e" + E;
+        if (b + 1 < c.ranks[k]) {
+          const std::string v = "v" + std::to_string(k) + "_" + std::to_string(b) + "e" + E;
+          o << "    const double2 " << v << " = __ldg(reinterpret_cast<const double2*>(" << rk << " + " << b << "));\n"
+            << "    const double " << ua << " = " << v << ".x, " << u(k, b + 1) << "e" << E << " = " << v << ".y;\n";
+        } else {
+          o << "    const double " << ua << " = __ldg(" << rk << " + " << b << ");\n";
+        }
       }
     }
+    for (int j = 0; j < c.ranks[n]; ++j) o << "    double d" << j << "e" << E << " = 0.0;\n";
   }
-  for (int j = 0; j < c.ranks[n]; ++j) o << "    double d" << j << " = 0.0;\n";
-  // nested prefix groups
-  size_t i = 0;
   auto same_prefix = [&](const Cell& a, const Cell& b, int upto) {
     for (int q = 0; q <= upto; ++q)
       if (a.beta[oth[q]] != b.beta[oth[q]]) return false;
     return true;
   };
+  size_t i = 0;
   while (i < cells.size()) {
-    // open the prefix levels of cells[i]
+    // open the prefix levels of cells[i] (both entries)
     for (int q = 0; q + 1 < L; ++q) {
       const int k = oth[q], b = cells[i].beta[k];
-      if (q == 0) o << "    { const double w0 = " << u(k, b) << ";\n";
-      else o << "    { const double w" << q << " = w" << (q - 1) << " * " << u(k, b) << ";\n";
+      o << "    {";
+      for (int e = 0; e < 2; ++e) {
+        const std::string E = std::to_string(e);
+        if (q == 0) o << " const double w0e" << E << " = " << u(k, b) << "e" << E << ";";
+        else o << " const double w" << q << "e" << E << " = w" << (q - 1) << "e" << E << " * " << u(k, b) << "e" << E << ";";
+      }
+      o << "\n";
     }
-    // all cells of this full prefix
-    size_t e = i;
-    while (e < cells.size() && (L < 2 || same_prefix(cells[i], cells[e], L - 2))) ++e;
-    size_t g = i;
-    while (g < e) {
+    size_t e_end = i;
+    while (e_end < cells.size() && (L < 2 || same_prefix(cells[i], cells[e_end], L - 2))) ++e_end;
+    const int kl = oth[L - 1];
+    for (size_t g = i; g < e_end;) {
       const int bn = cells[g].beta[n];
       size_t h = g;
-      const int kl = oth[L - 1];
-      o << "      { double t = G[" << cells[h].lin << "] * " << u(kl, cells[h].beta[kl]) << ";";
-      for (++h; h < e && cells[h].beta[n] == bn; ++h)
-        o << " t = fma(G[" << cells[h].lin << "], " << u(kl, cells[h].beta[kl]) << ", t);";
-      if (L >= 2) o << " d" << bn << " = fma(w" << (L - 2) << ", t, d" << bn << "); }\n";
-      else o << " d" << bn << " += t; }\n";
+      o << "      { double g = G[" << cells[h].lin << "]; double t0 = g * " << u(kl, cells[h].beta[kl]) << "e0, t1 = g * "
+        << u(kl, cells[h].beta[kl]) << "e1;";
+      for (++h; h < e_end && cells[h].beta[n] == bn; ++h)
+        o << " g = G[" << cells[h].lin << "]; t0 = fma(g, " << u(kl, cells[h].beta[kl]) << "e0, t0); t1 = fma(g, "
+          << u(kl, cells[h].beta[kl]) << "e1, t1);";
+      if (L >= 2)
+        o << " d" << bn << "e0 = fma(w" << (L - 2) << "e0, t0, d" << bn << "e0); d" << bn << "e1 = fma(w" << (L - 2)
+          << "e1, t1, d" << bn << "e1); }\n";
+      else
+        o << " d" << bn << "e0 += t0; d" << bn << "e1 += t1; }\n";
       g = h;
     }
     for (int q = 0; q + 1 < L; ++q) o << "    }\n";
-    i = e;
+    i = e_end;
   }
-  for (int j = 0; j < c.ranks[n]; ++j) o << "    a.out[" << j << "ull * a.stride + t] = d" << j << ";\n";
-  o << "  }\n}\n";
+  for (int j = 0; j < c.ranks[n]; ++j) o << "    a.out[" << j << "ull * a.stride + t0] = d" << j << "e0;\n";
+  o << "    if (t1 != t0) {\n";
+  for (int j = 0; j < c.ranks[n]; ++j) o << "      a.out[" << j << "ull * a.stride + t1] = d" << j << "e1;\n";
+  o << "    }\n  }\n}\n";
 }
 
 std::string gen_source(const Ctx& c) {
@@ -255,6 +272,17 @@ std::vector<char> nvrtc_compile(const std::string& src, const char* name) {
   std::vector<char> cubin(sz);
   nv.cubin(prog, cubin.data());
   nv.destroy(&prog);
+  if (const char* dir = getenv("VEST_NVRTC_DUMP")) {  // inspection: source + cubin (cuobjdump -sass)
+    const std::string base = std::string(dir) + "/" + name;
+    if (FILE* f = fopen((base + ".src").c_str(), "w")) {
+      fwrite(src.data(), 1, src.size(), f);
+      fclose(f);
+    }
+    if (FILE* f = fopen((base + ".cubin").c_str(), "wb")) {
+      fwrite(cubin.data(), 1, cubin.size(), f);
+      fclose(f);
+    }
+  }
   return cubin;
 }
 
@@ -293,7 +321,7 @@ void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
   a.stride = n;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8);
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 511) / 512, (uint64_t)sms * 4);
   void* args[] = {&a};
   check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->k[mode]), dim3(grid), dim3(256), args, 0, c.stream),
         "sparse delta launch");
