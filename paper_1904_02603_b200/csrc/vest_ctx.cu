@@ -308,6 +308,28 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
     if (!hchunks.empty())
       check(cudaMemcpy(md.d_heavy_chunks, hchunks.data(), hchunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice),
             "heavy chunks");
+    {  // tiny rows (light, <= kTinyRow entries) sorted by length; the rest of the chunks
+      std::vector<std::pair<uint32_t, uint32_t>> tiny;
+      std::vector<Chunk> big;
+      for (const Chunk& ch : chunks) {
+        if (ch.slot == kLight && ch.end - ch.beg <= kTinyRow) tiny.push_back({ch.end - ch.beg, ch.row});
+        else big.push_back(ch);
+      }
+      std::stable_sort(tiny.begin(), tiny.end(),
+                       [](const std::pair<uint32_t, uint32_t>& x, const std::pair<uint32_t, uint32_t>& y) {
+                         return x.first < y.first;
+                       });
+      std::vector<uint32_t> trows(tiny.size());
+      for (size_t q = 0; q < tiny.size(); ++q) trows[q] = tiny[q].second;
+      md.ntiny = (uint32_t)trows.size();
+      md.nchunks_big = (uint32_t)big.size();
+      md.d_tiny = static_cast<uint32_t*>(dalloc(c, std::max<size_t>(1, trows.size()) * 4));
+      md.d_chunks_big = static_cast<Chunk*>(dalloc(c, std::max<size_t>(1, big.size()) * sizeof(Chunk)));
+      if (!trows.empty())
+        check(cudaMemcpy(md.d_tiny, trows.data(), trows.size() * 4, cudaMemcpyHostToDevice), "tiny rows");
+      if (!big.empty())
+        check(cudaMemcpy(md.d_chunks_big, big.data(), big.size() * sizeof(Chunk), cudaMemcpyHostToDevice), "big");
+    }
     md.nchunks = (uint32_t)chunks.size();
     md.nheavy = (uint32_t)heavy.size();
     md.nslots = slot;
@@ -326,6 +348,15 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
 }
 
 // --------------------------------------------------------------- hot path --
+// VEST_TINY_ROWS=0: short rows through the warp-per-chunk kernel (A/B timing)
+static bool tiny_rows_off() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_TINY_ROWS");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+
 static RowPassArgs row_args(Ctx& c, int mode) {
   RowPassArgs a{};
   a.m = c.model_view();
@@ -389,7 +420,18 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
   }
   {
     ProfScope ps(c, fuse ? kProfFactorFused : kProfFactor);
-    check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
+    // short rows of skewed modes lane-per-row (the fused mode keeps them in
+    // the chunk kernel, which also writes their residuals)
+    const bool tiny = !fuse && c.ops && !c.force_generic && c.ops->rowtiny && mdd.ntiny > 0 && !tiny_rows_off();
+    if (tiny) {
+      RowPassArgs bg = a;
+      bg.csf.chunks = mdd.d_chunks_big;
+      bg.csf.nchunks = mdd.nchunks_big;
+      check(run_rows(c, bg, kStats, bg.csf.nchunks), "factor update");
+      check(c.ops->rowtiny(a, mdd.d_tiny, mdd.ntiny, c.stream), "factor update (short rows)");
+    } else {
+      check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
+    }
     if (reg == 1) l1_empty_rows(c, mode, lambda);
   }
   c.r_valid = false;

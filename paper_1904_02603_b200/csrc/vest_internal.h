@@ -28,6 +28,7 @@ namespace vest {
 
 constexpr uint32_t kLight = 0xFFFFFFFFu;
 constexpr uint32_t kChunk = 2048;  // max entries per work item
+constexpr uint32_t kTinyRow = 32;  // rows this short run lane-per-row (skewed modes' long tails)
 
 struct Chunk {
   uint32_t row, beg, end, slot;  // [beg, end) in the mode's CSF; slot = heavy partial index or kLight
@@ -88,6 +89,11 @@ struct ModeData {
   uint32_t* d_empty = nullptr;  // rows with no entries
   Chunk* d_heavy_chunks = nullptr;  // the chunks of heavy rows (residual pass after their solve)
   uint32_t nchunks = 0, nheavy = 0, nslots = 0, nempty = 0, nheavy_chunks = 0;
+  // rows with <= kTinyRow entries, sorted by length (lane-per-row statistics
+  // kernel), and the chunk list without them (warp-per-chunk kernel)
+  uint32_t* d_tiny = nullptr;
+  Chunk* d_chunks_big = nullptr;
+  uint32_t ntiny = 0, nchunks_big = 0;
   std::vector<uint64_t> h_offsets;
 };
 
@@ -102,6 +108,7 @@ struct ShapeOps {
   cudaError_t (*rowpass)(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s);
   cudaError_t (*coo_recon)(const DevModel& m, const uint32_t* coords, const double* values,
                            uint64_t n, double* out, double* partial, int nblocks, cudaStream_t s);
+  cudaError_t (*rowtiny)(const RowPassArgs& a, const uint32_t* rows, uint32_t nrows, cudaStream_t s);
 };
 
 struct ProfEvent {

@@ -625,6 +625,89 @@ __global__ void __launch_bounds__(256) k_heavy(RowPassArgs a, int kind) {
             a.m.fmask[mode] + (size_t)h.row * J, lane);
 }
 
+// -------------------------------------------------------------- short rows --
+// Rows with <= kTinyRow entries (the long tails of Zipf-distributed modes:
+// config 3's mode 0 has ~940k such rows holding 10 % of the entries) waste most
+// of a warp-per-chunk round.  Here one LANE owns one row: it contracts its
+// entries one after another (the single-entry static form; lanes of a warp
+// run different rows in lockstep, rows sorted by length so a warp's lanes
+// have (nearly) equal trip counts), accumulates the row statistics in its own
+// shared-memory slot and solves the row itself -- updates.hpp:61-151 for one
+// row per thread.
+template <class P>
+__global__ void __launch_bounds__(128) k_rowpass_tiny(RowPassArgs a, P pol, const uint32_t* __restrict__ rows,
+                                                      uint32_t nrows) {
+  constexpr int J = P::JN;
+  constexpr int NG = J * (J + 1) / 2, NA = NG + J;
+  constexpr int NAs = NA | 1;  // odd stride: conflict-free per-lane slots
+  extern __shared__ double tsm[];
+  double* g = tsm + threadIdx.x * NAs;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+#pragma unroll
+  for (int q = 0; q < NA; ++q) g[q] = 0.0;
+  const int mode = pol.mode();
+  const uint32_t row = __ldg(rows + t);
+  const uint32_t b = (uint32_t)__ldg(a.csf.offsets + row), e = (uint32_t)__ldg(a.csf.offsets + row + 1);
+  for (uint32_t pos = b; pos < e; ++pos) {
+    double d[P::MAXJ];
+    pol.entry1(a.m, a.csf, pos, d);
+    const double x = __ldg(a.csf.val + pos);
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < J; ++i)
+#pragma unroll
+      for (int j = i; j < J; ++j) g[q++] += d[i] * d[j];
+#pragma unroll
+    for (int i = 0; i < J; ++i) g[NG + i] += x * d[i];
+  }
+  // the row's Gauss-Seidel solve (update_factor_row_lf / _l1), this lane alone
+  double* arow = a.m.factor[mode] + (size_t)row * a.m.ld[mode];
+  const uint8_t* mask = a.m.fmask[mode] + (size_t)row * J;
+  double v[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) v[j] = arow[j];
+  auto gram = [&](int i, int j) {  // packed upper triangle
+    const int lo = i < j ? i : j, hi = i < j ? j : i;
+    return g[lo * J - lo * (lo - 1) / 2 + (hi - lo)];
+  };
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    if (mask[j]) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < J; ++i)
+      if (i != j) s = fma(gram(j, i), v[i], s);
+    const double lin = g[NG + j] - s;
+    const double gjj = gram(j, j);
+    if (a.reg == 0) {
+      const double den = gjj + a.lambda;
+      if (den != 0.0) v[j] = lin / den;
+    } else {
+      const double gg = -2.0 * lin, dd = 2.0 * gjj;
+      if (dd == 0.0) {
+        if (fabs(gg) <= a.lambda) v[j] = 0.0;
+      } else {
+        v[j] = gg > a.lambda ? (a.lambda - gg) / dd : (gg < -a.lambda ? -(a.lambda + gg) / dd : 0.0);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) arow[j] = v[j];
+}
+
+template <class P>
+cudaError_t launch_tiny(const RowPassArgs& a, const uint32_t* rows, uint32_t nrows, cudaStream_t s, P pol) {
+  if (nrows == 0) return cudaSuccess;
+  constexpr int J = P::JN;
+  constexpr int NAs = (J * (J + 1) / 2 + J) | 1;
+  const size_t sm = (size_t)128 * NAs * sizeof(double);
+  cudaFuncSetAttribute(k_rowpass_tiny<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_rowpass_tiny<P><<<(nrows + 127) / 128, 128, sm, s>>>(a, pol, rows, nrows);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // --------------------------------------------- statistics from a given delta --
 // The row pass when delta was produced elsewhere (the mask-specialised
 // contraction of vest_sparse.cu): delta[j][pos - p0] SoA.  One warp per
@@ -874,6 +957,16 @@ cudaError_t static_mode(const RowPassArgs& a, int kind, uint32_t nchunks, cudaSt
 }
 
 template <class S, int M = 0>
+cudaError_t static_rowtiny(const RowPassArgs& a, const uint32_t* rows, uint32_t nrows, cudaStream_t s) {
+  if constexpr (M < S::N) {
+    if (a.mode == M) return launch_tiny(a, rows, nrows, s, StaticPolicy<S, M>{});
+    return static_rowtiny<S, M + 1>(a, rows, nrows, s);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
+template <class S, int M = 0>
 cudaError_t static_rowpass(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s) {
   if constexpr (M < S::N) {
     if (a.mode == M) return static_mode<S, M>(a, kind, nchunks, s);
@@ -899,6 +992,7 @@ constexpr ShapeOps make_ops() {
   for (int k = 0; k < (int)sizeof...(Js); ++k) o.J[k] = js[k];
   o.rowpass = &static_rowpass<SShape<Js...>>;
   o.coo_recon = &static_coo<SShape<Js...>>;
+  o.rowtiny = &static_rowtiny<SShape<Js...>>;
   return o;
 }
 

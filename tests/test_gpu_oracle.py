@@ -172,6 +172,15 @@ def test_heavy_rows_split_across_chunks(ranks):
     phases([3, 60, 60], ranks, 9000, 19, 1, 0.05, iters=1)
 
 
+@pytest.mark.parametrize("dims,ranks", [([400, 30, 20], [5, 5, 5]), ([300, 40, 30], [10, 10, 5]),
+                                        ([200, 20, 18, 16], [8, 8, 8, 8])])
+def test_short_rows_lane_per_row(dims, ranks):
+    # mode-0 rows hold ~1-40 entries: the lane-per-row statistics kernel
+    # (k_rowpass_tiny) for rows <= 32 entries, the chunk kernel for the rest
+    phases(dims, ranks, 5000, 51, 0, 0.01, iters=2, mask_frac=0.1)
+    phases(dims, ranks, 5000, 52, 1, 0.05, iters=1, mask_frac=0.1)
+
+
 def test_skewed_rows():
     phases([12, 40, 30], [5, 5, 5], 8000, 20, 0, 0.01, iters=1, skew=1.6)
 
