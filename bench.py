@@ -419,6 +419,48 @@ CONFIGS = {
 }
 
 
+def run_shard_emulation(cfg_id, world, iters):
+    """Per-GPU device time of one rank's share of the sweep at `world` GPUs
+    (ranks 0 and world-1 of the nnz-balanced row partition, exchanges replaced
+    by no-ops: sharded.NullComm) -- the compute side of the scaling estimate on
+    one B200.  The exchange volume per iteration is reported beside it."""
+    import torch
+    from paper_1904_02603_b200 import sharded as sh
+    from paper_1904_02603_b200 import sparsetuck as st
+
+    c = CONFIGS[cfg_id]
+    coords, vals = synth(c["dims"], c["nnz"], 1000 + cfg_id, c["values_kind"], c["zipf"])
+    x = st.SparseTensor(c["dims"], coords, vals)
+    if c.get("sweep"):
+        x, _ = st.split_train_test(x, 0.1, 2026)
+    m = st.init_random(c["dims"], c["ranks"], 7)
+    if c["core_keep"] < 1.0:
+        rng = np.random.default_rng(44)
+        mask = (rng.random(m.core.shape) >= c["core_keep"]).astype(np.uint8)
+        m.core[mask == 1] = 0.0
+        m.core_mask = mask
+    bounds = sh.partition(x, world)
+    out = {"config": cfg_id, "world": world, "ranks": {}}
+    for rank in sorted({0, world - 1}):
+        dev = sh.ShardDevice(x, c["ranks"], rank, world, sh.NullComm(), bounds=bounds)
+        dev.set_model(m)
+        stream = torch.cuda.ExternalStream(dev.stream())
+        times = []
+        for t in range(iters + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dev.cd_iteration(0, c["lam"])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        out["ranks"][rank] = {"ms_per_iter": statistics.median(times[1:]), "local_nnz_last_mode":
+                              dev.local_nnz(len(c["dims"]) - 1)}
+        dev.close()
+    # exchanges per iteration: every factor once (row all-gather) + block statistics
+    out["allgather_bytes_per_iter"] = int(sum(int(d) * int(r) * 8 for d, r in zip(c["dims"], c["ranks"])))
+    print(json.dumps(out), flush=True)
+
+
 def run_config(cfg_id, iters_override=None):
     """Full-size run of BASELINE config `cfg_id` on one GPU: per-iteration device
     time (CUDA events on the library stream), prune events timed separately."""
@@ -487,6 +529,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=0, help="run BASELINE config 1..5 at full size (diagnostic)")
     ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--shard-emulate", type=int, default=0,
+                    help="with --config: per-GPU device time of one rank's share at W GPUs (no exchanges)")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
@@ -496,6 +540,9 @@ def main():
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
+    if args.config and args.shard_emulate:
+        run_shard_emulation(args.config, args.shard_emulate, args.iters or 3)
+        return
     if args.config:
         run_config(args.config, args.iters or None)
         return

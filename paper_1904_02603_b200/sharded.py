@@ -178,6 +178,23 @@ class TorchComm:
         return VestComm(None, ALLREDUCE(ar), ALLGATHER(ag))
 
 
+# ------------------------------------------------ timing-only null exchange --
+class NullComm:
+    """Hooks that exchange nothing: one rank's shard context runs its own share
+    of the sweep alone (bench.py --shard-emulate W, per-GPU device time at W
+    GPUs).  Results are NOT the sharded model's (nothing is summed/gathered);
+    the device work per iteration is the rank's -- timing only."""
+
+    def hooks(self, dev: "ShardDevice") -> VestComm:
+        def ar(user, p, n, stream):
+            return 0
+
+        def ag(user, mode, base, ld, stream):
+            return 0
+
+        return VestComm(None, ALLREDUCE(ar), ALLGATHER(ag))
+
+
 # --------------------------------------------------- one-GPU emulated group --
 class LocalGroup:
     """W shard contexts of one process on one GPU, driven by W threads.  Each
