@@ -21,6 +21,7 @@
 #include "sparsetuck/model_io.hpp"
 #include "sparsetuck/pruning.hpp"
 #include "sparsetuck/sparse_tensor.hpp"
+#include "sparsetuck/synthetic.hpp"
 #include "sparsetuck/trainer.hpp"
 #include "sparsetuck/tucker_model.hpp"
 #include "sparsetuck/updates.hpp"
@@ -367,6 +368,30 @@ int vr_load_model(const char* dir, int* order, uint64_t* dims, uint64_t* ranks, 
     for (std::size_t n = 0; n < m.order(); ++n) {
       if (factors && factors[n]) std::memcpy(factors[n], m.factors[n].data(), m.factors[n].size() * sizeof(double));
       if (factor_masks && factor_masks[n]) std::memcpy(factor_masks[n], m.factor_masks[n].data(), m.factor_masks[n].size());
+    }
+  });
+}
+
+// gen_synthetic (synthetic.hpp:105-155): planted model + observations
+int vr_gen_synthetic(int order, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz, double density,
+                     double noise, uint64_t seed, uint32_t* coords, double* values, double* core, uint8_t* core_mask,
+                     double* const* factors, uint8_t* const* factor_masks) {
+  return guard([&] {
+    SyntheticSpec spec;
+    spec.dims.assign(dims, dims + order);
+    spec.ranks.assign(ranks, ranks + order);
+    spec.nnz = nnz;
+    spec.factor_density = density;
+    spec.noise_std = noise;
+    spec.seed = seed;
+    const SyntheticData d = gen_synthetic(spec);
+    std::memcpy(coords, d.tensor.coords.data(), d.tensor.coords.size() * sizeof(Coord));
+    std::memcpy(values, d.tensor.values.data(), d.tensor.values.size() * sizeof(double));
+    std::memcpy(core, d.truth.core.data(), d.truth.core.size() * sizeof(double));
+    std::memcpy(core_mask, d.truth.core_mask.data(), d.truth.core_mask.size());
+    for (int n = 0; n < order; ++n) {
+      std::memcpy(factors[n], d.truth.factors[n].data(), d.truth.factors[n].size() * sizeof(double));
+      std::memcpy(factor_masks[n], d.truth.factor_masks[n].data(), d.truth.factor_masks[n].size());
     }
   });
 }

@@ -51,6 +51,23 @@ def test_sparse_delta_source_compiles_for_sm100a(L, ranks, keep):
     assert out[0] > 1000  # a cubin
 
 
+def test_cli_builds_and_reports_usage_errors():
+    """tools/sparsetuck_b200 (the reference CLI surface) builds against the C++
+    mirror; argument errors fail before any device work."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools")], check=True)
+    exe = os.path.join(ROOT, "tools", "sparsetuck_b200")
+    r = subprocess.run([exe, "--help"], capture_output=True, text=True)
+    assert r.returncode == 0 and "decompose" in r.stdout and "synth" in r.stdout
+    for args in (["decompose", "--input", "x.coo"], ["predict", "--model-dir", "d"], ["bogus"],
+                 ["decompose", "--input", "x", "--ranks", "2,2", "--reg", "l2"], ["evaluate", "--nope", "1"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True)
+        assert r.returncode != 0, args
+    r = subprocess.run([exe, "evaluate", "--model-dir", "/nonexistent", "--input", "x"], capture_output=True,
+                       text=True)
+    assert r.returncode == 1 and r.stderr.startswith("error: ")
+
+
 def test_init_random_host_matches_reference(L):
     g = golden("init_random")
     for k in range(int(g["ncases"])):
