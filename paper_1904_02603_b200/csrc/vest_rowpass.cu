@@ -634,14 +634,21 @@ __global__ void __launch_bounds__(256) k_heavy(RowPassArgs a, int kind) {
 // have (nearly) equal trip counts), accumulates the row statistics in its own
 // shared-memory slot and solves the row itself -- updates.hpp:61-151 for one
 // row per thread.
+#ifndef VEST_TINY_REG
+#define VEST_TINY_REG 1  // statistics in registers (J(J+1)/2 + J doubles) instead of a shared-memory slot
+#endif
 template <class P>
 __global__ void __launch_bounds__(128) k_rowpass_tiny(RowPassArgs a, P pol, const uint32_t* __restrict__ rows,
                                                       uint32_t nrows) {
   constexpr int J = P::JN;
   constexpr int NG = J * (J + 1) / 2, NA = NG + J;
   constexpr int NAs = NA | 1;  // odd stride: conflict-free per-lane slots
+#if VEST_TINY_REG
+  double g[NA];
+#else
   extern __shared__ double tsm[];
   double* g = tsm + threadIdx.x * NAs;
+#endif
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
 #pragma unroll
@@ -667,7 +674,7 @@ __global__ void __launch_bounds__(128) k_rowpass_tiny(RowPassArgs a, P pol, cons
   double v[J];
 #pragma unroll
   for (int j = 0; j < J; ++j) v[j] = arow[j];
-  auto gram = [&](int i, int j) {  // packed upper triangle
+  auto gram = [&](int i, int j) -> double {  // packed upper triangle (compile-time indices when unrolled)
     const int lo = i < j ? i : j, hi = i < j ? j : i;
     return g[lo * J - lo * (lo - 1) / 2 + (hi - lo)];
   };
@@ -701,7 +708,7 @@ cudaError_t launch_tiny(const RowPassArgs& a, const uint32_t* rows, uint32_t nro
   if (nrows == 0) return cudaSuccess;
   constexpr int J = P::JN;
   constexpr int NAs = (J * (J + 1) / 2 + J) | 1;
-  const size_t sm = (size_t)128 * NAs * sizeof(double);
+  const size_t sm = VEST_TINY_REG ? 0 : (size_t)128 * NAs * sizeof(double);
   cudaFuncSetAttribute(k_rowpass_tiny<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_rowpass_tiny<P><<<(nrows + 127) / 128, 128, sm, s>>>(a, pol, rows, nrows);
   count_launch();
