@@ -72,13 +72,15 @@ int vest_ctx_set_core_block(vest_ctx* ctx, int fibers);
 /* Mask-specialised delta contraction for pruned cores (NVRTC-compiled for the
  * current core mask, recompiled after prunes; replaces the dense contraction
  * of the factor-row update, updates.hpp:35-52 skipping zero cells):
- * -1 auto (unmasked cells < |G| / 4 on rank-specialised shapes), 0 off, 1 on.
- * vest_ctx_sparse_delta_active reports whether the next update uses it. */
+ * -1 auto (unmasked cells < |G| / 4 on rank-specialised shapes, from the
+ * second sweep with the same core mask on), 0 off, 1 on.
+ * vest_ctx_sparse_delta_active reports whether the current mask qualifies. */
 int vest_ctx_set_sparse_delta(vest_ctx* ctx, int mode);
 int vest_ctx_sparse_delta_active(const vest_ctx* ctx);
 /* Plan-specialised core-sweep passes for the general block plans (straight-line
  * passes generated per core mask, NVRTC-compiled): -1 auto (rank-specialised
- * shapes), 0 off (table-driven kernel), 1 on. */
+ * shapes, from the second sweep with the same core mask on), 0 off
+ * (table-driven kernel), 1 on. */
 int vest_ctx_set_core_gen(vest_ctx* ctx, int mode);
 /* Host-only: generate and NVRTC-compile that contraction for ranks and a core
  * mask (no GPU needed); *cubin_bytes = size of the sm_100a cubin. */

@@ -945,7 +945,7 @@ Blocks plan_general(const Ctx& c, int F) {
 
 bool use_core_gen(const Ctx& c) {
   if (c.core_gen_mode >= 0) return c.core_gen_mode == 1;
-  return c.ops && !c.force_generic && c.core_block == 0 && nvrtc_available();
+  return c.ops && !c.force_generic && c.core_block == 0 && nvrtc_available() && c.mask_sweeps >= 2;
 }
 
 std::vector<std::vector<uint32_t>> block_lists(const Blocks& b) {

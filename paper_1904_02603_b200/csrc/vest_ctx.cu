@@ -371,6 +371,7 @@ static cudaError_t run_rows(Ctx& c, const RowPassArgs& a, int kind, uint32_t nch
 }
 
 void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resid) {
+  if (mode == 0) note_sweep(c);
   RowPassArgs a = row_args(c, mode);
   const int J = c.ranks[mode];
   a.reg = reg;
@@ -932,7 +933,7 @@ int vest_ctx_set_core_gen(vest_ctx* h, int mode) {
   h->c.core_gen_mode = mode < 0 ? -1 : (mode ? 1 : 0);
   return VEST_OK;
 }
-int vest_ctx_sparse_delta_active(const vest_ctx* h) { return h && sparse_delta_enabled(h->c) ? 1 : 0; }
+int vest_ctx_sparse_delta_active(const vest_ctx* h) { return h && sparse_delta_eligible(h->c) ? 1 : 0; }
 int vest_sparse_compile_check(int order, const uint64_t* ranks, const uint8_t* core_mask, uint64_t* cubin_bytes) {
   return guard([&] {
     if (order < 2 || order > VEST_MAXN) throw ArgError{"order must be in [2, 8]"};

@@ -185,6 +185,11 @@ struct Ctx {
   SparseState* sparse = nullptr;
   CoreGenState* core_gen = nullptr;
   int core_gen_mode = -1;          // plan-specialised core passes: -1 auto, 0 off, 1 on
+  // sweeps run with the current core mask (auto mode compiles the mask's
+  // kernels from the second one on: a mask pruned every iteration never pays
+  // an NVRTC compile, a stable one pays it once)
+  uint64_t mask_key = 0;
+  int mask_sweeps = 0;
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
   double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
   uint32_t* d_hstab = nullptr;     size_t hstab_cap = 0;    // live-cell Gram entry table (k_core_hsample)
@@ -225,6 +230,8 @@ void sync_const_core(Ctx& c);  // copy d_core into every TU's constant-bank core
 cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
                                  uint64_t dstride, uint64_t p0, cudaStream_t s);
 bool sparse_delta_enabled(const Ctx& c);
+bool sparse_delta_eligible(const Ctx& c);
+void note_sweep(Ctx& c);  // a factor sweep starts (mode 0): count sweeps per core mask
 void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out);
 void sparse_free(Ctx& c);
 std::vector<char> nvrtc_compile(const std::string& src, const char* name);

@@ -235,12 +235,17 @@ bool nvrtc_available() {
 
 // Live-cell threshold: the generated contraction costs ~2 FMA per unmasked
 // cell against >= |G| for the dense factorised one.
-bool sparse_delta_enabled(const Ctx& c) {
+static int sparse_mode(const Ctx& c) {
   static const int env = [] {  // VEST_SPARSE_DELTA=0/1 overrides "auto" (A/B timing)
     const char* e = getenv("VEST_SPARSE_DELTA");
     return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
   }();
-  const int mode = c.sparse_delta >= 0 ? c.sparse_delta : env;
+  return c.sparse_delta >= 0 ? c.sparse_delta : env;
+}
+
+// The mask qualifies (or the path is forced on).
+bool sparse_delta_eligible(const Ctx& c) {
+  const int mode = sparse_mode(c);
   if (mode == 0 || c.N < 2) return false;
   for (int k = 0; k < c.N; ++k)
     if (c.ranks[k] > 15) return false;  // the statistics kernel's DMMA tile
@@ -249,6 +254,22 @@ bool sparse_delta_enabled(const Ctx& c) {
   long live = 0;
   for (uint8_t m : c.h_core_mask) live += !m;
   return 4 * live < c.G;
+}
+
+// ... and, in auto mode, the mask has outlived one sweep.
+bool sparse_delta_enabled(const Ctx& c) {
+  if (!sparse_delta_eligible(c)) return false;
+  return sparse_mode(c) == 1 || c.mask_sweeps >= 2;
+}
+
+void note_sweep(Ctx& c) {
+  const uint64_t key = mask_key(c);
+  if (key == c.mask_key && c.mask_sweeps > 0) {
+    ++c.mask_sweeps;
+  } else {
+    c.mask_key = key;
+    c.mask_sweeps = 1;
+  }
 }
 
 std::vector<char> nvrtc_compile(const std::string& src, const char* name) {
