@@ -521,7 +521,7 @@ def run_config(cfg_id, iters_override=None):
             "device_gb": dev.device_bytes() / 1e9, "kernel_families_ms": fams}
     if c.get("sweep"):
         p0 = time.perf_counter()
-        sweep = st.auto_search(x, test, dev.get_model(), [round(0.1 * k, 1) for k in range(1, 10)])
+        sweep = st.auto_search(x, test, dev.get_model(), [round(0.1 * k, 1) for k in range(1, 10)], dev=dev)
         line["sweep"] = [{"rate": r.rate, "train_re": r.train_re, "test_re": r.test_re, "sparsity": r.sparsity}
                          for r in sweep]
         line["sweep_s"] = time.perf_counter() - p0

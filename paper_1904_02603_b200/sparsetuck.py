@@ -809,21 +809,27 @@ class RateResult:
 
 
 def auto_search(x_train: SparseTensor, x_test: SparseTensor, model: TuckerModel, rates: Sequence[float],
-                device: int = 0) -> list:
+                device: int = 0, dev: Optional["Device"] = None) -> list:
     """Prune-rate sweep (BASELINE config 5; SURVEY App. C option (i)): for each
     rate, start from the trained model, score responsibilities on the training
     entries (pruning.hpp:181-191), prune_step(rate) (pruning.hpp:234-247) and
     evaluate the relative error on the training and held-out entries
-    (tucker_model.hpp:186-188, trainer.hpp:188-190).  Device-resident: the
-    trained model is uploaded once per rate; the evaluation is the inner loop."""
-    dev = Device(x_train, model.ranks, device)
+    (tucker_model.hpp:186-188, trainer.hpp:188-190).  Device-resident: every
+    rate starts from the same model, so its responsibility table is scored
+    once and reused; the model is re-uploaded per rate; the evaluation is the
+    inner loop.  `dev` reuses a context already built on x_train."""
+    own = dev is None
+    if own:
+        dev = Device(x_train, model.ranks, device)
+    dev.set_model(model)
+    table = dev.compute_responsibilities()
     out = []
     for pr in rates:
         dev.set_model(model)
-        dev.compute_responsibilities(want=False)
-        counts = dev.prune_step(float(pr))
+        counts = dev.prune_step(float(pr), table)
         train_re = dev.compute_residuals().re
         test_re = dev.evaluate(x_test)
         out.append(RateResult(float(pr), counts, dev.sparsity()[0], train_re, test_re))
-    dev.close()
+    if own:
+        dev.close()
     return out
