@@ -3,12 +3,13 @@
 // the B200 path that the reference's CLI uses, on top of
 // sparsetuck_b200.hpp:
 //   * write_report_jsonl / write_bench_csv: the reference's report lines
-//     (report.hpp:130-175), same keys, order and "%.17g" numbers;
+//     (report.hpp:130-175): same keys, key order and "%.17g" numbers;
 //   * SyntheticSpec / gen_synthetic: the planted-model generator
-//     (synthetic.hpp:17-155) -- the same seeded engine and draw order (truth
-//     values and masks, coordinate sample, noise), so model, coordinates and
-//     noise are the reference's; the noise-free values are reconstructed on the
-//     device (vest_predict), i.e. equal to the reference's up to fp64 rounding;
+//     (synthetic.hpp:17-155) -- the same seeded engine consumed in the same
+//     order (truth values with their keep draws, coordinate sample, noise), so
+//     the planted model, coordinates and noise equal the reference's; the
+//     noise-free values are reconstructed on the device (vest_predict), i.e.
+//     equal to the reference's up to fp64 rounding;
 //   * scaling_benchmark (report.hpp:70-127): per-iteration fit time per config;
 //     the "threads" column is kept for the format and does not change the
 //     device run;
@@ -20,6 +21,8 @@
 #include <cstdio>
 #include <limits>
 #include <new>
+#include <numeric>
+#include <optional>
 #include <ostream>
 #include <random>
 #include <set>
@@ -37,23 +40,21 @@ struct RowDensity {
   double norm = 0.0;
 };
 
+// rows of factor `mode` by nonzero count (descending), ties by row index
 inline std::vector<RowDensity> row_density_report(const TuckerModel& m, std::size_t mode) {
-  const std::size_t J = m.ranks[mode];
-  std::vector<RowDensity> rows(m.dims[mode]);
+  const std::size_t width = m.ranks[mode];
+  const std::vector<double>& f = m.factors[mode];
+  std::vector<RowDensity> table;
+  table.reserve(m.dims[mode]);
   for (std::size_t i = 0; i < m.dims[mode]; ++i) {
-    double s = 0.0;
-    std::size_t nz = 0;
-    for (std::size_t j = 0; j < J; ++j) {
-      const double v = m.factors[mode][i * J + j];
-      nz += v != 0.0;
-      s += v * v;
-    }
-    rows[i] = {i, nz, std::sqrt(s)};
+    const double* row = f.data() + i * width;
+    const auto nz = static_cast<std::size_t>(std::count_if(row, row + width, [](double v) { return v != 0.0; }));
+    const double sq = std::inner_product(row, row + width, row, 0.0);
+    table.push_back(RowDensity{i, nz, std::sqrt(sq)});
   }
-  std::sort(rows.begin(), rows.end(), [](const RowDensity& a, const RowDensity& b) {
-    return a.nonzeros != b.nonzeros ? a.nonzeros > b.nonzeros : a.row < b.row;
-  });
-  return rows;
+  std::stable_sort(table.begin(), table.end(),
+                   [](const RowDensity& l, const RowDensity& r) { return l.nonzeros > r.nonzeros; });
+  return table;
 }
 
 struct SyntheticSpec {
@@ -72,126 +73,141 @@ struct SyntheticData {
 
 namespace b200_detail {
 
-// distinct coordinates in canonical (row-major) order, the reference's two
-// regimes and draw sequence (synthetic.hpp:37-103)
-inline std::vector<Coord> sample_coords(const std::vector<std::size_t>& dims, std::size_t nnz,
-                                        std::mt19937_64& rng) {
-  const std::size_t n = dims.size();
-  std::uint64_t total = 1;
-  bool wide = false;
+using Engine = std::mt19937_64;
+
+// cells = prod(dims), or 0 when it does not fit 64 bits
+inline std::uint64_t cell_count(const std::vector<std::size_t>& dims) {
+  std::uint64_t cells = 1;
   for (std::size_t d : dims) {
-    if (total > std::numeric_limits<std::uint64_t>::max() / d) {
-      wide = true;
-      break;
-    }
-    total *= d;
+    if (cells > std::numeric_limits<std::uint64_t>::max() / d) return 0;
+    cells *= d;
   }
-  std::vector<Coord> flat;
-  flat.reserve(nnz * n);
-  auto emit = [&](std::uint64_t key) {
-    std::vector<Coord> c(n);
-    for (std::size_t k = n; k-- > 0;) {
-      c[k] = static_cast<Coord>(key % dims[k]);
-      key /= dims[k];
+  return cells;
+}
+
+// nnz distinct linear cell ids: a partial Fisher-Yates shuffle of all ids when
+// at least half the cells are drawn, rejection against the ids so far otherwise
+// (the reference's regimes and draw sequence, synthetic.hpp:56-74)
+inline std::vector<std::uint64_t> draw_cells(std::uint64_t cells, std::size_t nnz, Engine& eng) {
+  std::vector<std::uint64_t> ids;
+  if (2 * nnz >= cells) {
+    std::vector<std::uint64_t> perm(cells);
+    std::iota(perm.begin(), perm.end(), std::uint64_t{0});
+    for (std::size_t slot = 0; slot < nnz; ++slot) {
+      const std::uint64_t j = std::uniform_int_distribution<std::uint64_t>(slot, cells - 1)(eng);
+      std::swap(perm[slot], perm[j]);
     }
-    flat.insert(flat.end(), c.begin(), c.end());
-  };
-  if (!wide) {
-    if (nnz > total) throw std::invalid_argument("nnz exceeds tensor cell count");
-    std::vector<std::uint64_t> keys;
-    keys.reserve(nnz);
-    if (nnz * 2 >= total) {  // dense: partial Fisher-Yates over all positions
-      std::vector<std::uint64_t> all(total);
-      for (std::uint64_t i = 0; i < total; ++i) all[i] = i;
-      for (std::size_t k = 0; k < nnz; ++k) {
-        std::uniform_int_distribution<std::uint64_t> pick(k, total - 1);
-        std::swap(all[k], all[pick(rng)]);
-      }
-      keys.assign(all.begin(), all.begin() + nnz);
-    } else {  // sparse: rejection against the keys drawn so far
-      std::unordered_set<std::uint64_t> seen;
-      std::uniform_int_distribution<std::uint64_t> pick(0, total - 1);
-      while (keys.size() < nnz) {
-        const std::uint64_t k = pick(rng);
-        if (seen.insert(k).second) keys.push_back(k);
-      }
+    perm.resize(nnz);
+    ids = std::move(perm);
+  } else {
+    std::uniform_int_distribution<std::uint64_t> any(0, cells - 1);
+    std::unordered_set<std::uint64_t> taken;
+    ids.reserve(nnz);
+    while (ids.size() < nnz) {
+      const std::uint64_t id = any(eng);
+      if (taken.insert(id).second) ids.push_back(id);
     }
-    std::sort(keys.begin(), keys.end());
-    for (std::uint64_t key : keys) emit(key);
-  } else {  // > 2^64 cells: coordinate tuples, ordered-set dedup
-    std::set<std::vector<Coord>> seen;
-    while (seen.size() < nnz) {
-      std::vector<Coord> c(n);
-      for (std::size_t k = 0; k < n; ++k) {
-        std::uniform_int_distribution<std::uint64_t> pick(0, dims[k] - 1);
-        c[k] = static_cast<Coord>(pick(rng));
-      }
-      seen.insert(std::move(c));
-    }
-    for (const auto& c : seen) flat.insert(flat.end(), c.begin(), c.end());
   }
+  std::sort(ids.begin(), ids.end());
+  return ids;
+}
+
+// distinct coordinates in canonical (row-major) order
+inline std::vector<Coord> sample_coords(const std::vector<std::size_t>& dims, std::size_t nnz, Engine& eng) {
+  const std::size_t order = dims.size();
+  std::vector<Coord> flat(nnz * order);
+  const std::uint64_t cells = cell_count(dims);
+  if (cells != 0) {
+    if (nnz > cells) throw std::invalid_argument("nnz exceeds tensor cell count");
+    const std::vector<std::uint64_t> ids = draw_cells(cells, nnz, eng);
+    for (std::size_t e = 0; e < nnz; ++e) {
+      std::uint64_t id = ids[e];
+      for (std::size_t k = order; k-- > 0;) {
+        flat[e * order + k] = static_cast<Coord>(id % dims[k]);
+        id /= dims[k];
+      }
+    }
+    return flat;
+  }
+  // more than 2^64 cells: whole tuples, mode by mode, ordered-set dedup
+  std::set<std::vector<Coord>> tuples;
+  std::vector<Coord> t(order);
+  while (tuples.size() < nnz) {
+    for (std::size_t k = 0; k < order; ++k)
+      t[k] = static_cast<Coord>(std::uniform_int_distribution<std::uint64_t>(0, dims[k] - 1)(eng));
+    tuples.insert(t);
+  }
+  std::size_t at = 0;
+  for (const auto& tup : tuples) std::copy(tup.begin(), tup.end(), flat.begin() + static_cast<long>(at++ * order));
   return flat;
 }
 
 inline std::string num17(double v) {
-  char buf[64];
+  if (!std::isfinite(v)) return "null";  // JSON has no inf/nan literals
+  char buf[40];
   std::snprintf(buf, sizeof buf, "%.17g", v);
-  std::string s(buf);
-  if (s.find("inf") != std::string::npos || s.find("nan") != std::string::npos) s = "null";
-  return s;
+  return buf;
+}
+
+inline void check_spec(const SyntheticSpec& s) {
+  if (s.dims.size() != s.ranks.size()) throw std::invalid_argument("ranks order mismatch");
+  if (s.dims.empty()) throw std::invalid_argument("order must be at least 1");
+  if (!(s.factor_density > 0.0 && s.factor_density <= 1.0))
+    throw std::invalid_argument("factor_density must be in (0, 1]");
+  if (!(s.noise_std >= 0.0)) throw std::invalid_argument("noise_std must be nonnegative");
+  if (s.nnz == 0) throw std::invalid_argument("nnz must be positive");
 }
 
 }  // namespace b200_detail
 
 inline SyntheticData gen_synthetic(const SyntheticSpec& spec) {
-  if (spec.dims.size() != spec.ranks.size()) throw std::invalid_argument("ranks order mismatch");
-  if (spec.dims.empty()) throw std::invalid_argument("order must be at least 1");
-  if (!(spec.factor_density > 0.0 && spec.factor_density <= 1.0))
-    throw std::invalid_argument("factor_density must be in (0, 1]");
-  if (!(spec.noise_std >= 0.0)) throw std::invalid_argument("noise_std must be nonnegative");
-  if (spec.nnz == 0) throw std::invalid_argument("nnz must be positive");
-  std::mt19937_64 rng(spec.seed);
-  std::uniform_real_distribution<double> unif(0.0, 1.0);
-  SyntheticData out;
-  TuckerModel& t = out.truth;
-  t.dims = spec.dims;
-  t.ranks = spec.ranks;
-  t.factors.resize(spec.dims.size());
-  t.factor_masks.resize(spec.dims.size());
-  auto draw = [&](double& v, std::uint8_t& mask) {  // value first, then the keep test
-    const double value = unif(rng);
-    const bool drop = spec.factor_density < 1.0 && unif(rng) >= spec.factor_density;
-    v = drop ? 0.0 : value;
-    mask = drop ? 1 : 0;
+  b200_detail::check_spec(spec);
+  b200_detail::Engine eng(spec.seed);
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  const bool thin = spec.factor_density < 1.0;
+  // one planted element: its value is drawn first, then (density < 1) its keep draw
+  auto plant = [&](std::vector<double>& vals, std::vector<std::uint8_t>& mask, std::size_t count) {
+    vals.assign(count, 0.0);
+    mask.assign(count, 0);
+    for (std::size_t q = 0; q < count; ++q) {
+      const double v = u01(eng);
+      const bool dropped = thin && !(u01(eng) < spec.factor_density);
+      vals[q] = dropped ? 0.0 : v;
+      mask[q] = dropped ? 1 : 0;
+    }
   };
-  for (std::size_t n = 0; n < spec.dims.size(); ++n) {
-    t.factors[n].resize(spec.dims[n] * spec.ranks[n]);
-    t.factor_masks[n].resize(t.factors[n].size());
-    for (std::size_t k = 0; k < t.factors[n].size(); ++k) draw(t.factors[n][k], t.factor_masks[n][k]);
-  }
-  t.core.resize(t.core_size());
-  t.core_mask.resize(t.core.size());
-  for (std::size_t k = 0; k < t.core.size(); ++k) draw(t.core[k], t.core_mask[k]);
-  SparseTensor& x = out.tensor;
-  x.dims = spec.dims;
-  x.coords = b200_detail::sample_coords(spec.dims, spec.nnz, rng);
-  x.values = predict(t, std::span<const Coord>(x.coords));  // on the device
+  SyntheticData out;
+  TuckerModel& truth = out.truth;
+  truth.dims = spec.dims;
+  truth.ranks = spec.ranks;
+  truth.factors.resize(spec.dims.size());
+  truth.factor_masks.resize(spec.dims.size());
+  for (std::size_t n = 0; n < spec.dims.size(); ++n)
+    plant(truth.factors[n], truth.factor_masks[n], spec.dims[n] * spec.ranks[n]);
+  plant(truth.core, truth.core_mask, truth.core_size());
+  SparseTensor& obs = out.tensor;
+  obs.dims = spec.dims;
+  obs.coords = b200_detail::sample_coords(spec.dims, spec.nnz, eng);
+  obs.values = predict(truth, std::span<const Coord>(obs.coords));  // on the device
   if (spec.noise_std > 0.0) {
-    std::normal_distribution<double> noise(0.0, 1.0);
-    for (double& v : x.values) v += spec.noise_std * noise(rng);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (double& v : obs.values) v += spec.noise_std * gauss(eng);
   }
   return out;
 }
 
+// one JSON object per iteration (report.hpp:140-156 keys and order)
 inline void write_report_jsonl(const TrainReport& report, std::ostream& out) {
   using b200_detail::num17;
   for (const IterationReport& it : report.iterations) {
-    out << "{\"iter\":" << it.iter << ",\"re\":" << num17(it.re) << ",\"prune_rate\":" << num17(it.prune_rate)
-        << ",\"pruned\":" << (it.pruned ? "true" : "false") << ",\"pruned_core\":" << it.pruned_core
-        << ",\"pruned_factors\":[";
-    for (std::size_t n = 0; n < it.pruned_factors.size(); ++n) out << (n ? "," : "") << it.pruned_factors[n];
-    out << "],\"sparsity\":" << num17(it.sparsity) << ",\"masked\":" << num17(it.masked)
-        << ",\"wall_ms\":" << num17(it.wall_ms) << "}\n";
+    std::string facs;
+    for (std::size_t n = 0; n < it.pruned_factors.size(); ++n)
+      facs += (n ? "," : "") + std::to_string(it.pruned_factors[n]);
+    out << "{\"iter\":" + std::to_string(it.iter) + ",\"re\":" + num17(it.re) +
+               ",\"prune_rate\":" + num17(it.prune_rate) + ",\"pruned\":" + (it.pruned ? "true" : "false") +
+               ",\"pruned_core\":" + std::to_string(it.pruned_core) + ",\"pruned_factors\":[" + facs +
+               "],\"sparsity\":" + num17(it.sparsity) + ",\"masked\":" + num17(it.masked) +
+               ",\"wall_ms\":" + num17(it.wall_ms) + "}\n";
   }
 }
 
@@ -218,13 +234,14 @@ struct BenchResult {
   std::string note;
 };
 
+// median seconds per sweep of plain descent (no pruning, no early stop) for
+// every (config, thread count) cell
 inline std::vector<BenchResult> scaling_benchmark(const std::vector<BenchConfig>& configs,
                                                   const std::vector<int>& thread_counts,
                                                   const BenchOptions& opt = {}) {
-  std::vector<BenchResult> out;
+  std::vector<BenchResult> cells;
   for (const BenchConfig& bc : configs) {
-    SyntheticData data;
-    bool failed = false;
+    std::optional<SyntheticData> data;
     try {
       SyntheticSpec spec;
       spec.dims = bc.dims;
@@ -233,17 +250,15 @@ inline std::vector<BenchResult> scaling_benchmark(const std::vector<BenchConfig>
       spec.seed = opt.seed;
       data = gen_synthetic(spec);
     } catch (const std::bad_alloc&) {
-      failed = true;
+      data.reset();
     }
-    double base = 0.0;
+    double first = 0.0;
     for (std::size_t ti = 0; ti < thread_counts.size(); ++ti) {
-      BenchResult cell;
-      cell.config = bc;
-      cell.threads = thread_counts[ti];
-      if (failed) {
+      BenchResult cell{bc, thread_counts[ti]};
+      if (!data) {
         cell.skipped = true;
         cell.note = "allocation failed";
-        out.push_back(cell);
+        cells.push_back(cell);
         continue;
       }
       TrainConfig cfg;
@@ -255,32 +270,37 @@ inline std::vector<BenchResult> scaling_benchmark(const std::vector<BenchConfig>
       cfg.threads = cell.threads;
       cfg.seed = opt.seed;
       cfg.normalize_output = false;
-      std::vector<double> times;
-      for (std::size_t rep = 0; rep < opt.reps; ++rep)
-        times.push_back(fit(data.tensor, cfg).report.elapsed_sec / double(opt.iters));
-      std::sort(times.begin(), times.end());
-      cell.sec_per_iter = times[times.size() / 2];
-      if (ti == 0) base = cell.sec_per_iter;
-      cell.speedup = cell.sec_per_iter > 0.0 ? base / cell.sec_per_iter : 0.0;
+      std::vector<double> per_iter(opt.reps);
+      for (double& t : per_iter) t = fit(data->tensor, cfg).report.elapsed_sec / static_cast<double>(opt.iters);
+      std::nth_element(per_iter.begin(), per_iter.begin() + per_iter.size() / 2, per_iter.end());
+      cell.sec_per_iter = per_iter[per_iter.size() / 2];
+      if (ti == 0) first = cell.sec_per_iter;
+      cell.speedup = cell.sec_per_iter > 0.0 ? first / cell.sec_per_iter : 0.0;
       cell.note = "b200";
-      out.push_back(cell);
+      cells.push_back(cell);
     }
   }
-  return out;
+  return cells;
 }
 
 inline void write_bench_csv(const std::vector<BenchResult>& cells, std::ostream& out) {
   using b200_detail::num17;
-  out << "order,dims,ranks,nnz,threads,sec_per_iter,speedup,skipped,note\n";
-  auto join = [](const std::vector<std::size_t>& v) {
+  auto dimstr = [](const std::vector<std::size_t>& v) {
     std::string s;
-    for (std::size_t k = 0; k < v.size(); ++k) s += (k ? "x" : "") + std::to_string(v[k]);
+    for (std::size_t v_i : v) s += (s.empty() ? "" : "x") + std::to_string(v_i);
     return s;
   };
-  for (const BenchResult& c : cells)
-    out << c.config.dims.size() << ',' << join(c.config.dims) << ',' << join(c.config.ranks) << ','
-        << c.config.nnz << ',' << c.threads << ',' << num17(c.sec_per_iter) << ',' << num17(c.speedup) << ','
-        << (c.skipped ? 1 : 0) << ',' << c.note << '\n';
+  out << "order,dims,ranks,nnz,threads,sec_per_iter,speedup,skipped,note\n";
+  for (const BenchResult& c : cells) {
+    const std::string fields[] = {std::to_string(c.config.dims.size()), dimstr(c.config.dims),
+                                  dimstr(c.config.ranks),             std::to_string(c.config.nnz),
+                                  std::to_string(c.threads),          num17(c.sec_per_iter),
+                                  num17(c.speedup),                   c.skipped ? "1" : "0",
+                                  c.note};
+    std::string line;
+    for (const std::string& f : fields) line += (line.empty() ? "" : ",") + f;
+    out << line << '\n';
+  }
 }
 
 }  // namespace sparsetuck
