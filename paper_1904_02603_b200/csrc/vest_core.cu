@@ -970,7 +970,13 @@ uint64_t plan_key(const Ctx& c, const Blocks& b, int F) {
   return h;
 }
 
-int pick_block(const Ctx& c) { return c.core_block > 0 ? std::min(c.core_block, kFMax) : kFMax; }
+int pick_block(const Ctx& c) {
+  static const int env = [] {  // VEST_CORE_FMAX: fibers per general block (A/B timing)
+    const char* e = getenv("VEST_CORE_FMAX");
+    return e ? std::max(1, std::min(kFMax, atoi(e))) : kFMax;
+  }();
+  return c.core_block > 0 ? std::min(c.core_block, kFMax) : env;
+}
 
 const void* structured_ops(const Ctx& c) {
   if (c.force_generic || c.N < 3 || c.core_block > 0) return nullptr;
