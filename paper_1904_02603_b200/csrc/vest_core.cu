@@ -1204,7 +1204,13 @@ void core_sweep(Ctx& c, int reg, double lambda) {
   const void* sops = structured_ops(c);
   const int F = sops ? c.ranks[c.N - 2] : pick_block(c);
   const Blocks b = sops ? plan_structured(c) : plan_general(c, F);
-  if (b.fib.empty()) return;  // fully pruned core: nothing to update
+  if (b.fib.empty()) {  // fully pruned core: nothing to update, but the RE of
+    // the updated factors is still due (a residual emitted by the last factor
+    // mode carries no sum of squares yet)
+    c.r_fresh = false;
+    compute_residual(c);
+    return;
+  }
   upload_fibers(c, b);
   if (sops && !legacy_block_passes()) {
     if (const void* aops = find_core_all_ops(c.N, c.ranks)) {

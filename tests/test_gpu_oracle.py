@@ -429,3 +429,65 @@ def test_cd_iteration_trajectory_vs_oracle():
     assert_close(got.core, want.core, "core after 5 iterations")
     for n in range(3):
         assert_close(got.factors[n], want.factors[n], f"factor{n} after 5 iterations")
+
+
+@pytest.mark.parametrize("dims,ranks,mf,pr", [([24, 20, 18, 16], [8, 8, 8, 8], 0.9, 0.05),
+                                              ([9, 8, 8, 7, 7], [5, 5, 5, 5, 5], 0.0, 0.2)])
+def test_auto_kernel_switch_trajectory_vs_oracle(dims, ranks, mf, pr):
+    """Auto mode on rank-specialised 4/5-mode shapes: sweep 1 runs the
+    precompiled kernels, sweep 2 compiles the mask's NVRTC kernels (generated
+    core passes; the mask-specialised delta for the 90 %-masked core), a prune
+    changes the mask (precompiled again for one sweep, then recompiled) -- the
+    whole trajectory stays on the oracle's."""
+    coords, values, m = random_instance(dims, ranks, 5000, 61, mask_frac=mf, lo=0.0, hi=1.0)
+    x = st.make_tensor(dims, coords, values)
+    dev = st.Device(x, ranks)
+    dev.set_model(m)
+    s = oracle_session(dims, ranks, coords, values, m)
+    for t in range(6):
+        re = dev.cd_iteration(0, 0.01)
+        re_ref = s.cd_iteration(0, 0.01, 1)
+        assert abs(re - re_ref) <= 1e-6 * re_ref, t
+        if t == 2:
+            before = model_of(s, dims, ranks)
+            dev.compute_responsibilities(want=False)
+            s.compute_residuals(1)
+            rc, _ = s.compute_responsibilities(1)
+            counts = dev.prune_step(pr)
+            ref_counts = s.prune_step(pr)
+            assert 0 < counts.core < int(np.sum(m.core_mask == 0))  # the core survives the prune
+            assert [counts.core] + counts.factors == [int(c) for c in ref_counts]
+            want = model_of(s, dims, ranks)
+            assert_masks(dev.get_model().core_mask, want.core_mask, rc, before.core_mask, "core mask")
+            # near-threshold ties may pick different cells (within tolerance):
+            # continue both from the oracle's pruned model
+            dev.set_model(want)
+    got, want = dev.get_model(), model_of(s, dims, ranks)
+    assert_close(got.core, want.core, "core")
+    for n in range(len(dims)):
+        assert_close(got.factors[n], want.factors[n], f"factor{n}")
+
+
+@pytest.mark.parametrize("ranks", [[3, 3, 2], [5, 5, 5], [2, 3, 2, 2]])
+def test_iteration_re_after_core_fully_pruned(ranks):
+    """A prune that masks every core cell (k is floored against the block size,
+    masked cells included): the next iteration's RE is that of the zero
+    reconstruction, 1.0, exactly as the reference's."""
+    dims = [20, 18, 16, 14][: len(ranks)]
+    coords, values, m = random_instance(dims, ranks, 1500, 71, lo=0.0, hi=1.0)
+    m.core_mask[:] = 1
+    m.core_mask.reshape(-1)[0] = 0
+    m.core[m.core_mask == 1] = 0.0
+    x = st.make_tensor(dims, coords, values)
+    dev = st.Device(x, ranks)
+    dev.set_model(m)
+    s = oracle_session(dims, ranks, coords, values, m)
+    dev.cd_iteration(0, 0.01)
+    s.cd_iteration(0, 0.01, 1)
+    dev.compute_responsibilities(want=False)
+    s.compute_residuals(1)
+    s.compute_responsibilities(1)
+    assert dev.prune_step(0.5).core == int(s.prune_step(0.5)[0]) == 1
+    for _ in range(2):
+        re, re_ref = dev.cd_iteration(0, 0.01), s.cd_iteration(0, 0.01, 1)
+        assert re_ref == 1.0 and abs(re - re_ref) <= 1e-12, (re, re_ref)
