@@ -150,6 +150,10 @@ def test_core_gen_passes(dims, ranks, mf, gen):
 
 def test_sparse_delta_heavy_rows():
     phases([3, 60, 60], [5, 5, 5], 9000, 18, 0, 0.01, iters=1, sparse=1)
+    # heavy rows in the LAST mode: their residual after k_heavy's solve
+    # (k_rowpass_delta<kResid>) feeds the core sweep
+    phases([60, 60, 3], [5, 5, 5], 9000, 19, 0, 0.01, iters=2, sparse=1)
+    phases([40, 30, 25, 3], [3, 2, 4, 2], 9000, 21, 1, 0.05, iters=1, sparse=1, mask_frac=0.2)
     phases([12, 40, 30], [5, 5, 5], 8000, 20, 1, 0.05, iters=1, skew=1.6, sparse=1)
 
 
