@@ -548,14 +548,20 @@ __global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, i
 // statistics rows staged in shared memory); CTA partials are summed in a
 // fixed order afterwards (deterministic).
 constexpr int kHsBatch = 8, kHsPer = 8, kHsThreads = 256;
+__device__ __forceinline__ void hs_cp8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __restrict__ stats, int stride, int width,
                                                              const Chunk* __restrict__ chunks, uint32_t nchunks,
                                                              const double* __restrict__ A, int ld, int Jm,
                                                              const uint32_t* __restrict__ tab, int E,
                                                              double* __restrict__ partial) {
   extern __shared__ double hs[];
-  double* ss = hs;                     // [kHsBatch][width]
-  double* sa = hs + kHsBatch * width;  // [kHsBatch][Jm]
+  // two batch buffers [kHsBatch][width] + [kHsBatch][Jm]: the next batch's rows
+  // are copied by cp.async while this batch is accumulated
+  const int bufw = kHsBatch * (width + Jm);
   const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
   const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
   uint32_t my[kHsPer];
@@ -566,18 +572,33 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
     my[j] = e < E ? __ldg(tab + e) : 0xffffffffu;
     acc[j] = 0.0;
   }
-  for (uint32_t cb = c0; cb < c1; cb += kHsBatch) {
+  auto stage = [&](uint32_t cb, int buf) {
     const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
-    __syncthreads();
-    for (int t = threadIdx.x; t < nb * width; t += kHsThreads) {
-      const int b = t / width, w = t - b * width;
-      ss[t] = __ldg(stats + (size_t)(cb + b) * stride + w);
+    double* ss = hs + buf * bufw;
+    double* sa = ss + kHsBatch * width;
+    for (int b = 0; b < nb; ++b) {
+      const double* src = stats + (size_t)(cb + b) * stride;
+      for (int w = threadIdx.x; w < width; w += kHsThreads) hs_cp8(ss + b * width + w, src + w);
     }
     for (int t = threadIdx.x; t < nb * Jm; t += kHsThreads) {
       const int b = t / Jm, q = t - b * Jm;
-      sa[t] = __ldg(A + (size_t)chunks[cb + b].row * ld + q);
+      hs_cp8(sa + t, A + (size_t)chunks[cb + b].row * ld + q);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (c0 < c1) stage(c0, 0);
+  int buf = 0;
+  for (uint32_t cb = c0; cb < c1; cb += kHsBatch) {
+    const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
+    if (cb + kHsBatch < c1) {
+      stage(cb + kHsBatch, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const double* ss = hs + buf * bufw;
+    const double* sa = ss + kHsBatch * width;
     for (int b = 0; b < nb; ++b) {
 #pragma unroll
       for (int j = 0; j < kHsPer; ++j) {
@@ -588,6 +609,8 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
         acc[j] += v;
       }
     }
+    __syncthreads();  // the buffer is re-staged two batches from now
+    buf ^= 1;
   }
 #pragma unroll
   for (int j = 0; j < kHsPer; ++j) {
@@ -1156,7 +1179,7 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
   ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)E);
   double* raw = c.d_gemm_part + (size_t)nparts * E;
   const int width = NS + nf;
-  const size_t sm = (size_t)kHsBatch * (width + Jm) * sizeof(double);
+  const size_t sm = (size_t)2 * kHsBatch * (width + Jm) * sizeof(double);
   ProfScope ps(c, kProfCoreGemm);
   check(cudaFuncSetAttribute(k_core_hsample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "hsample smem");
   k_core_hsample<<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks, md.nchunks,
