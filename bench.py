@@ -461,6 +461,9 @@ def run_shard_emulation(cfg_id, world, iters):
     print(json.dumps(out), flush=True)
 
 
+NO_FAMILIES = False
+
+
 def run_config(cfg_id, iters_override=None):
     """Full-size run of BASELINE config `cfg_id` on one GPU: per-iteration device
     time (CUDA events on the library stream), prune events timed separately."""
@@ -489,7 +492,9 @@ def run_config(cfg_id, iters_override=None):
     iters = iters_override or c["iters"]
     from paper_1904_02603_b200 import _lib
     L = _lib.lib()
-    L.vest_ctx_profile(dev.h, 1)
+    # kernel-family timing (per-family events) disables the iteration graphs;
+    # --no-families measures the production path
+    L.vest_ctx_profile(dev.h, 0 if NO_FAMILIES else 1)
     times, res, prunes = [], [], []
     for t in range(1, iters + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -532,6 +537,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=0, help="run BASELINE config 1..5 at full size (diagnostic)")
     ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--no-families", action="store_true",
+                    help="with --config: no per-family event timing (iteration graphs stay enabled)")
     ap.add_argument("--shard-emulate", type=int, default=0,
                     help="with --config: per-GPU device time of one rank's share at W GPUs (no exchanges)")
     ap.add_argument("--gpus", type=int, default=1)
@@ -543,6 +550,8 @@ def main():
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
+    global NO_FAMILIES
+    NO_FAMILIES = args.no_families
     if args.config and args.shard_emulate:
         run_shard_emulation(args.config, args.shard_emulate, args.iters or 3)
         return

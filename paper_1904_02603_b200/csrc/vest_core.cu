@@ -1192,10 +1192,14 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
 }
 
 void upload_fibers(Ctx& c, const Blocks& b) {
+  // the plan changes only with the mask: skip identical uploads (a copy from a
+  // temporary host buffer must not be recorded into an iteration graph)
+  if (c.d_fibers && c.h_fibers == b.fib) return;
   ensure(c, reinterpret_cast<double**>(&c.d_fibers), &c.fibers_cap, (b.fib.size() + 1) / 2 + 1);
   check(cudaMemcpyAsync(c.d_fibers, b.fib.data(), b.fib.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                         c.stream),
         "fibers");
+  c.h_fibers = b.fib;
 }
 
 // Pack the structured pass operands (U, W) for this context's positions of the
@@ -1214,6 +1218,11 @@ void pack_operands(Ctx& c, const void* sops) {
 }
 
 }  // namespace
+
+bool core_sweep_capturable(const Ctx& c) {
+  const void* sops = structured_ops(c);
+  return sops && !legacy_block_passes() && find_core_all_ops(c.N, c.ranks);
+}
 
 // the general plan's blocks (host-only compile check of the generated passes)
 std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c) { return block_lists(plan_general(c, pick_block(c))); }

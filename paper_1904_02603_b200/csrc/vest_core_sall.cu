@@ -1087,9 +1087,11 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   }
   // r lacks the last group's update until someone reads it (core_apply_pending)
   check(cudaMemcpyAsync(c.h_small, c.d_small, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "sum readback");
-  check(cudaStreamSynchronize(c.stream), "sum sync");
-  c.sum_sq = std::max(0.0, c.h_small[0]);
-  c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  if (!c.capturing) {  // a captured iteration reads the sum after the graph launch
+    check(cudaStreamSynchronize(c.stream), "sum sync");
+    c.sum_sq = std::max(0.0, c.h_small[0]);
+    c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  }
   c.r_valid = false;
   c.r_fresh = false;
   c.r_pending[0] = prev[0];

@@ -895,6 +895,7 @@ int vest_ctx_destroy(vest_ctx* h) {
   cudaFree(c.d_small);
   cudaFree(c.d_fibers);
   cudaFree(c.d_dg);
+  if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
   cudaFree(c.d_delta);
   cudaFree(c.d_hstab);
   sparse_free(c);
@@ -1068,16 +1069,118 @@ int vest_compute_residuals(vest_ctx* h, double* r_out, double* sum_sq, double* x
   });
 }
 
+// ------------------------------------------------------- iteration graphs --
+// One CD iteration of the 3-mode all-prefix path is ~20 launches with no host
+// synchronisation except the final sum read-back, and its host logic depends
+// only on (core mask, regulariser, lambda, kernel choice).  Once the same key
+// has run twice, the iteration is captured into a CUDA graph (relaxed capture
+// mode; the read-back is a captured D2H copy into pinned memory) and replayed:
+// one launch per iteration instead of ~20 (config 1 is launch-bound).  Same
+// kernels in the same order: bit-identical to the stream path.
+// VEST_GRAPH=0 disables it.
+static bool graph_off() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_GRAPH");
+    return e && e[0] == '0';
+  }();
+  return v;
+}
+
+static bool graph_eligible(const Ctx& c) {
+  return !graph_off() && !c.prof_on && !c.comm.allreduce_sum && !c.comm.allgather_rows &&
+         core_sweep_capturable(c) && c.mask_sweeps >= 3;
+}
+
+static uint64_t graph_key_of(const Ctx& c, int reg, double lambda) {
+  uint64_t h = core_mask_hash(c) ^ 0x9E3779B97F4A7C15ull;
+  auto mix = [&](uint64_t v) {
+    h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  };
+  uint64_t lb;
+  std::memcpy(&lb, &lambda, 8);
+  mix((uint64_t)reg);
+  mix(lb);
+  mix(sparse_delta_enabled(c) ? 1 : 0);
+  return h;
+}
+
+static void graph_free(Ctx& c) {
+  if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
+  c.graph_exec = nullptr;
+  c.graph_key = 0;
+}
+
+static void iteration_body(Ctx& c, int reg, double lambda) {
+  sync_const_core(c);
+  for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda, true);
+  core_sweep(c, reg, lambda);
+  c.table_valid = false;
+}
+
+// replay the captured iteration and restore the host state it leaves
+static void graph_replay(Ctx& c) {
+  check(cudaGraphLaunch(c.graph_exec, c.stream), "graph launch");
+  launch_counter() += c.graph_launches;
+  note_sweep(c);
+  check(cudaStreamSynchronize(c.stream), "graph sync");
+  c.sum_sq = std::max(0.0, c.h_small[0]);
+  c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  c.r_valid = false;
+  c.r_fresh = false;
+  c.r_pending[0] = c.graph_pending[0];
+  c.r_pending[1] = c.graph_pending[1];
+  c.r_pending_ops = c.graph_pending_ops;
+  c.table_valid = false;
+}
+
 int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
   Ctx& c = h->c;
   return guard([&] {
     check_reg(reg);
     if (c.x_norm == 0.0) throw ArgError{"zero-norm tensor"};
     set_dev(c);
-    sync_const_core(c);
-    for (int n = 0; n < c.N; ++n) update_factor_mode(c, n, reg, lambda, true);
-    core_sweep(c, reg, lambda);
-    c.table_valid = false;
+    if (graph_eligible(c)) {
+      const uint64_t key = graph_key_of(c, reg, lambda);
+      if (c.graph_exec && c.graph_key == key) {
+        graph_replay(c);
+        if (re) *re = c.re;
+        return;
+      }
+      if (c.graph_seen_key == key && c.graph_seen >= 1) {
+        graph_free(c);
+        const uint64_t l0 = launch_counter();
+        check(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed), "begin capture");
+        c.capturing = true;
+        try {
+          iteration_body(c, reg, lambda);
+        } catch (...) {
+          cudaGraph_t g = nullptr;
+          cudaStreamEndCapture(c.stream, &g);
+          if (g) cudaGraphDestroy(g);
+          c.capturing = false;
+          throw;
+        }
+        c.capturing = false;
+        cudaGraph_t g = nullptr;
+        check(cudaStreamEndCapture(c.stream, &g), "end capture");
+        const cudaError_t ie = cudaGraphInstantiate(&c.graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        check(ie, "graph instantiate");
+        c.graph_key = key;
+        c.graph_launches = launch_counter() - l0;
+        launch_counter() = l0;  // counted when replayed
+        c.graph_pending[0] = c.r_pending[0];
+        c.graph_pending[1] = c.r_pending[1];
+        c.graph_pending_ops = c.r_pending_ops;
+        c.mask_sweeps -= 1;  // the capture ran no sweep; the replay counts it
+        graph_replay(c);
+        if (re) *re = c.re;
+        return;
+      }
+      c.graph_seen_key = key;
+      c.graph_seen = 1;
+    }
+    iteration_body(c, reg, lambda);
     if (re) *re = c.re;
   });
 }

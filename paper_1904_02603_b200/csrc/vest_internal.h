@@ -175,6 +175,7 @@ struct Ctx {
   double* d_small = nullptr;       // small reduction outputs (pinned-mapped readback)
   double* h_small = nullptr;
   uint32_t* d_fibers = nullptr;    size_t fibers_cap = 0;  // fiber prefix lin indices
+  std::vector<uint32_t> h_fibers;  // what d_fibers holds
   double* d_dg = nullptr;          size_t dg_cap = 0;
   double* d_pack_u = nullptr;      size_t pack_u_cap = 0;   // structured core pass operands
   double* d_pack_w = nullptr;      size_t pack_w_cap = 0;
@@ -190,6 +191,15 @@ struct Ctx {
   // an NVRTC compile, a stable one pays it once)
   uint64_t mask_key = 0;
   int mask_sweeps = 0;
+  // CUDA graph of one CD iteration (3-mode all-prefix path, single GPU):
+  // captured once the iteration's host logic has repeated with the same key
+  bool capturing = false;            // inside stream capture: no host syncs
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_key = 0, graph_seen_key = 0;
+  int graph_seen = 0;
+  uint64_t graph_launches = 0;       // kernels per replay (launch accounting)
+  int graph_pending[2] = {-1, -1};   // r_pending after the captured iteration
+  const void* graph_pending_ops = nullptr;
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
   double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
   uint32_t* d_hstab = nullptr;     size_t hstab_cap = 0;    // live-cell Gram entry table (k_core_hsample)
@@ -249,6 +259,8 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
 void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, int reg, double lambda);
 void compute_residual(Ctx& c);  // fresh r = x - B(alpha), sum_sq, re
 void core_sweep(Ctx& c, int reg, double lambda);
+bool core_sweep_capturable(const Ctx& c);  // the sweep takes the all-prefix path (no host syncs inside)
+uint64_t core_mask_hash(const Ctx& c);
 void responsibilities(Ctx& c);
 void prune(Ctx& c, double pr, uint64_t* counts);
 void sparsity(Ctx& c, double* zero_frac, double* masked_frac);

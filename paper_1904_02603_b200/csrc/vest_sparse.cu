@@ -262,6 +262,8 @@ bool sparse_delta_enabled(const Ctx& c) {
   return sparse_mode(c) == 1 || c.mask_sweeps >= 2;
 }
 
+uint64_t core_mask_hash(const Ctx& c) { return mask_key(c); }
+
 void note_sweep(Ctx& c) {
   const uint64_t key = mask_key(c);
   if (key == c.mask_key && c.mask_sweeps > 0) {

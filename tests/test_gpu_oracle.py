@@ -495,3 +495,34 @@ def test_iteration_re_after_core_fully_pruned(ranks):
     for _ in range(2):
         re, re_ref = dev.cd_iteration(0, 0.01), s.cd_iteration(0, 0.01, 1)
         assert re_ref == 1.0 and abs(re - re_ref) <= 1e-12, (re, re_ref)
+
+
+@pytest.mark.parametrize("ranks", [[5, 5, 5], [10, 10, 5]])
+def test_iteration_graph_replay_bit_identical(ranks):
+    """From the fifth iteration with an unchanged mask on, a 3-mode iteration is
+    captured once as a CUDA graph and replayed; it must reproduce the stream
+    path bit for bit (the stream path is forced by profiling, which disables
+    graphs), and a prune in between drops back to the stream path."""
+    from paper_1904_02603_b200 import _lib
+    dims = [60, 50, 40]
+    coords, values, m = random_instance(dims, ranks, 6000, 81, lo=0.0, hi=1.0)
+    x = st.make_tensor(dims, coords, values)
+    out = []
+    for profile in (0, 1):
+        dev = st.Device(x, ranks)
+        _lib.lib().vest_ctx_profile(dev.h, profile)
+        dev.set_model(m)
+        before = _lib.lib().vest_launch_count()
+        res = [dev.cd_iteration(0, 0.01) for _ in range(8)]
+        launches = _lib.lib().vest_launch_count() - before
+        dev.compute_responsibilities(want=False)
+        dev.prune_step(0.1)
+        res += [dev.cd_iteration(1, 0.05) for _ in range(8)]
+        out.append((res, dev.get_model(), launches))
+        dev.close()
+    (ra, ma, la), (rb, mb, lb) = out
+    assert ra == rb
+    assert la == lb  # replays are counted like the launches they contain
+    assert np.array_equal(ma.core, mb.core)
+    for n in range(3):
+        assert np.array_equal(ma.factors[n], mb.factors[n])
