@@ -46,6 +46,7 @@ void* dalloc(Ctx& c, size_t bytes) {
   if (bytes == 0) bytes = 16;
   check(cudaMalloc(&p, bytes), "cudaMalloc");
   c.device_bytes += bytes;
+  ++c.alloc_epoch;
   return p;
 }
 
@@ -1101,6 +1102,7 @@ static uint64_t graph_key_of(const Ctx& c, int reg, double lambda) {
   mix((uint64_t)reg);
   mix(lb);
   mix(sparse_delta_enabled(c) ? 1 : 0);
+  mix(c.alloc_epoch);  // any (re)allocation since the capture invalidates the graph
   return h;
 }
 

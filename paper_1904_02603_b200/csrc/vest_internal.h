@@ -194,6 +194,7 @@ struct Ctx {
   // CUDA graph of one CD iteration (3-mode all-prefix path, single GPU):
   // captured once the iteration's host logic has repeated with the same key
   bool capturing = false;            // inside stream capture: no host syncs
+  uint64_t alloc_epoch = 0;          // bumped by every device allocation (a graph's buffers must not move)
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_key = 0, graph_seen_key = 0;
   int graph_seen = 0;
