@@ -35,8 +35,11 @@ for k, v in sorted(agg.items(), key=lambda x: -x[1][0]):
     lines.append(f"| `{k}` | {v[1]} | {v[0] / 1e3:.1f} | {100 * v[0] / tot:.1f}% |")
 open(f"profiles/{tag}_ncu_launches.md", "w").write("\n".join(lines) + "\n")
 
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # a `--page raw --csv` export made on the GPU box
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 h, units, body = rows[0], rows[1], rows[2:]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
