@@ -183,6 +183,15 @@ static int bits_for(uint64_t d) {
   return b;
 }
 
+// rows up to this length run lane-per-row (VEST_TINY_MAX overrides kTinyRow: A/B timing)
+static uint32_t tiny_max() {
+  static const uint32_t v = [] {
+    const char* e = getenv("VEST_TINY_MAX");
+    return e ? (uint32_t)std::max(0, atoi(e)) : kTinyRow;
+  }();
+  return v;
+}
+
 void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
   const uint64_t nnz = c.nnz;
   const int N = c.N;
@@ -313,7 +322,7 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
       std::vector<std::pair<uint32_t, uint32_t>> tiny;
       std::vector<Chunk> big;
       for (const Chunk& ch : chunks) {
-        if (ch.slot == kLight && ch.end - ch.beg <= kTinyRow) tiny.push_back({ch.end - ch.beg, ch.row});
+        if (ch.slot == kLight && ch.end - ch.beg <= tiny_max()) tiny.push_back({ch.end - ch.beg, ch.row});
         else big.push_back(ch);
       }
       std::stable_sort(tiny.begin(), tiny.end(),
