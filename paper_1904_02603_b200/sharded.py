@@ -43,13 +43,20 @@ class VestComm(C.Structure):
     _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE), ("allgather_rows", ALLGATHER)]
 
 
-def partition(x: SparseTensor, world: int):
-    """Per-mode row bounds [world + 1] balanced by observed entries
-    (vest_partition_rows over each mode's row counts)."""
+def partition(x: SparseTensor, world: int, row_cost: Optional[int] = None):
+    """Per-mode row bounds [world + 1] balanced by work: observed entries plus
+    `row_cost` entry-equivalents per non-empty row (the per-row solve and the
+    short-row kernel's one-lane-per-row cost; VEST_ROW_COST overrides), through
+    vest_partition_rows over the weights' prefix sums."""
+    import os
+    if row_cost is None:
+        row_cost = int(os.environ.get("VEST_ROW_COST", "8"))
     L = _lib.lib()
     bounds = []
     for n in range(x.order()):
         counts = np.bincount(np.asarray(x.coords[:, n], np.int64), minlength=int(x.dims[n]))
+        if row_cost:
+            counts = counts + row_cost * (counts > 0)
         off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
         b = np.zeros(world + 1, np.uint64)
         check(L.vest_partition_rows(ptr(off, u64p), int(x.dims[n]), world, ptr(b, u64p)))
