@@ -136,6 +136,26 @@ def test_partition_rows_balanced(L):
             assert off[b[r]] >= target and (b[r] == b[r - 1] or off[b[r] - 1] < target)
 
 
+def test_sharded_partition_row_cost():
+    """sharded.partition balances entries + row_cost per non-empty row: a Zipf
+    mode's long tail of short rows moves its boundary towards the tail."""
+    from paper_1904_02603_b200 import sharded as sh
+    rng = np.random.default_rng(3)
+    rows = np.minimum(rng.zipf(1.3, 20000), 2000).astype(np.int64) - 1
+    rows = rows[rows < 2000]
+    coords = np.stack([rows, rng.integers(0, 50, len(rows)), rng.integers(0, 40, len(rows))], 1)
+    x = st.SparseTensor([2000, 50, 40], coords.astype(np.uint32), np.ones(len(rows)))
+    for rc in (0, 8):
+        b = sh.partition(x, 4, row_cost=rc)[0].astype(np.int64)
+        counts = np.bincount(rows, minlength=2000)
+        w = counts + rc * (counts > 0)
+        loads = [w[b[r]:b[r + 1]].sum() for r in range(4)]
+        assert b[0] == 0 and b[-1] == 2000 and np.all(np.diff(b) >= 0)
+        assert max(loads) <= w.sum() / 4 + w.max()  # balanced up to one row
+    b0, b8 = sh.partition(x, 4, row_cost=0)[0], sh.partition(x, 4, row_cost=8)[0]
+    assert b8[-2] >= b0[-2]  # the tail rank owns fewer (costlier) short rows
+
+
 # ---- host control logic (pruning.hpp:17-81), cases from tests/test_pruning.cpp:17-92
 def test_prune_schedule():
     s = st.PruneSchedule(0.01, 0.1)
