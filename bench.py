@@ -1,12 +1,16 @@
 #!/usr/bin/env python
 """VeST CD-sweep benchmark (BASELINE.json metric: observed-nnz*iter/s).
 
-Workload (BASELINE.json configs[1], "config 2"): 3-mode 100k x 100k x 100k,
-10M observed entries at uniform-random distinct coordinates, fp64 values
-U[0,1), Tucker ranks 10x10x10, lambda = 0.01 (LF), init_random(seed) factors.
-A step = one CD iteration as fit() runs it (trainer.hpp:121-127):
-update_all_factors + update_core + residuals/RE, over all 10M entries.
-Prune events (responsibilities + prune) are timed separately ("prune_event").
+Headline workload (BASELINE.json configs[3], "config 4" -- the largest
+configuration, fits one B200): 4-mode 1M^4 tensor, 200M observed entries at
+uniform-random distinct coordinates, values N(0,1) rounded to fp32 (held as
+fp64), Tucker ranks 8x8x8x8 with the core pruned to 10% nonzero (a seeded 90%
+core mask in the initial model), lambda = 0.01 (LF),
+init_random(7) factors.  A step = one CD iteration as fit() runs it
+(trainer.hpp:121-127): update_all_factors + update_core + residuals/RE over all
+200M entries.  Config 2 (3-mode 100k^3, 10M entries, R 10^3; the round-1
+headline) is measured after it as a secondary key.  Prune events
+(responsibilities + prune) are timed separately ("prune_event").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -17,7 +21,9 @@ ours:       device-resident steps, CUDA events on the library stream ("value");
             ("cpu_baseline").
 reference:  the reference's own CPU implementation (oracle/_ref: the
             unmodified reference headers; the C port when _ref is absent) on a
-            bounded sample of the same workload, all host threads.
+            bounded sample of the same workload (same dims, ranks, core mask,
+            lambda and value distribution; fewer entries, stated in `config`),
+            all host threads.  It never loads the repo's CUDA library.
 """
 from __future__ import annotations
 
@@ -37,9 +43,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "CD sweep observed-nnz*iter/s"
 UNIT = "nnz*iter/s"
-CONFIG2 = dict(dims=[100_000] * 3, nnz=10_000_000, ranks=[10, 10, 10], lam=0.01, reg=0, seed=2,
-               data_seed=20261020, values_kind=0)
-SAMPLE_NNZ = 300_000  # CPU reference sample (same shape/distribution, fewer entries)
+HEADLINE = 4
+SECONDARY = 2
+# CPU reference samples: entries per step (same dims/ranks/mask/distribution)
+SAMPLE_NNZ = {1: 100_000, 2: 300_000, 3: 300_000, 4: 500_000, 5: 200_000}
 
 
 def env_int(name, default):
@@ -104,22 +111,8 @@ def step_flops_per_entry(ranks, core_unmasked=None):
         for Ja in others:
             d += size
             size //= Ja
-        total += 2 * d + ranks[n] * (ranks[n] + 1) + 2 * ranks[n]
+        total += min(2 * d, Gu * N) + ranks[n] * (ranks[n] + 1) + 2 * ranks[n]
     return total + Gu * (N + 7) + 2
-
-
-def factor_launch_model(ranks, nnz, modes=None):
-    """(flops, bytes) per launch of the dominant kernel: the factor-row update
-    of one mode (k_rowpass<kStats>), averaged over modes 0..modes-1 (the last
-    mode carries the fused residual and is timed as its own family)."""
-    N = len(ranks)
-    modes = modes or N
-    fl, by = 0, 0
-    for n in range(modes):
-        J = ranks[n]
-        fl += 2 * nnz * (contraction_fmas(ranks, n) + J * (J + 1) // 2 + J)
-        by += nnz * ((N - 1) * 4 + 8)  # compulsory: other coords + value per entry
-    return fl / modes, by / modes
 
 
 # ------------------------------------------------------------------ clocks --
@@ -172,119 +165,212 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------- CPU baseline leg --
-def cpu_reference_rate(steps=1, nnz=SAMPLE_NNZ, threads=None):
-    """The reference CPU path (oracle/_ref when built, else the C port) on a
-    bounded sample of config 2: same dims/ranks/lambda/value distribution,
-    `nnz` entries.  Returns (rate nnz*iter/s, kind, threads, seconds/iter)."""
+# ------------------------------------------------------------- workloads --
+def core_mask(ranks, keep):
+    """Seeded core mask ("core pruned to 10% nonzero"
+    as a 90% mask in the initial model, identical for the GPU and the CPU arm)."""
+    rng = np.random.default_rng(44)
+    return (rng.random(int(np.prod(ranks))) >= keep).astype(np.uint8)
+
+
+def model_for(c):
+    """init_random(dims, ranks, 7) (tucker_model.hpp:88-108) + the config's core mask."""
+    from paper_1904_02603_b200 import sparsetuck as st
+    m = st.init_random(c["dims"], c["ranks"], 7)
+    if c["core_keep"] < 1.0:
+        mask = core_mask(c["ranks"], c["core_keep"]).reshape(m.core.shape)
+        m.core[mask == 1] = 0.0
+        m.core_mask = mask
+    return m
+
+
+def synth_numpy(dims, nnz, seed, values_kind=0):
+    """Seeded sample for the CPU arms, made with numpy only (the reference arm
+    must not load the repo's CUDA library): uniform distinct coordinates
+    (duplicates dropped; at 1M^4 there are none in practice), values U[0,1)
+    (kind 0), integers 1..5 (kind 1) or N(0,1) rounded to float (kind 2)."""
+    rng = np.random.default_rng(seed)
+    c = np.stack([rng.integers(0, int(d), nnz, dtype=np.int64) for d in dims], 1).astype(np.uint32)
+    c = np.unique(c, axis=0)  # canonical row-major order, distinct
+    n = len(c)
+    if values_kind == 1:
+        v = rng.integers(1, 6, n).astype(np.float64)
+    elif values_kind == 2:
+        v = rng.standard_normal(n).astype(np.float32).astype(np.float64)
+    else:
+        v = rng.random(n)
+    return c, v
+
+
+def cpu_session(cfg_id, nnz, threads):
+    """The reference CPU path (oracle/_ref = the unmodified reference headers
+    when built, else the C port) on a bounded sample of config `cfg_id`: the
+    config's dims, ranks, lambda, value distribution, initial model and core
+    mask, `nnz` entries."""
     from oracle import oracle as O  # test/baseline infrastructure only
     kind = "reference" if O.available("reference") else "port"
-    threads = threads or os.cpu_count() or 1
-    cfg = CONFIG2
-    coords, vals = synth(cfg["dims"], nnz, cfg["data_seed"] + 1)
-    s = O.Session(cfg["dims"], coords, vals, cfg["ranks"], kind)
-    s.init_random(cfg["seed"])
-    s.cd_iteration(cfg["reg"], cfg["lam"], threads)  # warm-up (first-touch, page-in)
+    c = CONFIGS[cfg_id]
+    coords, vals = synth_numpy(c["dims"], nnz, 77 + cfg_id, c["values_kind"])
+    s = O.Session(c["dims"], coords, vals, c["ranks"], kind)
+    s.init_random(7)
+    if c["core_keep"] < 1.0:
+        core, cm, fs, ms = s.get_model()
+        mask = core_mask(c["ranks"], c["core_keep"]).reshape(core.shape)
+        core[mask == 1] = 0.0
+        s.set_model(core, mask, fs, ms)
+    return s, kind, len(vals)
+
+
+def sample_desc(cfg_id, nnz):
+    c = CONFIGS[cfg_id]
+    return (f"config{cfg_id} shape ({'x'.join(str(d) for d in c['dims'])}, ranks {c['ranks']}, core keep "
+            f"{c['core_keep']}, lambda {c['lam']}) with {nnz} uniform entries (numpy-seeded) per step; dims kept "
+            f"so the factor gathers miss cache as at full size")
+
+
+def cpu_reference_rate(cfg_id, steps=2):
+    threads = os.cpu_count() or 1
+    s, kind, nnz = cpu_session(cfg_id, SAMPLE_NNZ[cfg_id], threads)
+    c = CONFIGS[cfg_id]
+    s.cd_iteration(0, c["lam"], threads)  # warm-up (first touch, page-in)
     t0 = time.perf_counter()
     for _ in range(steps):
-        s.cd_iteration(cfg["reg"], cfg["lam"], threads)
+        s.cd_iteration(0, c["lam"], threads)
     dt = (time.perf_counter() - t0) / steps
-    return nnz / dt, kind, threads, dt
+    return nnz / dt, kind, threads, dt, nnz
 
 
 def run_reference_arm(args, rank):
+    """`--impl reference`: the reference's own CPU implementation of the path
+    (oracle/_ref) on the host cores, each step one CD iteration over a bounded
+    sample of the headline workload.  Rank 0 only under torchrun."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    from oracle import oracle as O
-    kind = "reference" if O.available("reference") else "port"
-    cfg = CONFIG2
-    coords, vals = synth(cfg["dims"], SAMPLE_NNZ, cfg["data_seed"] + 1)
-    s = O.Session(cfg["dims"], coords, vals, cfg["ranks"], kind)
-    s.init_random(cfg["seed"])
+    cfg_id = args.workload
+    c = CONFIGS[cfg_id]
+    s, kind, nnz = cpu_session(cfg_id, SAMPLE_NNZ[cfg_id], threads)
     for _ in range(args.warmup):
-        s.cd_iteration(cfg["reg"], cfg["lam"], threads)
+        s.cd_iteration(0, c["lam"], threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        s.cd_iteration(cfg["reg"], cfg["lam"], threads)
+        s.cd_iteration(0, c["lam"], threads)
     dt = time.perf_counter() - t0
-    value = SAMPLE_NNZ * args.steps / dt
-    sample = f"config2 shape (100k^3, R=10, lambda=0.01, U[0,1)) with {SAMPLE_NNZ} entries per step"
+    value = nnz * args.steps / dt
+    cfgd = workload_config(cfg_id, args.gpus)
+    cfgd["nnz"] = nnz
+    cfgd["sample"] = sample_desc(cfg_id, nnz)
+    cfgd["parallelism"] = f"OpenMP, {threads} host threads"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args.gpus),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "data": "synthetic", "config": cfgd,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample_desc(cfg_id, nnz)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(n):
-    return {"workload": "config2: 3-mode 100k^3, 10M uniform distinct entries, fp64 U[0,1), ranks 10x10x10, "
-                        "lambda 0.01 LF; step = update_all_factors + update_core + RE",
-            "nnz": CONFIG2["nnz"], "ranks": CONFIG2["ranks"], "dims": CONFIG2["dims"],
+def workload_config(cfg_id, n):
+    c = CONFIGS[cfg_id]
+    return {"workload": f"config{cfg_id}: {c['desc']}; step = update_all_factors + update_core + RE "
+                        f"(trainer.hpp:121-127)",
+            "nnz": c["nnz"], "ranks": c["ranks"], "dims": c["dims"], "lambda": c["lam"],
+            "core_keep": c["core_keep"],
+            "values": {0: "fp64 U[0,1)", 1: "integers 1..5 as fp64", 2: "N(0,1) rounded to fp32, held as fp64"}[
+                c["values_kind"]],
             "parallelism": (f"rows sharded x{n} (NCCL)" if n > 1 or os.environ.get("VEST_FORCE_SHARDED") == "1"
                             else "single"),
-            "l2": "inputs larger than L2 (per-mode CSF 600 MB vs 126 MB L2)"}
+            "l2": "inputs larger than L2 (per-mode CSF >= 600 MB vs 126 MB L2)"}
+
+
+# ----------------------------------------------------------- roofline ---------
+def dense_delta_flops(ranks, n):
+    """dense-factorised delta cost 2 (|G| + |G|/J_a + ...) over the
+    N-1 contractions of mode n (largest J first)."""
+    G = int(np.prod(ranks))
+    others = sorted((ranks[k] for k in range(len(ranks)) if k != n), reverse=True)
+    d, size = 0, G
+    for Ja in others:
+        d += size
+        size //= Ja
+    return 2 * d
+
+
+def family_models(ranks, nnz, core_live):
+    """Algorithmic (reference-equivalent) flops and compulsory
+    bytes per entry of the two big families: one factor-mode update (averaged
+    over modes) and one whole core sweep."""
+    N = len(ranks)
+    f_fl = np.mean([min(dense_delta_flops(ranks, n), core_live * N) + ranks[n] * (ranks[n] + 1) + 2 * ranks[n]
+                    for n in range(N)])
+    f_by = (N - 1) * 4 + 8
+    c_fl = core_live * (N + 7)
+    c_by = 4 * N + 8 + 16
+    return float(f_fl), float(f_by), float(c_fl), float(c_by)
+
+
+def roofline_for(c, fams, steps, ms_total, peak_tf, hbm_peak, core_live, nnz_local, traffic_db):
+    """Roofline of the dominant kernel family of the step (largest share of
+    the timed region): achieved = algorithmic flops per launch / average launch
+    time (CUDA events on the library stream), against the measured FP64 peak."""
+    ranks = c["ranks"]
+    f_fl, f_by, c_fl, c_by = family_models(ranks, nnz_local, core_live)
+    fac_ms = fams["factor_update"]["ms"] + fams["factor_update_fused_residual"]["ms"]
+    fac_n = fams["factor_update"]["scopes"] + fams["factor_update_fused_residual"]["scopes"]
+    core_ms = fams["core_pass"]["ms"]
+    core_n = fams["core_pass"]["scopes"]
+    if fac_ms >= core_ms and fac_n:
+        avg = fac_ms / fac_n
+        fl, by = f_fl * nnz_local, f_by * nnz_local
+        kernel = "factor-mode update (per mode: " + ("mask-specialised delta + statistics/solve"
+                                                     if c["core_keep"] < 1.0 else "k_rowpass<kStats>") + ")"
+        fam = "factor_update"
+        share = fac_ms / ms_total
+    else:
+        avg = core_ms / max(core_n, 1)
+        sweeps = steps
+        fl = c_fl * nnz_local * sweeps / max(core_n, 1)
+        by = c_by * nnz_local * sweeps / max(core_n, 1)
+        kernel = "core-sweep block pass (per pass; one sweep's algorithmic work spread over its passes)"
+        fam = "core_pass"
+        share = core_ms / ms_total
+    ach = fl / (avg * 1e-3) / 1e12
+    ach_b = by / (avg * 1e-3) / 1e9
+    return {
+        "bound": "fp64", "kernel": kernel, "family": fam, "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+        "frac": ach / peak_tf, "peak_source": "measured live: vest_measure_fp64_peak (DFMA microbenchmark)",
+        "traffic": traffic_db.get(fam), "flops_per_launch": fl, "avg_launch_ms": avg, "step_share": share,
+        "hbm": {"achieved": ach_b, "peak": hbm_peak, "unit": "GB/s", "frac": ach_b / hbm_peak,
+                "bytes_per_launch": by, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+    }
 
 
 # --------------------------------------------------------------- our arm ------
-def run_ours(args, rank, world, local_rank):
-    import torch
-    from paper_1904_02603_b200 import _lib
-    from paper_1904_02603_b200 import sparsetuck as st
-
-    torch.cuda.set_device(local_rank)
-    dist = None
-    # VEST_FORCE_SHARDED=1: the sharded driver + NCCL hooks even at world size 1
-    # (exercises the multi-GPU plumbing on a single GPU; diagnostic only)
-    sharded = world > 1 or os.environ.get("VEST_FORCE_SHARDED") == "1"
-    if sharded:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    L = _lib.lib()
-    cfg = CONFIG2
-    coords, vals = synth(cfg["dims"], cfg["nnz"], cfg["data_seed"])
-    x = st.SparseTensor(cfg["dims"], coords, vals)
-    if sharded:
-        # rows of every mode sharded by nnz-balanced ranges; NCCL exchanges
-        # (paper_1904_02603_b200/sharded.py)
-        from paper_1904_02603_b200 import sharded as sh
-        comm = sh.TorchComm("cuda") if os.environ.get("VEST_TORCH_COMM") == "1" else sh.NcclNative()
-        dev = sh.ShardDevice(x, cfg["ranks"], rank, world, comm, local_rank)
-    else:
-        dev = st.Device(x, cfg["ranks"], local_rank)
-    assert dev.specialised(), "rank-specialised kernels expected for config 2"
-    dev.init_random(cfg["seed"])
+def measure(dev, c, steps, warmup, world, dist, local_rank, L, _lib, torch, families=True):
+    """Timed region: `steps` CD iterations, device-resident, CUDA events on the
+    library stream, barrier + synchronize on both sides, max over ranks."""
     stream = torch.cuda.ExternalStream(dev.stream(), device=torch.device("cuda", local_rank))
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
-    clk = Clocks(local_rank).__enter__()  # sampling starts before warm-up, covers the timed region
-    for _ in range(args.warmup):
-        dev.cd_iteration(cfg["reg"], cfg["lam"])
-    # ---- device-resident timed region
-    L.vest_ctx_profile(dev.h, 1)
+    for _ in range(warmup):
+        dev.cd_iteration(0, c["lam"])
+    L.vest_ctx_profile(dev.h, 1 if families else 0)
     ms_arr = np.zeros(8)
     n_arr = np.zeros(8, np.uint64)
     L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     launches0 = L.vest_launch_count()
-    barrier()
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    res = []
-    for _ in range(args.steps):
-        res.append(dev.cd_iteration(cfg["reg"], cfg["lam"]))
+    res = [dev.cd_iteration(0, c["lam"]) for _ in range(steps)]
     ev1.record(stream)
     torch.cuda.synchronize()
-    clk.__exit__(None, None, None)
-    barrier()
+    if dist is not None:
+        dist.barrier()
     launches = L.vest_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
@@ -293,16 +379,17 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = cfg["nnz"] * args.steps / (ms * 1e-3)  # whole job: the N ranks share the nnz
+    fam_names = ["factor_update", "core_pass", "core_gemm", "core_solve", "residual", "resp", "prune",
+                 "factor_update_fused_residual"]
+    fams = {fam_names[i]: {"ms": float(ms_arr[i]), "scopes": int(n_arr[i])} for i in range(8)}
+    return ms, res, fams, int(launches)
 
-    # ---- prune event (timed separately; not an iteration)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    dev.compute_responsibilities(want=False)
-    counts = dev.prune_step(0.3)
-    prune_ms = (time.perf_counter() - t0) * 1e3
 
-    # ---- e2e through the C-ABI with host buffers
+def measure_e2e(dev, c, steps, dist, torch):
+    """The same iteration through the C-ABI host entry point
+    (vest_cd_iteration_host): the model is copied in from pinned host memory
+    and the updated core and factors are read back inside the timed region."""
+    from paper_1904_02603_b200 import sparsetuck as st
     m_host = dev.get_model()
     pinned = []
 
@@ -318,75 +405,110 @@ def run_ours(args, rank, world, local_rank):
     h2d = m_host.core.nbytes + m_host.core_mask.nbytes + sum(f.nbytes + k.nbytes for f, k in
                                                               zip(m_host.factors, m_host.factor_masks))
     d2h = m_host.core.nbytes + sum(f.nbytes for f in m_host.factors)  # masks are inputs only
-    e2e_steps = max(1, min(args.steps, 5))
-    barrier()
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        dev.cd_iteration_host(m_host, cfg["reg"], cfg["lam"])
+    for _ in range(steps):
+        dev.cd_iteration_host(m_host, 0, c["lam"])
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = cfg["nnz"] * e2e_steps / e2e_s
+    return e2e_s, int(h2d), int(d2h)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_1904_02603_b200 import _lib
+    from paper_1904_02603_b200 import sparsetuck as st
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    # VEST_FORCE_SHARDED=1: the sharded driver + NCCL hooks even at world size 1
+    # (exercises the multi-GPU plumbing on a single GPU; diagnostic only)
+    sharded = world > 1 or os.environ.get("VEST_FORCE_SHARDED") == "1"
+    if sharded:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    L = _lib.lib()
+    cfg_id = args.workload
+    c = CONFIGS[cfg_id]
+    coords, vals = synth(c["dims"], c["nnz"], 1000 + cfg_id, c["values_kind"], c["zipf"])
+    x = st.SparseTensor(c["dims"], coords, vals)
+    del coords, vals
+    if sharded:
+        # rows of every mode sharded by work-balanced ranges; NCCL exchanges
+        # (paper_1904_02603_b200/sharded.py)
+        from paper_1904_02603_b200 import sharded as sh
+        comm = sh.TorchComm("cuda") if os.environ.get("VEST_TORCH_COMM") == "1" else sh.NcclNative()
+        dev = sh.ShardDevice(x, c["ranks"], rank, world, comm, local_rank)
+        nnz_local = dev.local_nnz(len(c["dims"]) - 1)
+    else:
+        dev = st.Device(x, c["ranks"], local_rank)
+        nnz_local = c["nnz"]
+    m0 = model_for(c)
+    core_live = int(np.count_nonzero(m0.core_mask == 0))
+    dev.set_model(m0)
+    clk = Clocks(local_rank).__enter__()  # sampling covers warm-up and the timed region
+    ms, res, fams, launches = measure(dev, c, args.steps, args.warmup, world, dist, local_rank, L, _lib, torch)
+    clk.__exit__(None, None, None)
+    value = c["nnz"] * args.steps / (ms * 1e-3)  # whole job: the N ranks share the nnz
+
+    # ---- e2e through the C-ABI with host buffers (before any prune: same mask)
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_s, h2d, d2h = measure_e2e(dev, c, e2e_steps, dist, torch)
+    e2e_value = c["nnz"] * e2e_steps / e2e_s
+
+    # ---- prune event (timed separately; not an iteration)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dev.compute_responsibilities(want=False)
+    counts = dev.prune_step(0.3)
+    prune_ms = (time.perf_counter() - t0) * 1e3
+    dev.close()
+    del dev, x
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
-    # ---- roofline of the dominant kernel family (factor-row update)
     peak = C.c_double()
     L.vest_measure_fp64_peak(local_rank, C.byref(peak))
-    fam_names = ["factor_update", "core_pass", "core_gemm", "core_solve", "residual", "resp", "prune",
-                 "factor_update_fused_residual"]
-    fams = {fam_names[i]: {"ms": float(ms_arr[i]), "scopes": int(n_arr[i])} for i in range(8)}
-    fl, by = factor_launch_model(cfg["ranks"], cfg["nnz"], modes=len(cfg["ranks"]) - 1)
-    nf = max(int(n_arr[0]), 1)
-    avg_ms = ms_arr[0] / nf
-    achieved_tf = fl / (avg_ms * 1e-3) / 1e12
-    achieved_gbs = by / (avg_ms * 1e-3) / 1e9
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    traffic = None
-    prof_json = os.path.join(ROOT, "profiles", "ncu_factor_update.json")
+    traffic_db = {}
+    prof_json = os.path.join(ROOT, "profiles", "ncu_dominant.json")
     if os.path.exists(prof_json):
         try:
-            traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
+            traffic_db = json.load(open(prof_json)).get(f"config{cfg_id}", {})
         except Exception:
-            traffic = None
-    roofline = {
-        "bound": "fp64", "kernel": "k_rowpass<StaticPolicy<10,10,10>,kStats> (factor-row update, modes 0-1; per launch)",
-        "achieved": achieved_tf, "peak": peak.value, "unit": "TFLOP/s", "frac": achieved_tf / peak.value,
-        "peak_source": "measured live: vest_measure_fp64_peak (DFMA microbenchmark)",
-        "traffic": traffic, "flops_per_launch": fl, "avg_launch_ms": avg_ms,
-        "hbm": {"achieved": achieved_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                "frac": achieved_gbs / peaks.get("hbm_gbs", 6650.0), "bytes_per_launch": by,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-        "step_share": float(ms_arr[0] / ms) if ms > 0 else None,
-    }
+            traffic_db = {}
+    roofline = roofline_for(c, fams, args.steps, ms, peak.value, peaks.get("hbm_gbs", 6650.0), core_live,
+                            nnz_local, traffic_db)
     # whole-iteration FMA roof: reference-equivalent flops of one
     # CD iteration over the whole job vs the measured FP64 peak of all GPUs
-    f_alg = step_flops_per_entry(cfg["ranks"])
+    f_alg = step_flops_per_entry(c["ranks"], core_live)
     step_tf = f_alg * value / 1e12
     roofline["step"] = {"flops_per_entry": f_alg, "achieved": step_tf, "peak": peak.value * world,
                         "unit": "TFLOP/s", "frac": step_tf / (peak.value * world),
                         "note": "SURVEY.md 8(d) F_alg (reference-equivalent work) at the measured rate"}
-    # ---- CPU baseline (rank 0, N = 1 only)
+    # ---- CPU baseline (rank 0, N = 1 only): the reference on a bounded sample
     cpu = None
     if world == 1 and not args.no_cpu:
-        rate, kind, thr, sec = cpu_reference_rate()
+        rate, kind, thr, sec, snnz = cpu_reference_rate(cfg_id)
         cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": kind,
-               "sample": f"one CD iteration of config2 shape with {SAMPLE_NNZ} entries ({sec:.1f} s)"}
+               "sample": f"one CD iteration ({sec:.1f} s) of " + sample_desc(cfg_id, snnz)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config 2 shape)",
-        "config": workload_config(world),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "steps": e2e_steps, "path": "vest_cd_iteration_host: host model in/out (pinned), factors read back behind the later modes"},
-        "gpu_launches": int(launches),
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded; BASELINE config {cfg_id} shape)",
+        "config": workload_config(cfg_id, world),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "path": "vest_cd_iteration_host: host model in/out (pinned)"},
+        "gpu_launches": launches,
         "roofline": roofline,
         "kernel_families_ms": fams,
         "prune_event": {"ms": prune_ms, "rate": 0.3, "counts": [counts.core] + counts.factors},
@@ -394,6 +516,21 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
+    # ---- secondary workload (config 2, the round-1 headline), N = 1 only
+    if world == 1 and args.secondary and args.secondary != cfg_id:
+        c2 = CONFIGS[args.secondary]
+        co, va = synth(c2["dims"], c2["nnz"], 1000 + args.secondary, c2["values_kind"], c2["zipf"])
+        x2 = st.SparseTensor(c2["dims"], co, va)
+        d2 = st.Device(x2, c2["ranks"], local_rank)
+        d2.set_model(model_for(c2))
+        ms2, _, fams2, l2 = measure(d2, c2, 20, 5, 1, None, local_rank, L, _lib, torch, families=False)
+        e2s, hb, db = measure_e2e(d2, c2, 5, None, torch)
+        d2.close()
+        line[f"config{args.secondary}"] = {
+            "workload": workload_config(args.secondary, 1)["workload"], "value": c2["nnz"] * 20 / (ms2 * 1e-3),
+            "ms_per_step": ms2 / 20, "steps": 20, "warmup": 5, "gpu_launches": l2,
+            "e2e": {"value": c2["nnz"] * 5 / e2s, "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db},
+            "step_roof_frac": step_flops_per_entry(c2["ranks"]) * c2["nnz"] * 20 / (ms2 * 1e-3) / 1e12 / peak.value}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -546,6 +683,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--workload", type=int, default=HEADLINE, help="BASELINE config of the headline line")
+    ap.add_argument("--secondary", type=int, default=SECONDARY,
+                    help="BASELINE config measured after the headline as an extra key (0: none)")
     args = ap.parse_args()
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)

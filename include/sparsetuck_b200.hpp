@@ -19,10 +19,12 @@
 // The `threads` arguments are accepted for source compatibility and ignored.
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <map>
 #include <memory>
@@ -120,6 +122,8 @@ namespace b200_detail {
 
 struct Ctx {
   vest_ctx* h = nullptr;
+  std::uint64_t fingerprint = 0;  // content of the tensor the CSF was built from
+  std::uint64_t last_use = 0;
   ~Ctx() {
     if (h) vest_ctx_destroy(h);
   }
@@ -136,22 +140,108 @@ inline std::mutex& registry_mutex() {
   return m;
 }
 
-// Context for (tensor buffers, ranks); created (CSF built on the device) on
-// first use.  An empty tensor gives a model-only context.
-inline vest_ctx* context(const SparseTensor& x, const std::vector<std::size_t>& ranks) {
+// 64-bit content hash of a byte range (8-byte words, multiply-rotate mixing;
+// split across threads, partial hashes combined in order).
+inline std::uint64_t hash_bytes(const void* p, std::size_t bytes) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  auto mix = [](std::uint64_t h, std::uint64_t w) {
+    h ^= w * 0x9E3779B97F4A7C15ull;
+    h = (h << 27) | (h >> 37);
+    return h * 0xBF58476D1CE4E5B9ull + 0x94D049BB133111EBull;
+  };
+  auto range = [&](std::size_t lo, std::size_t hi) {
+    std::uint64_t h = 0x2545F4914F6CDD1Dull ^ (hi - lo);
+    std::size_t i = lo;
+    for (; i + 8 <= hi; i += 8) {
+      std::uint64_t w;
+      std::memcpy(&w, b + i, 8);
+      h = mix(h, w);
+    }
+    std::uint64_t t = 0;
+    if (i < hi) std::memcpy(&t, b + i, hi - i);
+    return mix(h, t);
+  };
+  const std::size_t kPart = std::size_t(1) << 24;  // 16 MB per task
+  const std::size_t parts = (bytes + kPart - 1) / kPart;
+  if (parts <= 1) return range(0, bytes);
+  std::vector<std::uint64_t> ph(parts);
+  const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), (unsigned)parts));
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      for (std::size_t q = t; q < parts; q += nt) ph[q] = range(q * kPart, std::min(bytes, (q + 1) * kPart));
+    });
+  for (auto& th : pool) th.join();
+  std::uint64_t h = 0;
+  for (std::uint64_t v : ph) h = mix(h, v);
+  return h;
+}
+
+inline std::uint64_t fingerprint(const SparseTensor& x) {
+  return hash_bytes(x.coords.data(), x.coords.size() * sizeof(Coord)) * 31 +
+         hash_bytes(x.values.data(), x.values.size() * sizeof(double));
+}
+
+// Device contexts kept at once (least recently used evicted first);
+// SPARSETUCK_B200_MAX_CONTEXTS overrides.
+inline std::size_t max_contexts() {
+  if (const char* env = std::getenv("SPARSETUCK_B200_MAX_CONTEXTS")) {
+    const long v = std::strtol(env, nullptr, 10);
+    if (v > 0) return (std::size_t)v;
+  }
+  return 4;
+}
+
+// Context for (tensor, ranks); created (CSF built on the device) on first
+// use.  The cache is keyed on the buffers AND verified against a content
+// fingerprint on every lookup: a tensor edited in place, or a new tensor whose
+// buffers reuse a freed address, gets a fresh context instead of a stale CSF.
+// An empty tensor gives a model-only context.
+inline std::shared_ptr<Ctx> context(const SparseTensor& x, const std::vector<std::size_t>& ranks) {
   std::lock_guard<std::mutex> g(registry_mutex());
+  static std::uint64_t clock = 0;
+  auto& reg = registry();
   Key k{x.coords.data(), x.values.data(), x.nnz(), x.dims, ranks};
-  auto& slot = registry()[k];
-  if (!slot) {
+  const std::uint64_t fp = fingerprint(x);
+  auto it = reg.find(k);
+  if (it != reg.end() && it->second->fingerprint != fp) {
+    reg.erase(it);  // stale: the buffers at this address hold different data now
+    it = reg.end();
+  }
+  if (it == reg.end()) {
+    while (!reg.empty() && reg.size() >= max_contexts()) {
+      auto lru = reg.begin();
+      for (auto q = reg.begin(); q != reg.end(); ++q)
+        if (q->second->last_use < lru->second->last_use) lru = q;
+      reg.erase(lru);
+    }
     auto c = std::make_shared<Ctx>();
     std::vector<std::uint64_t> d(x.dims.begin(), x.dims.end()), r(ranks.begin(), ranks.end());
     check(vest_ctx_create((int)x.order(), d.data(), x.nnz(), x.coords.data(), x.values.data(), r.data(), 0, &c->h));
-    slot = c;
+    c->fingerprint = fp;
+    it = reg.emplace(k, c).first;
   }
-  return slot->h;
+  it->second->last_use = ++clock;
+  return it->second;  // the caller's reference keeps it alive across an eviction
 }
 
-inline vest_ctx* model_context(const TuckerModel& m) {
+// Number of cached device contexts (tests / diagnostics).
+inline std::size_t cached_contexts() {
+  std::lock_guard<std::mutex> g(registry_mutex());
+  return registry().size();
+}
+
+}  // namespace b200_detail
+
+// Frees every cached device context (their HBM); later calls rebuild them.
+inline void release_device_contexts() {
+  std::lock_guard<std::mutex> g(b200_detail::registry_mutex());
+  b200_detail::registry().clear();
+}
+
+namespace b200_detail {
+
+inline std::shared_ptr<Ctx> model_context(const TuckerModel& m) {
   static std::map<std::pair<std::vector<std::size_t>, std::vector<std::size_t>>, SparseTensor> empties;
   static std::mutex mu;
   const SparseTensor* x;
@@ -178,11 +268,11 @@ inline void pull(vest_ctx* h, TuckerModel& m) {
   check(vest_get_model(h, m.core.data(), m.core_mask.data(), f.data(), k.data()));
 }
 
-inline vest_ctx* bind(const TuckerModel& m, const SparseTensor& x) {
+inline std::shared_ptr<Ctx> bind(const TuckerModel& m, const SparseTensor& x) {
   if (m.dims != x.dims) throw std::invalid_argument("model/tensor shape mismatch");
-  vest_ctx* h = context(x, m.ranks);
-  push(h, m);
-  return h;
+  auto c = context(x, m.ranks);
+  push(c->h, m);
+  return c;
 }
 
 }  // namespace b200_detail
@@ -199,7 +289,8 @@ struct ModeIndex {
 };
 
 inline ModeIndex build_mode_index(const SparseTensor& x) {
-  vest_ctx* h = b200_detail::context(x, std::vector<std::size_t>(x.order(), 1));
+  const auto hold = b200_detail::context(x, std::vector<std::size_t>(x.order(), 1));
+  vest_ctx* h = hold->h;
   ModeIndex idx;
   idx.offsets.resize(x.order());
   idx.ids.resize(x.order());
@@ -260,7 +351,8 @@ inline std::vector<double> predict(const TuckerModel& m, std::span<const Coord> 
   const std::size_t n = m.order();
   if (n == 0 || flat_coords.size() % n != 0)
     throw std::invalid_argument("coordinate buffer must hold order() values per query");
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   std::vector<double> out(flat_coords.size() / n);
   b200_detail::check(vest_predict(h, flat_coords.data(), out.size(), out.data()));
@@ -274,6 +366,17 @@ inline double reconstruct_entry(const TuckerModel& m, std::span<const Coord> at)
   return reconstruct_entry(m, at.data());
 }
 
+// partial_reconstruct (tucker_model.hpp:136-154): the reconstruction restricted
+// to the core cells whose mode-`mode` index is j (bit-identical).
+inline double partial_reconstruct(const TuckerModel& m, const Coord* at, std::size_t mode, std::size_t j) {
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
+  b200_detail::push(h, m);
+  double out = 0.0;
+  b200_detail::check(vest_partial_reconstruct(h, at, 1, (int)mode, j, &out));
+  return out;
+}
+
 // Residuals / compute_residuals / reconstruction_error (tucker_model.hpp:161-188)
 struct Residuals {
   std::vector<double> r;
@@ -283,7 +386,8 @@ struct Residuals {
 };
 
 inline Residuals compute_residuals(const TuckerModel& m, const SparseTensor& x, int /*threads*/ = 1) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   Residuals res;
   res.r.resize(x.nnz());
   b200_detail::check(vest_compute_residuals(h, res.r.data(), &res.sum_sq, &res.x_norm, &res.re));
@@ -291,7 +395,8 @@ inline Residuals compute_residuals(const TuckerModel& m, const SparseTensor& x, 
 }
 
 inline double reconstruction_error(const TuckerModel& m, const SparseTensor& x) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   double re = 0.0;
   b200_detail::check(vest_compute_residuals(h, nullptr, nullptr, nullptr, &re));
   return re;
@@ -299,14 +404,16 @@ inline double reconstruction_error(const TuckerModel& m, const SparseTensor& x) 
 
 // sparsity / masked_fraction (tucker_model.hpp:192-207)
 inline double sparsity(const TuckerModel& m) {
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   double z = 0, k = 0;
   b200_detail::check(vest_sparsity(h, &z, &k));
   return z;
 }
 inline double masked_fraction(const TuckerModel& m) {
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   double z = 0, k = 0;
   b200_detail::check(vest_sparsity(h, &z, &k));
@@ -315,7 +422,8 @@ inline double masked_fraction(const TuckerModel& m) {
 
 // normalize_columns (tucker_model.hpp:212-236)
 inline void normalize_columns(TuckerModel& m) {
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   b200_detail::check(vest_normalize_columns(h));
   b200_detail::pull(h, m);
@@ -324,7 +432,8 @@ inline void normalize_columns(TuckerModel& m) {
 // ------------------------------------------------------------- updates -------
 // compute_delta (updates.hpp:35-59)
 inline void compute_delta(const TuckerModel& m, const Coord* at, std::size_t mode, std::span<double> out) {
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   b200_detail::check(vest_compute_delta(h, at, (int)mode, out.data()));
 }
@@ -334,36 +443,99 @@ inline std::vector<double> compute_delta(const TuckerModel& m, const Coord* at, 
   return out;
 }
 
-// update_factor_row_lf / _l1 (updates.hpp:88-151)
+// RowUpdateScratch (updates.hpp:17-30): per-call workspace of one row update.
+struct RowUpdateScratch {
+  std::vector<double> delta;   // J (the slice's last entry, as the reference leaves it)
+  std::vector<double> gram;    // J x J, gram[t*J+j] = sum_e delta(t)*delta(j)
+  std::vector<double> xdelta;  // J, sum_e x[e]*delta(j)
+
+  void reset(std::size_t J) {
+    delta.assign(J, 0.0);
+    gram.assign(J * J, 0.0);
+    xdelta.assign(J, 0.0);
+  }
+};
+
+namespace b200_detail {
+inline void row_stats(vest_ctx* h, std::size_t mode, std::size_t i, std::size_t J, RowUpdateScratch& s) {
+  s.reset(J);
+  check(vest_compute_row_stats(h, (int)mode, i, s.gram.data(), s.xdelta.data(), s.delta.data()));
+}
+// only row i of factor `mode` changes in a row update: read back just that row
+inline void pull_row(vest_ctx* h, TuckerModel& m, std::size_t mode, std::size_t i) {
+  check(vest_get_factor_rows(h, (int)mode, i, 1, m.factors[mode].data() + i * m.ranks[mode]));
+}
+inline void check_row(const TuckerModel& m, std::size_t mode, std::size_t i) {
+  if (mode >= m.order() || i >= m.dims[mode]) throw std::invalid_argument("row out of range");
+}
+}  // namespace b200_detail
+
+// compute_row_stats (updates.hpp:64-79): gram and xdelta over the row's
+// observed entries, bit-identical to the reference (device, reference order).
+inline void compute_row_stats(const TuckerModel& m, const SparseTensor& x, const ModeIndex&, std::size_t mode,
+                              std::size_t i, RowUpdateScratch& s) {
+  b200_detail::check_row(m, mode, i);
+  const auto hold = b200_detail::bind(m, x);
+  b200_detail::row_stats(hold->h, mode, i, m.ranks[mode], s);
+}
+
+// update_factor_row_lf / _l1 (updates.hpp:88-151); the scratch overloads
+// leave the row's statistics in `s` as the reference does.
+inline void update_factor_row_lf(TuckerModel& m, const SparseTensor& x, const ModeIndex& idx, std::size_t mode,
+                                 std::size_t i, double lambda, RowUpdateScratch& s) {
+  b200_detail::check_row(m, mode, i);
+  if (!idx.offsets.empty() && idx.slice(mode, static_cast<Coord>(i)).empty()) return;  // updates.hpp:91
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
+  b200_detail::row_stats(h, mode, i, m.ranks[mode], s);
+  b200_detail::check(vest_update_factor_row(h, VEST_LF, (int)mode, i, lambda));
+  b200_detail::pull_row(h, m, mode, i);
+}
+inline void update_factor_row_l1(TuckerModel& m, const SparseTensor& x, const ModeIndex&, std::size_t mode,
+                                 std::size_t i, double lambda, RowUpdateScratch& s) {
+  b200_detail::check_row(m, mode, i);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
+  b200_detail::row_stats(h, mode, i, m.ranks[mode], s);
+  b200_detail::check(vest_update_factor_row(h, VEST_L1, (int)mode, i, lambda));
+  b200_detail::pull_row(h, m, mode, i);
+}
 inline void update_factor_row_lf(TuckerModel& m, const SparseTensor& x, const ModeIndex&, std::size_t mode,
                                  std::size_t i, double lambda) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  b200_detail::check_row(m, mode, i);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   b200_detail::check(vest_update_factor_row(h, VEST_LF, (int)mode, i, lambda));
-  b200_detail::pull(h, m);
+  b200_detail::pull_row(h, m, mode, i);
 }
 inline void update_factor_row_l1(TuckerModel& m, const SparseTensor& x, const ModeIndex&, std::size_t mode,
                                  std::size_t i, double lambda) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  b200_detail::check_row(m, mode, i);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   b200_detail::check(vest_update_factor_row(h, VEST_L1, (int)mode, i, lambda));
-  b200_detail::pull(h, m);
+  b200_detail::pull_row(h, m, mode, i);
 }
 
 // update_all_factors (updates.hpp:157-175)
 inline void update_all_factors(TuckerModel& m, const SparseTensor& x, const ModeIndex&, Regularizer reg,
                                double lambda, int /*threads*/ = 1) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   b200_detail::check(vest_update_all_factors(h, reg == Regularizer::LF ? VEST_LF : VEST_L1, lambda));
   b200_detail::pull(h, m);
 }
 
 // update_core_lf / _l1 (updates.hpp:253-262)
 inline void update_core_lf(TuckerModel& m, const SparseTensor& x, double lambda, int /*threads*/ = 1) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   b200_detail::check(vest_update_core(h, VEST_LF, lambda));
   b200_detail::pull(h, m);
 }
 inline void update_core_l1(TuckerModel& m, const SparseTensor& x, double lambda, int /*threads*/ = 1) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   b200_detail::check(vest_update_core(h, VEST_L1, lambda));
   b200_detail::pull(h, m);
 }
@@ -430,7 +602,8 @@ struct ResponsibilityTable {
 
 inline ResponsibilityTable compute_responsibilities(const TuckerModel& m, const SparseTensor& x, const ModeIndex&,
                                                     const Residuals&, int /*threads*/ = 1) {
-  vest_ctx* h = b200_detail::bind(m, x);
+  const auto hold = b200_detail::bind(m, x);
+  vest_ctx* h = hold->h;
   ResponsibilityTable t;
   t.core.resize(m.core_size());
   t.factors.resize(m.order());
@@ -467,7 +640,8 @@ struct PruneCounts {
 
 inline PruneCounts prune_step(TuckerModel& m, const ResponsibilityTable& t, double pr) {
   if (!(pr >= 0.0 && pr < 1.0)) throw std::invalid_argument("prune rate must be in [0, 1)");
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   std::vector<const double*> f(m.order());
   for (std::size_t n = 0; n < m.order(); ++n) f[n] = t.factors[n].data();
@@ -627,7 +801,8 @@ inline FitResult fit(const SparseTensor& x, const TrainConfig& cfg) {
 // evaluate_test (trainer.hpp:188-190)
 inline double evaluate_test(const TuckerModel& m, const SparseTensor& test) {
   if (m.dims != test.dims) throw std::invalid_argument("model/tensor shape mismatch");
-  vest_ctx* h = b200_detail::model_context(m);
+  const auto hold = b200_detail::model_context(m);
+  vest_ctx* h = hold->h;
   b200_detail::push(h, m);
   double re = 0.0;
   b200_detail::check(vest_evaluate(h, test.coords.data(), test.values.data(), test.nnz(), &re));

@@ -166,6 +166,22 @@ int vest_cd_iteration_host(vest_ctx* ctx, double* core, const uint8_t* core_mask
                            const uint8_t* const* factor_masks, int reg, double lambda, double* re);
 /* compute_delta (updates.hpp:35-52) at one coordinate. */
 int vest_compute_delta(vest_ctx* ctx, const uint32_t* at, int mode, double* out);
+/* compute_row_stats (updates.hpp:64-79): gram (J*J, gram[t*J+j]) and xdelta
+ * (J) of row `row` of `mode` over its observed entries in ascending entry id,
+ * skipping delta_t == 0, with the reference's rounding (bit-identical).
+ * last_delta (J, may be NULL) receives the delta of the slice's last entry --
+ * what RowUpdateScratch::delta holds after the reference call (zeros for an
+ * empty slice). */
+int vest_compute_row_stats(vest_ctx* ctx, int mode, uint64_t row, double* gram, double* xdelta,
+                           double* last_delta);
+/* partial_reconstruct (tucker_model.hpp:136-154) at nq coordinates: the
+ * reconstruction restricted to the core cells with beta_mode == j, reference
+ * cell order and rounding (bit-identical). */
+int vest_partial_reconstruct(vest_ctx* ctx, const uint32_t* coords, uint64_t nq, int mode, uint64_t j,
+                             double* out);
+/* Rows [row_lo, row_lo + nrows) of factor `mode` (row-major, J per row) to
+ * host memory: the per-row drop-in calls read back only what they changed. */
+int vest_get_factor_rows(vest_ctx* ctx, int mode, uint64_t row_lo, uint64_t nrows, double* out);
 /* predict (trainer.hpp:172-185): reconstruction at nq coordinates. */
 int vest_predict(vest_ctx* ctx, const uint32_t* coords, uint64_t nq, double* out);
 /* evaluate_test (trainer.hpp:188-190): relative error on held-out entries. */

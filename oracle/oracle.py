@@ -68,7 +68,11 @@ def _lib(kind: str) -> tuple[C.CDLL, str]:
             "normalize_columns": (C.c_int, [vp]),
             "frobenius_norm": (C.c_double, [vp]),
             "cd_iteration": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, _f64p]),
+            "row_stats": (C.c_int, [vp, C.c_int, C.c_uint64, _f64p, _f64p, _f64p]),
+            "partial_reconstruct": (C.c_int, [vp, _u32p, C.c_uint64, C.c_int, C.c_uint64, _f64p]),
         }
+        if kind == "port":
+            sig["update_factor_mode"] = (C.c_int, [vp, C.c_int, C.c_int, C.c_double, C.c_int])
         for name, (res, args) in sig.items():
             fn = getattr(lib, p + name)
             fn.restype = res
@@ -173,6 +177,24 @@ class Session:
 
     def update_factor_row(self, reg: int, mode: int, row: int, lam: float):
         self._check(self._f("update_factor_row")(self.h, reg, mode, row, lam))
+
+    def update_factor_mode(self, reg: int, mode: int, lam: float, threads: int = 1):
+        """One mode of update_all_factors (port only)."""
+        self._check(self._f("update_factor_mode")(self.h, reg, mode, lam, threads))
+
+    def row_stats(self, mode: int, row: int):
+        """compute_row_stats (updates.hpp:64-79) -> (delta, gram J x J, xdelta)."""
+        J = int(self.ranks[mode])
+        d, g, x = np.zeros(J), np.zeros(J * J), np.zeros(J)
+        self._check(self._f("row_stats")(self.h, mode, row, _ptr(d, _f64p), _ptr(g, _f64p), _ptr(x, _f64p)))
+        return d, g.reshape(J, J), x
+
+    def partial_reconstruct(self, coords, mode: int, j: int):
+        c = np.ascontiguousarray(coords, np.uint32).reshape(-1)
+        nq = len(c) // self.order
+        out = np.zeros(max(nq, 1), np.float64)
+        self._check(self._f("partial_reconstruct")(self.h, _ptr(c, _u32p), nq, mode, j, _ptr(out, _f64p)))
+        return out[:nq]
 
     def update_all_factors(self, reg: int, lam: float, threads: int = 1):
         self._check(self._f("update_all_factors")(self.h, reg, lam, threads))

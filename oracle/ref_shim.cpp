@@ -153,6 +153,24 @@ int vr_update_factor_row(void* p, int reg, int mode, uint64_t row, double lambda
   });
 }
 
+int vr_row_stats(void* p, int mode, uint64_t row, double* delta, double* gram, double* xdelta) {
+  auto* s = static_cast<Session*>(p);
+  return guard([&] {
+    RowUpdateScratch sc;
+    compute_row_stats(s->m, s->x, s->idx, mode, row, sc);
+    std::memcpy(delta, sc.delta.data(), sc.delta.size() * sizeof(double));
+    std::memcpy(gram, sc.gram.data(), sc.gram.size() * sizeof(double));
+    std::memcpy(xdelta, sc.xdelta.data(), sc.xdelta.size() * sizeof(double));
+  });
+}
+
+int vr_partial_reconstruct(const void* p, const uint32_t* at, uint64_t nq, int mode, uint64_t j, double* out) {
+  const auto* s = static_cast<const Session*>(p);
+  return guard([&] {
+    for (uint64_t q = 0; q < nq; ++q) out[q] = partial_reconstruct(s->m, at + q * s->m.order(), mode, j);
+  });
+}
+
 int vr_update_all_factors(void* p, int reg, double lambda, int threads) {
   auto* s = static_cast<Session*>(p);
   return guard([&] {

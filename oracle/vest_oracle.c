@@ -300,6 +300,92 @@ static void compute_delta(const vo_session* s, const uint32_t* at, int mode, dou
   } while (advance(beta, s->ranks, n));
 }
 
+/* The nonzero core cells in row-major order with their multi-indices: the
+ * cells compute_delta / reconstruct_entry do not skip (updates.hpp:44,
+ * tucker_model.hpp:121).  Iterating this list instead of the odometer visits
+ * the same cells in the same order with the same arithmetic (bit-identical);
+ * it only saves the skipped iterations at BASELINE sizes (config 4: 411 of
+ * 4096 cells). */
+typedef struct {
+  uint64_t n;
+  double* g;
+  uint16_t* beta; /* n * order */
+} cell_list;
+
+static cell_list nonzero_cells(const vo_session* s) {
+  cell_list c;
+  c.n = 0;
+  c.g = (double*)malloc((s->core_size + 1) * sizeof(double));
+  c.beta = (uint16_t*)malloc((s->core_size + 1) * s->n * sizeof(uint16_t));
+  uint64_t beta[VO_MAXN] = {0};
+  uint64_t lin = 0;
+  do {
+    if (s->core[lin] != 0.0) {
+      c.g[c.n] = s->core[lin];
+      for (int k = 0; k < s->n; ++k) c.beta[c.n * s->n + k] = (uint16_t)beta[k];
+      ++c.n;
+    }
+    ++lin;
+  } while (advance(beta, s->ranks, s->n));
+  return c;
+}
+
+static void free_cells(cell_list* c) {
+  free(c->g);
+  free(c->beta);
+}
+
+static void compute_delta_cells(const vo_session* s, const cell_list* c, const uint32_t* at, int mode, double* out) {
+  const int n = s->n;
+  const uint64_t J = s->ranks[mode];
+  for (uint64_t j = 0; j < J; ++j) out[j] = 0.0;
+  for (uint64_t q = 0; q < c->n; ++q) {
+    const uint16_t* b = c->beta + q * n;
+    double p = c->g[q];
+    for (int k = 0; k < n; ++k)
+      if (k != mode) p *= s->factors[k][at[k] * s->ranks[k] + b[k]];
+    out[b[mode]] += p;
+  }
+}
+
+static double reconstruct_cells(const vo_session* s, const cell_list* c, const uint32_t* at) {
+  const int n = s->n;
+  double acc = 0.0;
+  for (uint64_t q = 0; q < c->n; ++q) {
+    const uint16_t* b = c->beta + q * n;
+    double p = c->g[q];
+    for (int k = 0; k < n; ++k) p *= s->factors[k][at[k] * s->ranks[k] + b[k]];
+    acc += p;
+  }
+  return acc;
+}
+
+/* partial_reconstruct (tucker_model.hpp:136-154) */
+int vo_partial_reconstruct(const vo_session* s, const uint32_t* at, uint64_t nq, int mode, uint64_t j,
+                           double* out) {
+  if (mode < 0 || mode >= s->n) return fail(1, "mode out of range");
+  const int n = s->n;
+  for (uint64_t q = 0; q < nq; ++q) {
+    const uint32_t* a = at + q * n;
+    uint64_t beta[VO_MAXN] = {0};
+    double acc = 0.0;
+    uint64_t lin = 0;
+    do {
+      if (beta[mode] == j) {
+        const double g = s->core[lin];
+        if (g != 0.0) {
+          double p = g;
+          for (int k = 0; k < n; ++k) p *= s->factors[k][a[k] * s->ranks[k] + beta[k]];
+          acc += p;
+        }
+      }
+      ++lin;
+    } while (advance(beta, s->ranks, n));
+    out[q] = acc;
+  }
+  return 0;
+}
+
 int vo_compute_delta(const vo_session* s, const uint32_t* at, int mode, double* out) {
   if (mode < 0 || mode >= s->n) return fail(1, "mode out of range");
   compute_delta(s, at, mode, out);
@@ -308,7 +394,7 @@ int vo_compute_delta(const vo_session* s, const uint32_t* at, int mode, double* 
 
 /* compute_row_stats (updates.hpp:64-79); delta/gram/xdelta are the
  * RowUpdateScratch buffers (:20-30). */
-static void row_stats(const vo_session* s, int mode, uint64_t i, double* delta, double* gram,
+static void row_stats(const vo_session* s, const cell_list* cl, int mode, uint64_t i, double* delta, double* gram,
                       double* xdelta) {
   const uint64_t J = s->ranks[mode];
   for (uint64_t t = 0; t < J; ++t) delta[t] = 0.0, xdelta[t] = 0.0;
@@ -318,7 +404,7 @@ static void row_stats(const vo_session* s, int mode, uint64_t i, double* delta, 
   slice(s, mode, i, &ids, &len);
   for (uint64_t q = 0; q < len; ++q) {
     const uint32_t e = ids[q];
-    compute_delta(s, entry(s, e), mode, delta);
+    compute_delta_cells(s, cl, entry(s, e), mode, delta);
     const double xv = s->values[e];
     for (uint64_t t = 0; t < J; ++t) {
       const double dt = delta[t];
@@ -331,11 +417,11 @@ static void row_stats(const vo_session* s, int mode, uint64_t i, double* delta, 
 }
 
 /* update_factor_row_lf (updates.hpp:88-106) / update_factor_row_l1 (:113-139) */
-static void update_row(vo_session* s, int reg, int mode, uint64_t i, double lambda, double* delta,
-                       double* gram, double* xdelta) {
+static void update_row(vo_session* s, const cell_list* cl, int reg, int mode, uint64_t i, double lambda,
+                       double* delta, double* gram, double* xdelta) {
   const uint64_t J = s->ranks[mode];
   if (reg == 0 && s->offsets[mode][i + 1] == s->offsets[mode][i]) return;
-  row_stats(s, mode, i, delta, gram, xdelta);
+  row_stats(s, cl, mode, i, delta, gram, xdelta);
   double* row = s->factors[mode] + i * J;
   const uint8_t* mask = s->fmasks[mode] + i * J;
   for (uint64_t j = 0; j < J; ++j) {
@@ -372,28 +458,47 @@ int vo_update_factor_row(vo_session* s, int reg, int mode, uint64_t row, double 
   if (mode < 0 || mode >= s->n || row >= s->dims[mode]) return fail(1, "row out of range");
   const uint64_t J = s->ranks[mode];
   double* buf = (double*)malloc((J * J + 2 * J) * sizeof(double));
-  update_row(s, reg, mode, row, lambda, buf, buf + J, buf + J + J * J);
+  cell_list cl = nonzero_cells(s);
+  update_row(s, &cl, reg, mode, row, lambda, buf, buf + J, buf + J + J * J);
+  free_cells(&cl);
   free(buf);
+  s->have_res = s->have_table = 0;
+  return 0;
+}
+
+/* compute_row_stats (updates.hpp:64-79) into RowUpdateScratch-shaped buffers */
+int vo_row_stats(vo_session* s, int mode, uint64_t row, double* delta, double* gram, double* xdelta) {
+  if (mode < 0 || mode >= s->n || row >= s->dims[mode]) return fail(1, "row out of range");
+  cell_list cl = nonzero_cells(s);
+  row_stats(s, &cl, mode, row, delta, gram, xdelta);
+  free_cells(&cl);
+  return 0;
+}
+
+/* One mode of update_all_factors (updates.hpp:162-173): the rows of `mode`
+ * in parallel (independent within a mode). */
+int vo_update_factor_mode(vo_session* s, int reg, int mode, double lambda, int threads) {
+  if (mode < 0 || mode >= s->n) return fail(1, "mode out of range");
+  const int T = threads > 0 ? threads : 1;
+  const long rows = (long)s->dims[mode];
+  const uint64_t J = s->ranks[mode];
+  cell_list cl = nonzero_cells(s);
+#pragma omp parallel num_threads(T)
+  {
+    double* buf = (double*)malloc((J * J + 2 * J) * sizeof(double));
+#pragma omp for schedule(dynamic, 8)
+    for (long i = 0; i < rows; ++i)
+      update_row(s, &cl, reg, mode, (uint64_t)i, lambda, buf, buf + J, buf + J + J * J);
+    free(buf);
+  }
+  free_cells(&cl);
   s->have_res = s->have_table = 0;
   return 0;
 }
 
 /* update_all_factors (updates.hpp:157-175) */
 int vo_update_all_factors(vo_session* s, int reg, double lambda, int threads) {
-  const int T = threads > 0 ? threads : 1;
-  for (int mode = 0; mode < s->n; ++mode) {
-    const long rows = (long)s->dims[mode];
-    const uint64_t J = s->ranks[mode];
-#pragma omp parallel num_threads(T)
-    {
-      double* buf = (double*)malloc((J * J + 2 * J) * sizeof(double));
-#pragma omp for schedule(dynamic, 8)
-      for (long i = 0; i < rows; ++i)
-        update_row(s, reg, mode, (uint64_t)i, lambda, buf, buf + J, buf + J + J * J);
-      free(buf);
-    }
-  }
-  s->have_res = s->have_table = 0;
+  for (int mode = 0; mode < s->n; ++mode) vo_update_factor_mode(s, reg, mode, lambda, threads);
   return 0;
 }
 
@@ -403,8 +508,12 @@ int vo_update_core(vo_session* s, int reg, double lambda, int threads) {
   const long nnz = (long)s->nnz;
   const int n = s->n;
   double* recon = (double*)malloc((s->nnz + 1) * sizeof(double));
+  {
+    cell_list cl = nonzero_cells(s);
 #pragma omp parallel for schedule(static) num_threads(T)
-  for (long e = 0; e < nnz; ++e) recon[e] = reconstruct_entry(s, entry(s, e));
+    for (long e = 0; e < nnz; ++e) recon[e] = reconstruct_cells(s, &cl, entry(s, e));
+    free_cells(&cl);
+  }
   double* prod = (double*)malloc((s->nnz + 1) * sizeof(double));
   uint64_t beta[VO_MAXN] = {0};
   uint64_t lin = 0;
@@ -464,8 +573,10 @@ int vo_compute_residuals(vo_session* s, int threads, double* r_out, double* sum_
   const double xn = vo_frobenius_norm(s);
   if (xn == 0.0) return fail(1, "zero-norm tensor");
   const long nnz = (long)s->nnz;
+  cell_list cl = nonzero_cells(s);
 #pragma omp parallel for schedule(static) num_threads(T)
-  for (long e = 0; e < nnz; ++e) s->r[e] = s->values[e] - reconstruct_entry(s, entry(s, e));
+  for (long e = 0; e < nnz; ++e) s->r[e] = s->values[e] - reconstruct_cells(s, &cl, entry(s, e));
+  free_cells(&cl);
   double acc = 0.0;
   for (long e = 0; e < nnz; ++e) acc += s->r[e] * s->r[e];
   s->sum_sq = acc;
@@ -521,6 +632,7 @@ static void factor_resp(vo_session* s, int mode, int T, double* resp) {
   if (s->re == 0.0) return;
   const double x2 = s->x_norm * s->x_norm;
   const double re2 = s->re * s->re;
+  cell_list cl = nonzero_cells(s);
 #pragma omp parallel num_threads(T)
   {
     double* delta = (double*)malloc(J * sizeof(double));
@@ -533,7 +645,7 @@ static void factor_resp(vo_session* s, int mode, int T, double* resp) {
       slice(s, mode, (uint64_t)i, &ids, &len);
       for (uint64_t q = 0; q < len; ++q) {
         const uint32_t e = ids[q];
-        compute_delta(s, entry(s, e), mode, delta);
+        compute_delta_cells(s, &cl, entry(s, e), mode, delta);
         const double r = s->r[e];
         for (uint64_t j = 0; j < J; ++j) {
           const double p = delta[j] * s->factors[mode][(uint64_t)i * J + j];
@@ -550,6 +662,7 @@ static void factor_resp(vo_session* s, int mode, int T, double* resp) {
     free(delta);
     free(acc);
   }
+  free_cells(&cl);
 }
 
 /* compute_responsibilities (pruning.hpp:181-191) */

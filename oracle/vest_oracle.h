@@ -60,6 +60,13 @@ int vo_reconstruct(const vo_session* s, const uint32_t* at, uint64_t nq, double*
 /* reg: 0 = LF (ridge), 1 = L1 (lasso)  (updates.hpp:15) */
 int vo_update_factor_row(vo_session* s, int reg, int mode, uint64_t row, double lambda);
 int vo_update_all_factors(vo_session* s, int reg, double lambda, int threads);
+/* one mode of update_all_factors (updates.hpp:162-173) */
+int vo_update_factor_mode(vo_session* s, int reg, int mode, double lambda, int threads);
+/* compute_row_stats (updates.hpp:64-79): RowUpdateScratch delta (J), gram (J*J), xdelta (J) */
+int vo_row_stats(vo_session* s, int mode, uint64_t row, double* delta, double* gram, double* xdelta);
+/* partial_reconstruct (tucker_model.hpp:136-154) at nq coordinates */
+int vo_partial_reconstruct(const vo_session* s, const uint32_t* at, uint64_t nq, int mode, uint64_t j,
+                           double* out);
 int vo_update_core(vo_session* s, int reg, double lambda, int threads);
 
 /* compute_residuals (tucker_model.hpp:168-183).  Stores r in the session

@@ -52,6 +52,9 @@ SIGNATURES = {
                                          f64p]),
     "vest_compute_delta": (C.c_int, [vp, u32p, C.c_int, f64p]),
     "vest_predict": (C.c_int, [vp, u32p, C.c_uint64, f64p]),
+    "vest_compute_row_stats": (C.c_int, [vp, C.c_int, C.c_uint64, f64p, f64p, f64p]),
+    "vest_partial_reconstruct": (C.c_int, [vp, u32p, C.c_uint64, C.c_int, C.c_uint64, f64p]),
+    "vest_get_factor_rows": (C.c_int, [vp, C.c_int, C.c_uint64, C.c_uint64, f64p]),
     "vest_evaluate": (C.c_int, [vp, u32p, f64p, C.c_uint64, f64p]),
     "vest_compute_responsibilities": (C.c_int, [vp, f64p, C.POINTER(f64p), f64p]),
     "vest_prune_step": (C.c_int, [vp, C.c_double, f64p, C.POINTER(f64p), u64p]),

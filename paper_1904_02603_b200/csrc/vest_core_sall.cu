@@ -868,7 +868,10 @@ __global__ void __launch_bounds__(32) k_core_solve_g(const double* Ha, const dou
       s += -2.0 * warp_sum(d) + 2.0 * quad(bufA, nq, dla, dgb) + quad(bufB, nq, dlb, dgb);
     }
   }
-  if (s_out && lane == 0) *s_out = s;
+  if (s_out && lane == 0) {
+    s_out[0] = s;
+    s_out[1] = C[2 * nq];  // the sum before the group's update (cancellation check, sum_from_quadratic_form)
+  }
 }
 
 // --------------------------------------------------------------- dispatch --
@@ -1086,17 +1089,33 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
     prev[1] = gr.p[1];
   }
   // r lacks the last group's update until someone reads it (core_apply_pending)
-  check(cudaMemcpyAsync(c.h_small, c.d_small, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "sum readback");
-  if (!c.capturing) {  // a captured iteration reads the sum after the graph launch
-    check(cudaStreamSynchronize(c.stream), "sum sync");
-    c.sum_sq = std::max(0.0, c.h_small[0]);
-    c.re = std::sqrt(c.sum_sq) / c.x_norm;
-  }
+  check(cudaMemcpyAsync(c.h_small, c.d_small, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "sum readback");
   c.r_valid = false;
   c.r_fresh = false;
   c.r_pending[0] = prev[0];
   c.r_pending[1] = prev[1];
   c.r_pending_ops = ops_;
+  if (!c.capturing) {  // a captured iteration reads the sum after the graph launch
+    check(cudaStreamSynchronize(c.stream), "sum sync");
+    sum_from_quadratic_form(c);
+  }
+}
+
+// The sum of squared residuals after the sweep from the last group's
+// statistics, s' = s - 2 dg.C + dg^T H dg (h_small[0]; h_small[1] = s).  When
+// s' cancels to a small fraction of s (a near-exact fit) its relative error
+// grows like s / s', so the pending update is applied and the sum recomputed
+// exactly from the residuals, as the reference's compute_residuals
+// (tucker_model.hpp:168-183) would give: the RE drives StopController
+// (pruning.hpp:45-81) and the convergence test (trainer.hpp:152).
+void sum_from_quadratic_form(Ctx& c) {
+  const double s1 = c.h_small[0], s0 = c.h_small[1];
+  if (!(s1 >= kQuadCancel * s0) || s0 <= 0.0) {
+    core_apply_pending(c);
+    return;
+  }
+  c.sum_sq = s1;
+  c.re = std::sqrt(c.sum_sq) / c.x_norm;
 }
 
 // Apply the deferred last-group update to r (and recompute sum r^2 exactly).

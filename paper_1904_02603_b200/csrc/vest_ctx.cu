@@ -376,7 +376,10 @@ static RowPassArgs row_args(Ctx& c, int mode) {
 }
 
 static cudaError_t run_rows(Ctx& c, const RowPassArgs& a, int kind, uint32_t nchunks) {
-  if (c.ops && !c.force_generic) return c.ops->rowpass(a, kind, nchunks, c.stream);
+  if (c.ops && !c.force_generic) {
+    ConstBankLease lease(c);
+    return c.ops->rowpass(a, kind, nchunks, c.stream);
+  }
   return launch_rowpass_generic(a, kind, nchunks, c.stream);
 }
 
@@ -405,7 +408,11 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
     {
       ProfScope ps(c, fuse_d ? kProfFactorFused : kProfFactor);
       sparse_delta(c, mode, p0, p1 - p0, c.d_delta);
-      check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream), "factor update (delta)");
+      {
+        ConstBankLease lease(c);
+        check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream),
+              "factor update (delta)");
+      }
       if (reg == 1) l1_empty_rows(c, mode, lambda);
     }
     c.r_valid = false;
@@ -422,6 +429,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
         ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, mdd.nchunks + 1);
         b.chunk_out = c.d_chunk_sum;
         ProfScope ps(c, kProfResid);
+        ConstBankLease lease(c);
         check(launch_rowpass_delta(b, kResid, b.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream), "heavy-row residual");
       }
       c.r_fresh = true;
@@ -439,6 +447,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
       bg.csf.chunks = mdd.d_chunks_big;
       bg.csf.nchunks = mdd.nchunks_big;
       check(run_rows(c, bg, kStats, bg.csf.nchunks), "factor update");
+      ConstBankLease lease(c);
       check(c.ops->rowtiny(a, mdd.d_tiny, mdd.ntiny, c.stream), "factor update (short rows)");
     } else {
       check(run_rows(c, a, kStats, a.csf.nchunks), "factor update");
@@ -703,6 +712,72 @@ __global__ void k_delta_one(DevModel m, const uint32_t* at, int mode, double* ou
   }
 }
 
+__global__ void k_partial_recon(DevModel m, const uint32_t* coords, uint64_t nq, int mode, uint32_t j, double* out) {
+  // partial_reconstruct (tucker_model.hpp:136-154): cells with beta_mode == j
+  // in row-major order, zeros skipped, p = g * a_0 * ... * a_{N-1}
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* at = coords + q * m.N;
+    double acc = 0.0;
+    for (int lin = 0; lin < m.G; ++lin) {
+      const uint32_t b = m.cellbeta[lin];
+      if (((b >> (4 * mode)) & 15u) != j) continue;
+      const double g = m.core[lin];
+      if (g == 0.0) continue;
+      double p = g;
+      for (int k = 0; k < m.N; ++k) p = __dmul_rn(p, m.factor[k][(size_t)at[k] * m.ld[k] + ((b >> (4 * k)) & 15u)]);
+      acc = __dadd_rn(acc, p);
+    }
+    out[q] = acc;
+  }
+}
+
+__global__ void k_row_stats_ref(DevModel m, DevCSF csf, int mode, uint32_t row, uint64_t p0, uint64_t p1,
+                                double* gram, double* xdelta, double* last_delta) {
+  // compute_row_stats (updates.hpp:64-79): one block; thread j < J forms
+  // delta_j of each entry (compute_delta's cell order for that j), thread
+  // (t, j) accumulates gram[t*J+j] serially over the slice in ascending entry
+  // id, thread t also xdelta[t]; reference rounding (no contraction)
+  __shared__ double dsh[VEST_MAXJ];
+  __shared__ double xv_sh;
+  const int J = m.J[mode], tid = threadIdx.x;
+  const int t = tid / J, jj = tid % J;
+  double g_acc = 0.0, x_acc = 0.0;
+  if (tid < J) dsh[tid] = 0.0;
+  __syncthreads();
+  for (uint64_t p = p0; p < p1; ++p) {
+    if (tid < J) {
+      double d = 0.0;
+      for (int lin = 0; lin < m.G; ++lin) {
+        const uint32_t b = m.cellbeta[lin];
+        if ((int)((b >> (4 * mode)) & 15u) != tid) continue;
+        const double g = m.core[lin];
+        if (g == 0.0) continue;
+        double pr = g;
+        for (int k = 0; k < m.N; ++k) {
+          if (k == mode) continue;
+          const uint32_t ik = csf.oc[k][p];
+          pr = __dmul_rn(pr, m.factor[k][(size_t)ik * m.ld[k] + ((b >> (4 * k)) & 15u)]);
+        }
+        d = __dadd_rn(d, pr);
+      }
+      dsh[tid] = d;
+    }
+    if (tid == 0) xv_sh = csf.val[p];
+    __syncthreads();
+    if (tid < J * J) {
+      const double dt = dsh[t];
+      if (dt != 0.0) {
+        if (jj == 0) x_acc = __dadd_rn(x_acc, __dmul_rn(xv_sh, dt));
+        g_acc = __dadd_rn(g_acc, __dmul_rn(dt, dsh[jj]));
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < J * J) gram[tid] = g_acc;
+  if (tid < J * J && jj == 0) xdelta[t] = x_acc;
+  if (tid < J) last_delta[tid] = dsh[tid];
+}
+
 int coo_recon(Ctx& c, const uint32_t* coords, const double* values, uint64_t n, double* out, double* sums) {
   for (uint64_t q = 0; q < n; ++q)
     for (int k = 0; k < c.N; ++k)
@@ -719,7 +794,7 @@ int coo_recon(Ctx& c, const uint32_t* coords, const double* values, uint64_t n, 
     if (values) check(cudaMemcpyAsync(dv, values, n * 8, cudaMemcpyHostToDevice, c.stream), "coo h2d");
     const DevModel m = c.model_view();
     if (c.ops && !c.force_generic) {
-      sync_const_core(c);
+      ConstBankLease lease(c);
       check(c.ops->coo_recon(m, dc, dv, n, dout, dpart, nblocks, c.stream), "coo recon");
     } else {
       check(launch_coo_recon_generic(m, dc, dv, n, dout, dpart, nblocks, c.stream), "coo recon");
@@ -874,6 +949,7 @@ int vest_ctx_destroy(vest_ctx* h) {
   Ctx& c = h->c;
   cudaSetDevice(c.device);
   if (c.stream) cudaStreamSynchronize(c.stream);
+  const_bank_forget(c);  // a later context at this address must reload the bank
   if (c.comm_free) {
     c.comm_free(c.comm.user);
     c.comm_free = nullptr;
@@ -1130,18 +1206,20 @@ static void iteration_body(Ctx& c, int reg, double lambda) {
 
 // replay the captured iteration and restore the host state it leaves
 static void graph_replay(Ctx& c) {
-  check(cudaGraphLaunch(c.graph_exec, c.stream), "graph launch");
+  {
+    ConstBankLease lease(c, true);
+    check(cudaGraphLaunch(c.graph_exec, c.stream), "graph launch");
+  }
   launch_counter() += c.graph_launches;
   note_sweep(c);
   check(cudaStreamSynchronize(c.stream), "graph sync");
-  c.sum_sq = std::max(0.0, c.h_small[0]);
-  c.re = std::sqrt(c.sum_sq) / c.x_norm;
   c.r_valid = false;
   c.r_fresh = false;
   c.r_pending[0] = c.graph_pending[0];
   c.r_pending[1] = c.graph_pending[1];
   c.r_pending_ops = c.graph_pending_ops;
   c.table_valid = false;
+  sum_from_quadratic_form(c);
 }
 
 int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
@@ -1169,10 +1247,12 @@ int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
           cudaStreamEndCapture(c.stream, &g);
           if (g) cudaGraphDestroy(g);
           c.capturing = false;
+          const_bank_forget(c);
           throw;
         }
         c.capturing = false;
         cudaGraph_t g = nullptr;
+        const_bank_forget(c);
         check(cudaStreamEndCapture(c.stream, &g), "end capture");
         const cudaError_t ie = cudaGraphInstantiate(&c.graph_exec, g, 0);
         cudaGraphDestroy(g);
@@ -1261,6 +1341,72 @@ int vest_compute_delta(vest_ctx* h, const uint32_t* at, int mode, double* out) {
     check(cudaStreamSynchronize(c.stream), "delta");
     cudaFree(da);
     cudaFree(dout);
+  });
+}
+
+int vest_compute_row_stats(vest_ctx* h, int mode, uint64_t row, double* gram, double* xdelta, double* last_delta) {
+  Ctx& c = h->c;
+  return guard([&] {
+    if (mode < 0 || mode >= c.N || row >= c.dims[mode]) throw ArgError{"row out of range"};
+    if (!gram || !xdelta) throw ArgError{"null output buffer"};
+    set_dev(c);
+    const int J = c.ranks[mode];
+    const ModeData& md = c.modes[mode];
+    const uint64_t p0 = md.h_offsets[row], p1 = md.h_offsets[row + 1];
+    double* d = nullptr;
+    check(cudaMalloc(&d, (J * J + 2 * J) * sizeof(double)), "tmp");
+    k_row_stats_ref<<<1, std::max(J * J, 32), 0, c.stream>>>(c.model_view(), c.csf_view(mode), mode, (uint32_t)row,
+                                                            p0, p1, d, d + J * J, d + J * J + J);
+    count_launch();
+    check(cudaGetLastError(), "row stats");
+    std::vector<double> h_out(J * J + 2 * J);
+    check(cudaMemcpyAsync(h_out.data(), d, h_out.size() * 8, cudaMemcpyDeviceToHost, c.stream), "d2h");
+    check(cudaStreamSynchronize(c.stream), "row stats");
+    cudaFree(d);
+    std::copy(h_out.begin(), h_out.begin() + J * J, gram);
+    std::copy(h_out.begin() + J * J, h_out.begin() + J * J + J, xdelta);
+    if (last_delta) std::copy(h_out.begin() + J * J + J, h_out.end(), last_delta);
+  });
+}
+
+int vest_partial_reconstruct(vest_ctx* h, const uint32_t* coords, uint64_t nq, int mode, uint64_t j, double* out) {
+  Ctx& c = h->c;
+  return guard([&] {
+    if (mode < 0 || mode >= c.N) throw ArgError{"mode out of range"};
+    if (j >= (uint64_t)c.ranks[mode]) throw ArgError{"rank index out of range"};
+    for (uint64_t q = 0; q < nq; ++q)
+      for (int k = 0; k < c.N; ++k)
+        if (coords[q * c.N + k] >= c.dims[k]) throw ArgError{"query coordinate out of bounds"};
+    if (nq == 0) return;
+    set_dev(c);
+    uint32_t* dc = nullptr;
+    double* dout = nullptr;
+    check(cudaMalloc(&dc, nq * c.N * 4), "tmp");
+    check(cudaMalloc(&dout, nq * 8), "tmp");
+    check(cudaMemcpyAsync(dc, coords, nq * c.N * 4, cudaMemcpyHostToDevice, c.stream), "h2d");
+    const int blocks = (int)std::min<uint64_t>((nq + 255) / 256, 4096);
+    k_partial_recon<<<blocks, 256, 0, c.stream>>>(c.model_view(), dc, nq, mode, (uint32_t)j, dout);
+    count_launch();
+    check(cudaGetLastError(), "partial reconstruct");
+    check(cudaMemcpyAsync(out, dout, nq * 8, cudaMemcpyDeviceToHost, c.stream), "d2h");
+    check(cudaStreamSynchronize(c.stream), "partial reconstruct");
+    cudaFree(dc);
+    cudaFree(dout);
+  });
+}
+
+int vest_get_factor_rows(vest_ctx* h, int mode, uint64_t row_lo, uint64_t nrows, double* out) {
+  Ctx& c = h->c;
+  return guard([&] {
+    if (mode < 0 || mode >= c.N || row_lo > c.dims[mode] || nrows > c.dims[mode] - row_lo)
+      throw ArgError{"row out of range"};
+    if (nrows == 0) return;
+    set_dev(c);
+    const int J = c.ranks[mode];
+    check(cudaMemcpy2DAsync(out, J * sizeof(double), c.d_factor[mode] + row_lo * c.ld[mode], c.ld[mode] * sizeof(double),
+                            J * sizeof(double), nrows, cudaMemcpyDeviceToHost, c.stream),
+          "factor rows d2h");
+    check(cudaStreamSynchronize(c.stream), "factor rows");
   });
 }
 

@@ -141,6 +141,7 @@ struct Ctx {
   int ranks[VEST_MAXN] = {};
   uint64_t nnz = 0;
   int G = 1;
+  uint64_t core_ver = 1;  // bumped when d_core changes (sync_const_core)
   double x_norm = 0.0;  // frobenius norm over observed values
 
   ModeData modes[VEST_MAXN];
@@ -237,7 +238,23 @@ const ShapeOps* find_shape_ops(int N, const int* J);
 cudaError_t launch_rowpass_generic(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s);
 cudaError_t launch_coo_recon_generic(const DevModel& m, const uint32_t* coords, const double* values,
                                      uint64_t n, double* out, double* partial, int nblocks, cudaStream_t s);
-void sync_const_core(Ctx& c);  // copy d_core into every TU's constant-bank core
+void sync_const_core(Ctx& c);  // the core changed: the constant-bank copy is stale (ConstBankLease)
+// Scope that may enqueue kernels reading the constant-bank core (ConstCore):
+// serialises contexts of one device and reloads the bank when needed
+// (vest_rowpass.cu).  whole_graph: around a graph launch (it loads the bank itself).
+struct ConstBankLease {
+  explicit ConstBankLease(Ctx& c, bool whole_graph = false);
+  ~ConstBankLease();
+  ConstBankLease(const ConstBankLease&) = delete;
+  ConstBankLease& operator=(const ConstBankLease&) = delete;
+  Ctx& c;
+  bool graph = false;
+  bool active = false;
+};
+void const_bank_forget(Ctx& c);  // after a stream capture
+bool core_apply_pending(Ctx& c);       // vest_core_sall.cu: apply the deferred last core group to r
+void sum_from_quadratic_form(Ctx& c);  // vest_core_sall.cu: sum r^2 after a 3-mode sweep (exact fallback)
+constexpr double kQuadCancel = 1e-4;   // s'/s below this: recompute the sum from r
 cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
                                  uint64_t dstride, uint64_t p0, cudaStream_t s);
 bool sparse_delta_enabled(const Ctx& c);

@@ -10,6 +10,7 @@
 // per observed entry; the per-entry delta is the factorised contraction of
 // vest_common.cuh with the core in the constant bank (compile-time ranks) or
 // the reference's cell loop (generic ranks).
+#include <mutex>
 #include <type_traits>
 
 #include "vest_common.cuh"
@@ -1028,12 +1029,64 @@ const ShapeOps* find_shape_ops(int N, const int* J) {
   return nullptr;
 }
 
-void sync_const_core(Ctx& c) {
-  if (c.G <= VEST_CONST_CORE_MAX) {
-    check(cudaMemcpyToSymbolAsync(c_core_pairs, c.d_core, sizeof(double) * c.G, 0,
-                                  cudaMemcpyDeviceToDevice, c.stream),
+// The rank-specialised kernels read the core from this module's constant
+// bank, which is one per device, not one per context.  Contexts on the same
+// device take turns: a lease (held only while its kernels are enqueued)
+// reloads the bank from its context's d_core when another context (or an
+// older core) is in it, after the previous holder's kernels are done (event),
+// so concurrent host threads driving different contexts never read each
+// other's core.
+namespace {
+struct BankState {
+  std::mutex mu;
+  const Ctx* owner = nullptr;
+  uint64_t ver = 0;
+  cudaEvent_t done = nullptr;  // recorded after the holder's last kernel that reads the bank
+};
+BankState& bank_state(int device) {
+  static BankState s[64];
+  return s[device & 63];
+}
+}  // namespace
+
+void sync_const_core(Ctx& c) { ++c.core_ver; }
+
+ConstBankLease::ConstBankLease(Ctx& ctx, bool whole_graph) : c(ctx), graph(whole_graph) {
+  active = c.G <= VEST_CONST_CORE_MAX;
+  if (!active) return;
+  BankState& b = bank_state(c.device);
+  b.mu.lock();
+  const bool other = b.owner != &c;
+  if (other && b.done && !c.capturing) check(cudaStreamWaitEvent(c.stream, b.done, 0), "constant bank turn");
+  if (!graph && (other || b.ver != c.core_ver)) {
+    check(cudaMemcpyToSymbolAsync(c_core_pairs, c.d_core, sizeof(double) * c.G, 0, cudaMemcpyDeviceToDevice,
+                                  c.stream),
           "core -> constant bank (pairs)");
+    b.owner = &c;
+    b.ver = c.core_ver;
   }
+}
+
+ConstBankLease::~ConstBankLease() {
+  if (!active) return;
+  BankState& b = bank_state(c.device);
+  if (!c.capturing) {
+    if (!b.done) cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming);
+    cudaEventRecord(b.done, c.stream);
+  }
+  if (graph) {  // the graph loaded some core version itself
+    b.owner = &c;
+    b.ver = 0;
+  }
+  b.mu.unlock();
+}
+
+// After a stream capture: its copies run at replay time, so the bank's real
+// content is unknown.
+void const_bank_forget(Ctx& c) {
+  BankState& b = bank_state(c.device);
+  std::lock_guard<std::mutex> g(b.mu);
+  if (b.owner == &c) b.owner = nullptr;
 }
 
 }  // namespace vest

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import hashlib
 import math
 import os
 import time
@@ -372,6 +373,29 @@ class Device:
         check(self._L.vest_compute_delta(self.h, ptr(a, u32p), mode, ptr(out, f64p)))
         return out
 
+    def row_stats(self, mode: int, row: int):
+        """compute_row_stats (updates.hpp:64-79), bit-identical: (delta of the
+        slice's last entry, gram J x J, xdelta)."""
+        J = self.ranks[mode]
+        d, g, x = np.zeros(J), np.zeros(J * J), np.zeros(J)
+        check(self._L.vest_compute_row_stats(self.h, mode, row, ptr(g, f64p), ptr(x, f64p), ptr(d, f64p)))
+        return d, g.reshape(J, J), x
+
+    def partial_reconstruct(self, coords, mode: int, j: int) -> np.ndarray:
+        """partial_reconstruct (tucker_model.hpp:136-154) at each coordinate."""
+        c = np.ascontiguousarray(coords, np.uint32).reshape(-1)
+        if c.size % self.order:
+            raise ValueError("coordinate buffer must hold order() values per query")
+        nq = c.size // self.order
+        out = np.zeros(max(nq, 1))
+        check(self._L.vest_partial_reconstruct(self.h, ptr(c, u32p), nq, mode, j, ptr(out, f64p)))
+        return out[:nq]
+
+    def get_factor_rows(self, mode: int, lo: int, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        out = np.zeros((n, self.ranks[mode])) if out is None else out
+        check(self._L.vest_get_factor_rows(self.h, mode, lo, n, ptr(out, f64p)))
+        return out
+
     def predict(self, coords) -> np.ndarray:
         c = np.ascontiguousarray(coords, np.uint32).reshape(-1)
         if c.size % self.order:
@@ -419,13 +443,26 @@ class Device:
         check(self._L.vest_normalize_columns(self.h))
 
 
+def _fingerprint(x: SparseTensor) -> bytes:
+    h = hashlib.blake2b(digest_size=16)
+    h.update(np.ascontiguousarray(x.coords).view(np.uint8).reshape(-1))
+    h.update(np.ascontiguousarray(x.values).view(np.uint8).reshape(-1))
+    return h.digest()
+
+
 def _tensor_device(x: SparseTensor, ranks) -> Device:
+    """The tensor's cached device context; rebuilt when the tensor's contents
+    changed since it was built (in-place edits of coords/values)."""
     key = tuple(int(r) for r in ranks)
-    dev = x._devices.get(key)
-    if dev is None:
-        dev = Device(x, key)
-        x._devices[key] = dev
-    return dev
+    fp = _fingerprint(x)
+    hit = x._devices.get(key)
+    if hit is not None and hit[1] != fp:
+        hit[0].close()
+        hit = None
+    if hit is None:
+        hit = (Device(x, key), fp)
+        x._devices[key] = hit
+    return hit[0]
 
 
 _model_devices: dict = {}
@@ -463,18 +500,61 @@ def reconstruct_entry(m: TuckerModel, at) -> float:
     return float(predict(m, np.asarray(at, np.uint32).reshape(1, -1))[0])
 
 
-def update_factor_row_lf(m, x, idx, mode, i, lam):
-    """update_factor_row_lf (updates.hpp:88-106, :141-145)."""
+def partial_reconstruct(m: TuckerModel, at, mode: int, j: int) -> float:
+    """partial_reconstruct (tucker_model.hpp:136-154)."""
+    dev = _model_device(m)
+    dev.set_model(m)
+    return float(dev.partial_reconstruct(np.asarray(at, np.uint32).reshape(1, -1), mode, j)[0])
+
+
+class RowUpdateScratch:
+    """RowUpdateScratch (updates.hpp:17-30)."""
+
+    def __init__(self):
+        self.delta = np.zeros(0)
+        self.gram = np.zeros(0)
+        self.xdelta = np.zeros(0)
+
+    def reset(self, J: int):
+        self.delta = np.zeros(J)
+        self.gram = np.zeros(J * J)
+        self.xdelta = np.zeros(J)
+
+
+def _row_stats_into(dev: Device, mode: int, i: int, s: RowUpdateScratch):
+    d, g, x = dev.row_stats(mode, i)
+    s.delta, s.gram, s.xdelta = d, g.reshape(-1), x
+
+
+def compute_row_stats(m, x, idx, mode: int, i: int, s: RowUpdateScratch):
+    """compute_row_stats (updates.hpp:64-79), bit-identical."""
+    if not (0 <= mode < m.order() and 0 <= i < m.dims[mode]):
+        raise ValueError("row out of range")
+    _row_stats_into(_bind(m, x), mode, i, s)
+
+
+def _row_update(m, x, idx, mode, i, lam, reg, s):
+    if not (0 <= mode < m.order() and 0 <= i < m.dims[mode]):
+        raise ValueError("row out of range")
+    if reg == Regularizer.LF and s is not None and idx is not None and len(idx.slice(mode, i)) == 0:
+        return  # updates.hpp:91: the scratch is not touched either
     dev = _bind(m, x)
-    dev.update_factor_row(Regularizer.LF, mode, i, lam)
-    dev.get_model(into=m)
+    if s is not None:
+        _row_stats_into(dev, mode, i, s)
+    dev.update_factor_row(reg, mode, i, lam)
+    f = m.factors[mode]
+    dev.get_factor_rows(mode, i, 1, out=f[i:i + 1])  # only this row changed
 
 
-def update_factor_row_l1(m, x, idx, mode, i, lam):
+def update_factor_row_lf(m, x, idx, mode, i, lam, s: Optional[RowUpdateScratch] = None):
+    """update_factor_row_lf (updates.hpp:88-106, :141-145); with `s` the
+    scratch overload (the row's statistics are left in s)."""
+    _row_update(m, x, idx, mode, i, lam, Regularizer.LF, s)
+
+
+def update_factor_row_l1(m, x, idx, mode, i, lam, s: Optional[RowUpdateScratch] = None):
     """update_factor_row_l1 (updates.hpp:113-139, :147-151)."""
-    dev = _bind(m, x)
-    dev.update_factor_row(Regularizer.L1, mode, i, lam)
-    dev.get_model(into=m)
+    _row_update(m, x, idx, mode, i, lam, Regularizer.L1, s)
 
 
 def update_all_factors(m, x, idx, reg, lam, threads: int = 1):

@@ -163,6 +163,110 @@ int main() {
     }
     CHECK(threw);
   }
+  // RowUpdateScratch / compute_row_stats / scratch overloads / partial_reconstruct
+  // (updates.hpp:17-30,64-139; tucker_model.hpp:136-154) vs the C restatement,
+  // bit for bit
+  {
+    std::mt19937_64 rng(5);
+    std::vector<Coord> coords;
+    std::vector<double> values;
+    std::uniform_int_distribution<int> pi(0, 24), pj(0, 7), pk(0, 6);
+    std::uniform_real_distribution<double> u(-1.0, 2.0);
+    std::vector<char> seen(25 * 8 * 7, 0);
+    while (values.size() < 500) {
+      const int i = pi(rng) % 20, j = pj(rng), k = pk(rng);  // rows 20..24 of mode 0 stay empty
+      if (seen[(i * 8 + j) * 7 + k]) continue;
+      seen[(i * 8 + j) * 7 + k] = 1;
+      coords.insert(coords.end(), {Coord(i), Coord(j), Coord(k)});
+      values.push_back(u(rng));
+    }
+    const auto x = make_tensor({25, 8, 7}, coords, values);
+    const ModeIndex idx = build_mode_index(x);
+    TuckerModel m = init_random(x.dims, {4, 3, 2}, 21);
+    m.core[5] = 0.0, m.core_mask[5] = 1;
+    m.core[11] = 0.0;  // an incidental zero: skipped like a masked one
+    vo_session* s = nullptr;
+    const std::uint64_t d[3] = {25, 8, 7}, rk[3] = {4, 3, 2};
+    CHECK(vo_create(3, d, x.nnz(), x.coords.data(), x.values.data(), rk, &s) == 0);
+    std::vector<const double*> fp(3);
+    std::vector<const std::uint8_t*> mp(3);
+    for (int n = 0; n < 3; ++n) fp[n] = m.factors[n].data(), mp[n] = m.factor_masks[n].data();
+    CHECK(vo_set_model(s, m.core.data(), m.core_mask.data(), fp.data(), mp.data()) == 0);
+    for (std::size_t n = 0; n < 3; ++n) {
+      for (std::size_t i : {std::size_t(0), std::size_t(3), std::size_t(6)}) {
+        RowUpdateScratch sc;
+        compute_row_stats(m, x, idx, n, i, sc);
+        const std::size_t J = m.ranks[n];
+        std::vector<double> dd(J), gg(J * J), xx(J);
+        CHECK(vo_row_stats(s, (int)n, i, dd.data(), gg.data(), xx.data()) == 0);
+        CHECK(sc.delta == dd && sc.gram == gg && sc.xdelta == xx);
+      }
+      for (std::size_t j = 0; j < m.ranks[n]; ++j) {
+        for (std::size_t e : {std::size_t(0), std::size_t(17), std::size_t(499)}) {
+          double want = 0.0;
+          CHECK(vo_partial_reconstruct(s, x.entry(e), 1, (int)n, j, &want) == 0);
+          CHECK(partial_reconstruct(m, x.entry(e), n, j) == want);
+        }
+      }
+    }
+    // LF on an empty row: returns before touching the scratch (updates.hpp:91)
+    RowUpdateScratch sc;
+    sc.reset(4);
+    sc.gram.assign(16, 7.0);
+    const auto before = m.factors[0];
+    update_factor_row_lf(m, x, idx, 0, 22, 0.05, sc);
+    CHECK(sc.gram == std::vector<double>(16, 7.0) && m.factors[0] == before);
+    // L1 on an empty row: statistics are zero, unmasked elements become 0
+    update_factor_row_l1(m, x, idx, 0, 22, 0.05, sc);
+    CHECK(sc.gram == std::vector<double>(16, 0.0));
+    CHECK(vo_update_factor_row(s, 1, 0, 22, 0.05) == 0);
+    // a busy row through the scratch overload == the oracle's row update
+    update_factor_row_lf(m, x, idx, 0, 3, 0.05, sc);
+    CHECK(vo_update_factor_row(s, 0, 0, 3, 0.05) == 0);
+    std::vector<double> f0(25 * 4), f1(8 * 3), f2(7 * 2);
+    double* fo[3] = {f0.data(), f1.data(), f2.data()};
+    CHECK(vo_get_model(s, nullptr, nullptr, fo, nullptr) == 0);
+    CHECK(m.factors[0] == f0 && m.factors[1] == f1 && m.factors[2] == f2);
+    vo_destroy(s);
+  }
+  // the tensor-context cache is verified against the tensor's contents:
+  // an in-place edit, or new contents in the same buffers (address reuse),
+  // gets a fresh device CSF; at most a few contexts stay cached (LRU)
+  {
+    auto x = make_tensor({6, 5, 4}, {0, 0, 0, 1, 2, 3, 5, 4, 3, 2, 2, 2}, {1.0, 2.0, 3.0, 4.0});
+    TuckerModel m = init_random(x.dims, {2, 2, 2}, 4);
+    auto oracle_re = [&](const SparseTensor& t) {
+      vo_session* s = nullptr;
+      const std::uint64_t d[3] = {6, 5, 4}, rk[3] = {2, 2, 2};
+      vo_create(3, d, t.nnz(), t.coords.data(), t.values.data(), rk, &s);
+      std::vector<const double*> fp(3);
+      std::vector<const std::uint8_t*> mp(3);
+      for (int n = 0; n < 3; ++n) fp[n] = m.factors[n].data(), mp[n] = m.factor_masks[n].data();
+      vo_set_model(s, m.core.data(), m.core_mask.data(), fp.data(), mp.data());
+      double ss, xn, re;
+      vo_compute_residuals(s, 1, nullptr, &ss, &xn, &re);
+      vo_destroy(s);
+      return re;
+    };
+    const double re1 = reconstruction_error(m, x);
+    CHECK(std::abs(re1 - oracle_re(x)) <= 1e-12 * re1);
+    x.values[2] = -7.5;  // in place
+    const double re2 = reconstruction_error(m, x);
+    CHECK(re2 != re1 && std::abs(re2 - oracle_re(x)) <= 1e-12 * re2);
+    const Coord* addr = x.coords.data();
+    x.coords = {0, 1, 0, 1, 2, 1, 5, 4, 0, 3, 2, 2};  // same size: the same buffer, new tensor
+    CHECK(x.coords.data() == addr);
+    const double re3 = reconstruction_error(m, x);
+    CHECK(std::abs(re3 - oracle_re(x)) <= 1e-12 * re3);
+    for (int t = 0; t < 7; ++t) {
+      auto y = make_tensor({6, 5, 4}, {Coord(t % 6), 0, 0, 1, 2, 3}, {1.0 + t, 2.0});
+      reconstruction_error(m, y);
+    }
+    CHECK(b200_detail::cached_contexts() <= b200_detail::max_contexts());
+    release_device_contexts();
+    CHECK(b200_detail::cached_contexts() == 0);
+    CHECK(std::abs(reconstruction_error(m, x) - re3) <= 1e-15 * re3);
+  }
   if (failures == 0) std::printf("ALL OK\n");
   return failures == 0 ? 0 : 1;
 }

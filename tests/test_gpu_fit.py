@@ -64,3 +64,38 @@ def test_auto_search_rates_vs_oracle():
         assert [rr.pruned.core] + rr.pruned.factors == [int(c) for c in counts]
         assert abs(rr.train_re - re_train) <= 1e-6 * re_train
         assert abs(rr.test_re - re_test) <= 1e-6 * re_test
+
+
+def test_noiseless_planted_re_trace_vs_reference():
+    """A near-exact fit (x = a planted model's reconstruction, start = the
+    planted model perturbed by 1e-4): the per-iteration RE follows the
+    reference's exact compute_residuals (trainer.hpp:127) down to RE < 1e-6,
+    where the 3-mode sweep's quadratic-form sum of squares would cancel
+     -- the device falls back to the exact residual sum there."""
+    kind = "reference" if O.available("reference") else "port"
+    rng = np.random.default_rng(12)
+    dims, ranks = [60, 50, 40], [3, 3, 3]
+    cells = np.sort(rng.choice(int(np.prod(dims)), 12000, replace=False))
+    coords = np.stack(np.unravel_index(cells, dims), 1).astype(np.uint32)
+    planted = st.init_random(dims, ranks, 3)
+    p = O.Session(dims, coords, np.ones(len(cells)), ranks, kind)
+    p.set_model(planted.core, planted.core_mask, planted.factors, planted.factor_masks)
+    values = p.reconstruct(coords)
+    x = st.make_tensor(dims, coords, values)
+    m0 = planted.copy()
+    for f in m0.factors:
+        f *= 1.0 + 1e-4 * rng.standard_normal(f.shape)
+    dev = st.Device(x, ranks)
+    dev.set_model(m0)
+    ref = O.Session(dims, coords, values, ranks, kind)
+    ref.set_model(m0.core, m0.core_mask, m0.factors, m0.factor_masks)
+    trace = []
+    for t in range(40):
+        re = dev.cd_iteration(0, 0.0)
+        re_o = ref.cd_iteration(0, 0.0, 4)
+        assert abs(re - re_o) <= 1e-6 * re_o, (t, re, re_o)
+        trace.append(re)
+        if re < 3e-7:
+            break
+    assert trace[-1] < 1e-6, trace
+    assert all(r > 0.0 for r in trace)  # never clamped to 0 (StopController.should_prune, pruning.hpp:50)

@@ -161,3 +161,49 @@ def test_errors(oracle_lib):
     s = O.Session([2, 2], np.array([[0, 1]], np.uint32), np.zeros(1), [1, 1], "port")
     with pytest.raises(ValueError, match="zero-norm"):
         s.compute_residuals()
+
+
+def _ref_available(O):
+    return O.available("reference")
+
+
+@pytest.mark.parametrize("case", ["seq_543_l1_masked", "seq_4mode_l1", "seq_5mode_lf", "seq_2mode_lf"])
+def test_row_stats_and_partial_reconstruct_match_reference(oracle_lib, case):
+    """compute_row_stats (updates.hpp:64-79) and partial_reconstruct
+    (tucker_model.hpp:136-154) of the port vs the reference itself, bit for
+    bit, on the golden instances (masked cores, empty rows included)."""
+    if not _ref_available(oracle_lib):
+        pytest.skip("oracle/_ref not built (reference tree absent)")
+    g = golden(case)
+    N = len(g["dims"])
+    p = _session(oracle_lib, g, "port")
+    r = _session(oracle_lib, g, "reference")
+    rng = np.random.default_rng(3)
+    for n in range(N):
+        rows = list(range(min(int(g["dims"][n]), 6))) + list(rng.integers(0, int(g["dims"][n]), 6))
+        for i in rows:
+            a = p.row_stats(n, int(i))
+            b = r.row_stats(n, int(i))
+            for u, v in zip(a, b):
+                assert np.array_equal(u, v), (case, n, i)
+    coords = g["coords"][:40]
+    for n in range(N):
+        for j in range(int(g["ranks"][n])):
+            assert np.array_equal(p.partial_reconstruct(coords, n, j), r.partial_reconstruct(coords, n, j))
+
+
+def test_update_factor_mode_composes_update_all_factors(oracle_lib):
+    """vo_update_factor_mode over modes 0..N-1 == the reference's
+    update_all_factors (updates.hpp:157-175), bit for bit."""
+    if not _ref_available(oracle_lib):
+        pytest.skip("oracle/_ref not built (reference tree absent)")
+    for case in ["seq_543_l1_masked", "seq_4mode_l1"]:
+        g = golden(case)
+        p = _session(oracle_lib, g, "port")
+        r = _session(oracle_lib, g, "reference")
+        reg, lam = int(g["reg"]), float(g["lam"])
+        for n in range(len(g["dims"])):
+            p.update_factor_mode(reg, n, lam, 3)
+        r.update_all_factors(reg, lam, 2)
+        for a, b in zip(p.get_model()[2], r.get_model()[2]):
+            assert np.array_equal(a, b)
