@@ -633,7 +633,11 @@ def run_config(cfg_id, iters_override=None):
     # --no-families measures the production path
     L.vest_ctx_profile(dev.h, 0 if NO_FAMILIES else 1)
     times, res, prunes = [], [], []
+    ms_arr = np.zeros(8)
+    n_arr = np.zeros(8, np.uint64)
     for t in range(1, iters + 1):
+        if t == iters:  # kernel families of the last (steady-state) iteration only
+            L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         res.append(dev.cd_iteration(0, c["lam"]))
@@ -647,12 +651,10 @@ def run_config(cfg_id, iters_override=None):
                 cnt = dev.prune_step(pr)
                 prunes.append({"iter": t, "rate": pr, "ms": (time.perf_counter() - p0) * 1e3,
                                "counts": [cnt.core] + cnt.factors})
-    ms_arr = np.zeros(8)
-    n_arr = np.zeros(8, np.uint64)
     L.vest_ctx_profile_read(dev.h, _lib.ptr(ms_arr, _lib.f64p), _lib.ptr(n_arr, _lib.u64p), 1)
     fam_names = ["factor_update", "core_pass", "core_gemm", "core_solve", "residual", "resp", "prune",
                  "factor_update_fused_residual"]
-    fams = {fam_names[i]: {"ms": float(ms_arr[i]), "scopes": int(n_arr[i])} for i in range(8)}
+    fams = {fam_names[i]: {"ms": float(ms_arr[i]), "scopes": int(n_arr[i])} for i in range(8)}  # last iteration
     # steady state: the first sweep with a new core mask runs the precompiled
     # kernels and the second compiles the mask-specialised ones (NVRTC, auto
     # mode), so the median is taken from the third iteration on when there is one
@@ -660,7 +662,7 @@ def run_config(cfg_id, iters_override=None):
     line = {"config": cfg_id, "workload": c["desc"], "nnz": x.nnz(), "ms_per_iter_median": med,
             "ms_per_iter": times, "value": x.nnz() / (med * 1e-3), "unit": UNIT, "re_trace": res,
             "prune_events": prunes, "gen_s": gen_s, "ctx_build_s": build_s, "specialised": dev.specialised(),
-            "device_gb": dev.device_bytes() / 1e9, "kernel_families_ms": fams}
+            "device_gb": dev.device_bytes() / 1e9, "kernel_families_ms_last_iter": fams}
     if c.get("sweep"):
         p0 = time.perf_counter()
         sweep = st.auto_search(x, test, dev.get_model(), [round(0.1 * k, 1) for k in range(1, 10)], dev=dev)

@@ -82,6 +82,15 @@ int vest_ctx_sparse_delta_active(const vest_ctx* ctx);
  * shapes, from the second sweep with the same core mask on), 0 off
  * (table-driven kernel), 1 on. */
 int vest_ctx_set_core_gen(vest_ctx* ctx, int mode);
+/* Gather precision of the generated (NVRTC) kernels: on = their factor-row
+ * gathers read fp32 copies of the factors (arithmetic stays fp64; the
+ * factors themselves stay fp64).  For fp32 workloads (BASELINE config 4:
+ * north_star's 1e-4 fp32 tolerance); default off (fp64 gathers). */
+int vest_ctx_set_gather_f32(vest_ctx* ctx, int on);
+/* With the mask-specialised delta: fuse the contraction with the row
+ * statistics and solves in one kernel (modes other than the one carrying the
+ * fused residual).  -1 auto (on), 0 off (delta through HBM, A/B), 1 on. */
+int vest_ctx_set_sparse_fused(vest_ctx* ctx, int mode);
 /* Host-only: generate and NVRTC-compile that contraction for ranks and a core
  * mask (no GPU needed); *cubin_bytes = size of the sm_100a cubin. */
 int vest_sparse_compile_check(int order, const uint64_t* ranks, const uint8_t* core_mask, uint64_t* cubin_bytes);

@@ -52,6 +52,8 @@ SIGNATURES = {
                                          f64p]),
     "vest_compute_delta": (C.c_int, [vp, u32p, C.c_int, f64p]),
     "vest_predict": (C.c_int, [vp, u32p, C.c_uint64, f64p]),
+    "vest_ctx_set_gather_f32": (C.c_int, [vp, C.c_int]),
+    "vest_ctx_set_sparse_fused": (C.c_int, [vp, C.c_int]),
     "vest_compute_row_stats": (C.c_int, [vp, C.c_int, C.c_uint64, f64p, f64p, f64p]),
     "vest_partial_reconstruct": (C.c_int, [vp, u32p, C.c_uint64, C.c_int, C.c_uint64, f64p]),
     "vest_get_factor_rows": (C.c_int, [vp, C.c_int, C.c_uint64, C.c_uint64, f64p]),

@@ -988,6 +988,7 @@ uint64_t plan_key(const Ctx& c, const Blocks& b, int F) {
   for (int k = 0; k < c.N; ++k) mix((uint64_t)c.ranks[k] << 8 | (uint64_t)c.ld[k]);
   mix((uint64_t)F);
   mix(b.pre ? 1 : 0);
+  mix(0xF32u + (uint64_t)c.gather_f32);
   for (size_t i = 0; i < b.start.size(); ++i) mix((uint64_t)b.start[i] << 20 | (uint64_t)b.len[i]);
   for (uint32_t f : b.fib) mix(f);
   return h;
@@ -1227,7 +1228,18 @@ bool core_sweep_capturable(const Ctx& c) {
 // the general plan's blocks (host-only compile check of the generated passes)
 std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c) { return block_lists(plan_general(c, pick_block(c))); }
 
+static void core_sweep_impl(Ctx& c, int reg, double lambda);
+
+// The sweep rewrites d_core: the constant-bank copy is stale after it (and a
+// ConstCore kernel inside it -- the residual it may recompute first -- must not
+// leave the pre-sweep core marked current).
 void core_sweep(Ctx& c, int reg, double lambda) {
+  sync_const_core(c);
+  core_sweep_impl(c, reg, lambda);
+  sync_const_core(c);
+}
+
+static void core_sweep_impl(Ctx& c, int reg, double lambda) {
   const int m = c.N - 1, Jm = c.ranks[m];
   // r = x - B(alpha) for the model after the factor updates
   // (the reference rebuilds its reconstruction cache here, updates.hpp:190-192);

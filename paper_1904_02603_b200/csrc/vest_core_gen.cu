@@ -30,6 +30,7 @@ namespace vest {
 struct CoreGenArgs {
   const uint32_t* oc[VEST_MAXN];
   const double* f[VEST_MAXN];
+  const float* g[VEST_MAXN];  // fp32 factor copies (gather_f32)
   double* r;
   const double* prev_dg;
   double* stats;
@@ -53,7 +54,7 @@ namespace {
 const char* kPrelude = R"CUDA(
 struct Chunk { unsigned row, beg, end, slot; };
 struct CoreGenArgs {
-  const unsigned* oc[8]; const double* f[8]; double* r; const double* prev_dg; double* stats;
+  const unsigned* oc[8]; const double* f[8]; const float* g[8]; double* r; const double* prev_dg; double* stats;
   double* chunk_sq; const Chunk* chunks; unsigned nchunks; int stride;
 };
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
@@ -278,10 +279,12 @@ void core_gen_free(Ctx& c) {
 std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, std::vector<int>& nts,
                             int& ldr_out) {
   const int M = c.N - 1;
+  const bool f32 = c.gather_f32 != 0;
   int soff[VEST_MAXN] = {}, o = 0;
   for (int k = 0; k < M; ++k) {
+    if (f32 && (c.ld[k] / 2) % 2 == 0) o = (o + 1) & ~1;  // 16-byte aligned cp.async targets
     soff[k] = o;
-    o += c.ld[k];
+    o += f32 ? c.ld[k] / 2 : c.ld[k];  // an fp32 row takes ld/2 double slots
   }
   const int rslot = o++;
   while (o % 4 != 2) ++o;
@@ -306,6 +309,19 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     }, used);
     std::ostringstream iss, lu;
     for (int k = 0; k < M; ++k) {
+      if (f32) {  // fp32 row copies: ld floats, 16-byte pieces when ld % 4 == 0, else 8-byte
+        iss << "      { const float* row = a.g[" << k << "] + (unsigned long long)idx[" << k << "] * " << c.ld[k] << ";\n";
+        const bool v4 = c.ld[k] % 4 == 0;
+        for (int t = 0; t < c.ld[k] / (v4 ? 4 : 2); ++t)
+          iss << "        " << (v4 ? "cp16" : "cp8") << "(st + " << soff[k] * 8 + t * (v4 ? 16 : 8) << "u, row + "
+              << t * (v4 ? 4 : 2) << ");\n";
+        iss << "      }\n";
+        for (int b = 0; b < c.ranks[k]; ++b)
+          if (used[k * 16 + b])
+            lu << "    const double " << uname(k, b) << " = (double)reinterpret_cast<const float*>(st + " << soff[k]
+               << ")[" << b << "];\n";
+        continue;
+      }
       iss << "      { const double* row = a.f[" << k << "] + (unsigned long long)idx[" << k << "] * " << c.ld[k] << ";\n";
       for (int t = 0; t < c.ld[k] / 2; ++t)
         iss << "        cp16(st + " << (soff[k] + 2 * t) * 8 << "u, row + " << 2 * t << ");\n";
@@ -364,9 +380,11 @@ void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stri
   const DevCSF csf = c.csf_view(m);
   if (csf.nchunks == 0) return;
   CoreGenArgs a{};
+  if (c.gather_f32 && i == 0) refresh_factor_shadows(c, m);  // the factors are fixed during the sweep
   for (int k = 0; k < c.N; ++k) {
     a.oc[k] = csf.oc[k];
     a.f[k] = c.d_factor[k];
+    a.g[k] = c.d_factor32[k];
   }
   a.r = c.d_r;
   a.prev_dg = prev_dg;

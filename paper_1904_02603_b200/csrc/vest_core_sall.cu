@@ -970,8 +970,8 @@ RPassArgs rpass_args(Ctx& c, const int (&prev)[2], const int (&cur)[2], double* 
   a.part = c.d_gemm_part;
   a.cout = cout;
   a.counter = c.d_counter;
-  a.W = c.d_pack_w;
-  a.wstride = c.nnz;
+  a.W = c.d_pack_w - c.modes[c.N - 1].pos0;  // [P][local nnz], absolute positions
+  a.wstride = c.local_nnz[c.N - 1];
   a.want_sq = want_sq;
   a.hot = hot_modes(c);
   return a;
@@ -1007,7 +1007,7 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   const size_t hs = h_stride(nq);
   const size_t nH = (size_t)RW * hs + 2;  // (+2: bulk copies round up to 16 bytes)
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)csf.nchunks * LW + 1);
-  ensure(c, &c.d_pack_w, &c.pack_w_cap, (size_t)c.nnz * P + 1);
+  ensure(c, &c.d_pack_w, &c.pack_w_cap, (size_t)c.local_nnz[m] * P + 1);
   ensure(c, &c.d_gemm_part, &c.gemm_part_cap, std::max((size_t)ksplit * nT, (size_t)rgrid * (2 * nq + 1)) + 1);
   ensure(c, &c.d_gemm_out, &c.gemm_out_cap, nT + 1 + nH + 2 * nq + 2);
   ensure(c, &c.d_dg, &c.dg_cap, (size_t)2 * nq + 1);
@@ -1021,7 +1021,8 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   double* Cb = Hd + nH;                                  // [C_a | C_b | sum r^2]
   {
     ProfScope ps(c, kProfCorePass);
-    check(ops->sall(mv, csf, c.d_chunk_stats, c.d_pack_w, c.nnz, hot_modes(c), 3 * sms, c.stream),
+    check(ops->sall(mv, csf, c.d_chunk_stats, c.d_pack_w - c.modes[m].pos0, c.local_nnz[m], hot_modes(c), 3 * sms,
+                    c.stream),
           "core all-prefix statistics");
   }
   {

@@ -192,6 +192,30 @@ static uint32_t tiny_max() {
   return v;
 }
 
+// Keep only positions [p0, p1) of mode n's entry arrays (a shard's own rows;
+// each GPU stores the mode-n CSF only for its row range), stored
+// shifted by -p0 so that absolute CSF positions still index them.
+static void compact_owned(Ctx& c, int n) {
+  ModeData& md = c.modes[n];
+  const uint64_t p0 = md.h_offsets[c.row_lo[n]], p1 = md.h_offsets[c.row_hi[n]];
+  if (p0 == 0 && p1 == c.nnz) return;
+  const uint64_t keep = std::max<uint64_t>(p1 - p0, 1), full = std::max<uint64_t>(c.nnz, 1);
+  auto shrink = [&](auto*& ptr, size_t elem) {
+    using T = std::remove_reference_t<decltype(*ptr)>;
+    T* fresh = static_cast<T*>(dalloc(c, keep * elem));
+    if (p1 > p0) check(cudaMemcpyAsync(fresh, ptr + p0, (p1 - p0) * elem, cudaMemcpyDeviceToDevice, c.stream), "compact");
+    check(cudaStreamSynchronize(c.stream), "compact");
+    cudaFree(ptr);
+    c.device_bytes -= full * elem;
+    ptr = fresh - p0;
+  };
+  shrink(md.d_eid, sizeof(uint32_t));
+  shrink(md.d_val, sizeof(double));
+  for (int k = 0; k < c.N; ++k)
+    if (k != n) shrink(md.d_oc[k], sizeof(uint32_t));
+  md.pos0 = p0;
+}
+
 void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
   const uint64_t nnz = c.nnz;
   const int N = c.N;
@@ -287,6 +311,7 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
     std::vector<uint32_t> empty;
     uint32_t slot = 0;
     c.local_nnz[n] = md.h_offsets[c.row_hi[n]] - md.h_offsets[c.row_lo[n]];
+    compact_owned(c, n);  // a shard keeps only the CSF positions of its own rows
     {
       uint64_t mx = 0;
       for (uint64_t i = 0; i < c.dims[n]; ++i) mx = std::max(mx, md.h_offsets[i + 1] - md.h_offsets[i]);
@@ -367,6 +392,22 @@ static bool tiny_rows_off() {
   return v;
 }
 
+__global__ void k_factor_f32(const double* __restrict__ src, float* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];  // round to nearest; same (row, ld) layout as d_factor
+}
+
+void refresh_factor_shadows(Ctx& c, int skip_mode) {
+  for (int k = 0; k < c.N; ++k) {
+    if (k == skip_mode) continue;
+    const uint64_t n = c.dims[k] * (uint64_t)c.ld[k];
+    if (!c.d_factor32[k]) c.d_factor32[k] = static_cast<float*>(dalloc(c, std::max<uint64_t>(n, 1) * sizeof(float)));
+    k_factor_f32<<<592, 256, 0, c.stream>>>(c.d_factor[k], c.d_factor32[k], n);
+    count_launch();
+  }
+  check(cudaGetLastError(), "factor shadows");
+}
+
 static RowPassArgs row_args(Ctx& c, int mode) {
   RowPassArgs a{};
   a.m = c.model_view();
@@ -404,15 +445,17 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
     // solves and fused residual from the materialised delta
     const bool fuse_d = fuse_resid && mode == c.N - 1;
     a.fuse_resid = fuse_d ? 1 : 0;
-    ensure(c, &c.d_delta, &c.delta_cap, (size_t)J * (p1 - p0) + 1);
-    {
+    if (!fuse_d && sparse_fused_enabled(c)) {
+      // contraction, statistics and solves in one kernel (no delta in HBM)
+      ProfScope ps(c, kProfFactor);
+      sparse_fused(c, mode, a);
+      if (reg == 1) l1_empty_rows(c, mode, lambda);
+    } else {
+      ensure(c, &c.d_delta, &c.delta_cap, (size_t)J * (p1 - p0) + 1);
       ProfScope ps(c, fuse_d ? kProfFactorFused : kProfFactor);
       sparse_delta(c, mode, p0, p1 - p0, c.d_delta);
-      {
-        ConstBankLease lease(c);
-        check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream),
-              "factor update (delta)");
-      }
+      check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream),
+            "factor update (delta)");
       if (reg == 1) l1_empty_rows(c, mode, lambda);
     }
     c.r_valid = false;
@@ -429,7 +472,6 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
         ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, mdd.nchunks + 1);
         b.chunk_out = c.d_chunk_sum;
         ProfScope ps(c, kProfResid);
-        ConstBankLease lease(c);
         check(launch_rowpass_delta(b, kResid, b.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream), "heavy-row residual");
       }
       c.r_fresh = true;
@@ -670,6 +712,7 @@ void copy_factor_d2h(Ctx& c, int n, double* host) {
 
 void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const double* const* factors,
                   const uint8_t* const* fmasks) {
+  sync_const_core(c);  // the core changes: the constant-bank copy is stale
   if (core) check(cudaMemcpyAsync(c.d_core, core, c.G * sizeof(double), cudaMemcpyHostToDevice, c.stream), "core");
   if (core_mask) {
     check(cudaMemcpyAsync(c.d_core_mask, core_mask, c.G, cudaMemcpyHostToDevice, c.stream), "core mask");
@@ -691,8 +734,8 @@ void upload_model(Ctx& c, const double* core, const uint8_t* core_mask, const do
   c.table_valid = false;
 }
 
-__global__ void k_scatter_r(const double* r, const uint32_t* eid, uint64_t n, double* out) {
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+__global__ void k_scatter_r(const double* r, const uint32_t* eid, uint64_t p0, uint64_t n, double* out) {
+  for (uint64_t p = p0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < p0 + n; p += (uint64_t)gridDim.x * blockDim.x)
     out[eid[p]] = r[p];
 }
 
@@ -867,6 +910,7 @@ static int create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint
   *out = nullptr;
   auto* h = new vest_ctx();
   Ctx& c = h->c;
+  if (const char* e = getenv("VEST_GATHER_F32")) c.gather_f32 = e[0] == '1';  // A/B default
   const int rc = guard([&] {
     if (order <= 0) throw ArgError{"tensor order must be at least 1"};
     if (order > VEST_MAXN) throw ArgError{"tensor order exceeds the device kernels' limit (8)"};
@@ -911,7 +955,6 @@ static int create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint
     check(cudaMemsetAsync(c.d_core, 0, c.G * sizeof(double), c.stream), "zero");
     check(cudaMemsetAsync(c.d_core_mask, 0, c.G, c.stream), "zero");
     c.h_core_mask.assign(c.G, 0);
-    c.d_r = static_cast<double*>(dalloc(c, std::max<uint64_t>(nnz, 1) * sizeof(double)));
     c.d_counts = static_cast<unsigned long long*>(dalloc(c, 4096 * sizeof(unsigned long long)));
     c.d_sel = dalloc(c, 4096);
     c.d_small = static_cast<double*>(dalloc(c, 64));
@@ -920,6 +963,10 @@ static int create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint
     k_cellbeta<<<(c.G + 255) / 256, 256, 0, c.stream>>>(c.d_cellbeta, c.G, c.N, mv);
     count_launch();
     build_csf(c, coords, values);
+    {  // residual, CSF order of the last mode: this context's positions only
+      const ModeData& ml = c.modes[c.N - 1];
+      c.d_r = static_cast<double*>(dalloc(c, std::max<uint64_t>(c.local_nnz[c.N - 1], 1) * sizeof(double))) - ml.pos0;
+    }
     c.ops = find_shape_ops(c.N, c.ranks);
     if (c.ops && c.G > VEST_CONST_CORE_MAX) c.ops = nullptr;
     check(cudaStreamSynchronize(c.stream), "create");
@@ -957,21 +1004,23 @@ int vest_ctx_destroy(vest_ctx* h) {
   for (int n = 0; n < VEST_MAXN; ++n) {
     ModeData& md = c.modes[n];
     cudaFree(md.d_offsets);
-    for (int k = 0; k < VEST_MAXN; ++k) cudaFree(md.d_oc[k]);
-    cudaFree(md.d_val);
-    cudaFree(md.d_eid);
+    for (int k = 0; k < VEST_MAXN; ++k)
+      if (md.d_oc[k]) cudaFree(md.d_oc[k] + md.pos0);
+    if (md.d_val) cudaFree(md.d_val + md.pos0);
+    if (md.d_eid) cudaFree(md.d_eid + md.pos0);
     cudaFree(md.d_chunks);
     cudaFree(md.d_heavy);
     cudaFree(md.d_empty);
     cudaFree(md.d_heavy_chunks);
     cudaFree(c.d_factor[n]);
+    cudaFree(c.d_factor32[n]);
     cudaFree(c.d_fmask[n]);
     cudaFree(c.d_resp_f[n]);
   }
   cudaFree(c.d_core);
   cudaFree(c.d_core_mask);
   cudaFree(c.d_cellbeta);
-  cudaFree(c.d_r);
+  if (c.d_r) cudaFree(c.d_r + c.modes[c.N > 0 ? c.N - 1 : 0].pos0);
   cudaFree(c.d_resp_core);
   cudaFree(c.d_heavy_part);
   cudaFree(c.d_chunk_stats);
@@ -1016,6 +1065,18 @@ int vest_ctx_set_sparse_delta(vest_ctx* h, int mode) {
   h->c.sparse_delta = mode < 0 ? -1 : (mode ? 1 : 0);
   return VEST_OK;
 }
+int vest_ctx_set_sparse_fused(vest_ctx* h, int mode) {
+  if (!h) return VEST_EINVAL;
+  h->c.sparse_fused = mode < 0 ? -1 : (mode ? 1 : 0);
+  return VEST_OK;
+}
+
+int vest_ctx_set_gather_f32(vest_ctx* h, int on) {
+  if (!h) return VEST_EINVAL;
+  h->c.gather_f32 = on ? 1 : 0;
+  return VEST_OK;
+}
+
 int vest_ctx_set_core_gen(vest_ctx* h, int mode) {
   h->c.core_gen_mode = mode < 0 ? -1 : (mode ? 1 : 0);
   return VEST_OK;
@@ -1034,6 +1095,7 @@ int vest_sparse_compile_check(int order, const uint64_t* ranks, const uint8_t* c
 int vest_init_random(vest_ctx* h, uint64_t seed) {
   Ctx& c = h->c;
   return guard([&] {
+    sync_const_core(c);  // the core changes here: the constant-bank copy is stale
     // init_random (tucker_model.hpp:88-108): same engine, distribution and
     // draw order, so the host-side model is identical to the reference's.
     std::mt19937_64 rng(seed);
@@ -1116,6 +1178,7 @@ int vest_update_factor_row(vest_ctx* h, int reg, int mode, uint64_t row, double 
   return guard([&] {
     check_reg(reg);
     if (mode < 0 || mode >= c.N || row >= c.dims[mode]) throw ArgError{"row out of range"};
+    if (row < c.row_lo[mode] || row >= c.row_hi[mode]) throw ArgError{"row not owned by this shard context"};
     set_dev(c);
     const uint32_t r = (uint32_t)row;
     update_factor_rows(c, mode, &r, 1, reg, lambda);
@@ -1143,7 +1206,9 @@ int vest_compute_residuals(vest_ctx* h, double* r_out, double* sum_sq, double* x
       double* tmp = nullptr;
       check(cudaMalloc(&tmp, c.nnz * sizeof(double)), "r tmp");
       const ModeData& md = c.modes[c.N - 1];
-      k_scatter_r<<<592, 256, 0, c.stream>>>(c.d_r, md.d_eid, c.nnz, tmp);
+      // a shard holds the residuals of its own last-mode rows; the rest are 0
+      check(cudaMemsetAsync(tmp, 0, c.nnz * sizeof(double), c.stream), "r tmp");
+      k_scatter_r<<<592, 256, 0, c.stream>>>(c.d_r, md.d_eid, md.pos0, c.local_nnz[c.N - 1], tmp);
       count_launch();
       check(cudaMemcpyAsync(r_out, tmp, c.nnz * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "r d2h");
       check(cudaStreamSynchronize(c.stream), "r sync");
@@ -1348,6 +1413,7 @@ int vest_compute_row_stats(vest_ctx* h, int mode, uint64_t row, double* gram, do
   Ctx& c = h->c;
   return guard([&] {
     if (mode < 0 || mode >= c.N || row >= c.dims[mode]) throw ArgError{"row out of range"};
+    if (row < c.row_lo[mode] || row >= c.row_hi[mode]) throw ArgError{"row not owned by this shard context"};
     if (!gram || !xdelta) throw ArgError{"null output buffer"};
     set_dev(c);
     const int J = c.ranks[mode];
@@ -1454,6 +1520,7 @@ int vest_prune_step(vest_ctx* h, double pr, const double* core_resp, const doubl
                     uint64_t* counts) {
   Ctx& c = h->c;
   return guard([&] {
+    sync_const_core(c);  // the core changes here: the constant-bank copy is stale
     if (!(pr >= 0.0 && pr < 1.0)) throw ArgError{"prune rate must be in [0, 1)"};
     set_dev(c);
     if (core_resp) {
@@ -1470,6 +1537,7 @@ int vest_prune_step(vest_ctx* h, double pr, const double* core_resp, const doubl
     c.r_pending[0] = c.r_pending[1] = -1;
     c.r_fresh = false;
     c.table_valid = false;
+    sync_const_core(c);
   });
 }
 
@@ -1484,12 +1552,14 @@ int vest_sparsity(vest_ctx* h, double* zero_fraction, double* masked_fraction) {
 int vest_normalize_columns(vest_ctx* h) {
   Ctx& c = h->c;
   return guard([&] {
+    sync_const_core(c);  // the core changes here: the constant-bank copy is stale
     set_dev(c);
     normalize_columns(c);
     c.r_valid = false;
     c.r_pending[0] = c.r_pending[1] = -1;
     c.r_fresh = false;
     c.table_valid = false;
+    sync_const_core(c);
   });
 }
 
@@ -1499,6 +1569,7 @@ int vest_get_mode_index(vest_ctx* h, int mode, uint64_t* offsets, uint32_t* ids)
     if (mode < 0 || mode >= c.N) throw ArgError{"mode out of range"};
     set_dev(c);
     const ModeData& md = c.modes[mode];
+    if (c.local_nnz[mode] != c.nnz) throw ArgError{"a shard context holds the index of its own rows only"};
     std::memcpy(offsets, md.h_offsets.data(), (c.dims[mode] + 1) * sizeof(uint64_t));
     if (c.nnz) check(cudaMemcpy(ids, md.d_eid, c.nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost), "ids");
   });

@@ -80,6 +80,10 @@ struct RowPassArgs {
 };
 
 struct ModeData {
+  // Entry arrays (d_oc, d_val, d_eid) hold CSF positions [pos0, pos0 + local
+  // nnz) -- a shard context keeps only its own rows -- and are stored as
+  // base - pos0, so absolute CSF positions index them (allocation = ptr + pos0).
+  uint64_t pos0 = 0;
   uint64_t* d_offsets = nullptr;
   uint32_t* d_oc[VEST_MAXN] = {};
   double* d_val = nullptr;
@@ -148,6 +152,12 @@ struct Ctx {
 
   double* d_factor[VEST_MAXN] = {};
   int ld[VEST_MAXN] = {};
+  // fp32 copies of the factors, gathered by the generated (NVRTC) kernels when
+  // gather_f32 is on (fp64 arithmetic on fp32-rounded factor operands; BASELINE
+  // config 4 is the fp32 configuration).  Refreshed from d_factor before each
+  // use (refresh_factor_shadows).
+  float* d_factor32[VEST_MAXN] = {};
+  int gather_f32 = 0;
   uint8_t* d_fmask[VEST_MAXN] = {};
   double* d_core = nullptr;
   uint8_t* d_core_mask = nullptr;
@@ -203,6 +213,7 @@ struct Ctx {
   int graph_pending[2] = {-1, -1};   // r_pending after the captured iteration
   const void* graph_pending_ops = nullptr;
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
+  int sparse_fused = -1;           // ... fused with the statistics (modes without the fused residual): -1 auto
   double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
   uint32_t* d_hstab = nullptr;     size_t hstab_cap = 0;    // live-cell Gram entry table (k_core_hsample)
   bool force_generic = false;
@@ -238,6 +249,7 @@ const ShapeOps* find_shape_ops(int N, const int* J);
 cudaError_t launch_rowpass_generic(const RowPassArgs& a, int kind, uint32_t nchunks, cudaStream_t s);
 cudaError_t launch_coo_recon_generic(const DevModel& m, const uint32_t* coords, const double* values,
                                      uint64_t n, double* out, double* partial, int nblocks, cudaStream_t s);
+void refresh_factor_shadows(Ctx& c, int skip_mode);  // d_factor32[k] = fp32(d_factor[k]), k != skip_mode
 void sync_const_core(Ctx& c);  // the core changed: the constant-bank copy is stale (ConstBankLease)
 // Scope that may enqueue kernels reading the constant-bank core (ConstCore):
 // serialises contexts of one device and reloads the bank when needed
@@ -255,6 +267,9 @@ void const_bank_forget(Ctx& c);  // after a stream capture
 bool core_apply_pending(Ctx& c);       // vest_core_sall.cu: apply the deferred last core group to r
 void sum_from_quadratic_form(Ctx& c);  // vest_core_sall.cu: sum r^2 after a 3-mode sweep (exact fallback)
 constexpr double kQuadCancel = 1e-4;   // s'/s below this: recompute the sum from r
+cudaError_t launch_heavy_stats(const RowPassArgs& a, cudaStream_t s);  // k_heavy after a chunk-statistics pass
+bool sparse_fused_enabled(const Ctx& c);                               // vest_sparse.cu
+void sparse_fused(Ctx& c, int mode, const RowPassArgs& a);             // fused delta + statistics + solves
 cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
                                  uint64_t dstride, uint64_t p0, cudaStream_t s);
 bool sparse_delta_enabled(const Ctx& c);

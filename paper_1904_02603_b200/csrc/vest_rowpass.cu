@@ -824,6 +824,13 @@ cudaError_t launch_delta_j(const RowPassArgs& a, int kind, uint32_t nchunks, con
   return cudaGetLastError();
 }
 
+cudaError_t launch_heavy_stats(const RowPassArgs& a, cudaStream_t s) {
+  if (a.csf.nheavy == 0) return cudaSuccess;
+  k_heavy<<<(a.csf.nheavy + 7) / 8, 256, 0, s>>>(a, kStats);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
                                  uint64_t dstride, uint64_t p0, cudaStream_t s) {
   switch (a.m.J[a.mode]) {

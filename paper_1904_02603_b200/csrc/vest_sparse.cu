@@ -39,6 +39,7 @@ namespace vest {
 struct SparseDeltaArgs {
   const uint32_t* oc[VEST_MAXN];
   const double* f[VEST_MAXN];
+  const float* g[VEST_MAXN];  // fp32 factor copies (gather_f32)
   double* out;
   unsigned long long p0, n, stride;
 };
@@ -93,12 +94,14 @@ struct Cell {
 // u<k>_<b>: mode k's factor value beta = b of the entry (registers)
 std::string u(int k, int b) { return "u" + std::to_string(k) + "_" + std::to_string(b); }
 
-void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
+// the unmasked cells in contraction order for mode n: other modes but the
+// last (prefix), then beta_n, then the last other mode
+std::vector<Cell> ordered_cells(const Ctx& c, int n, std::vector<int>& oth) {
   const int N = c.N;
-  std::vector<int> oth;
+  oth.clear();
   for (int k = 0; k < N; ++k)
     if (k != n) oth.push_back(k);
-  const int L = (int)oth.size();  // other modes; the last one is contracted innermost
+  const int L = (int)oth.size();
   std::vector<Cell> cells;
   for (int lin = 0; lin < c.G; ++lin) {
     if (c.h_core_mask[lin]) continue;
@@ -110,7 +113,6 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     }
     cells.push_back(cl);
   }
-  // order: other modes but the last (prefix), then beta_n, then the last other mode
   auto key = [&](const Cell& a, const Cell& b) {
     for (int q = 0; q + 1 < L; ++q)
       if (a.beta[oth[q]] != b.beta[oth[q]]) return a.beta[oth[q]] < b.beta[oth[q]];
@@ -118,33 +120,54 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     return a.beta[oth[L - 1]] < b.beta[oth[L - 1]];
   };
   std::sort(cells.begin(), cells.end(), key);
+  return cells;
+}
 
-  // two entries per thread (E = 0, 1: t and t + 256 of the block's stride
-  // window): every core value is loaded once (uniform constant load) and
-  // feeds both entries' FMAs
-  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) vest_sd_" << n << "(const SparseDeltaArgs a) {\n"
-    << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
-    << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
-  for (int e = 0; e < 2; ++e) {
-    const std::string E = std::to_string(e);
-    for (int k : oth) {
-      const int ld = c.ld[k];
-      const std::string rk = "r" + std::to_string(k) + "e" + E;
-      o << "    const double* " << rk << " = a.f[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + a.p0 + t"
-        << E << ") * " << ld << "ull;\n";
-      for (int b = 0; b < c.ranks[k]; b += 2) {
-        const std::string ua = u(k, b) + "e" + E;
-        if (b + 1 < c.ranks[k]) {
-          const std::string v = "v" + std::to_string(k) + "_" + std::to_string(b) + "e" + E;
-          o << "    const double2 " << v << " = __ldg(reinterpret_cast<const double2*>(" << rk << " + " << b << "));\n"
-            << "    const double " << ua << " = " << v << ".x, " << u(k, b + 1) << "e" << E << " = " << v << ".y;\n";
-        } else {
-          o << "    const double " << ua << " = __ldg(" << rk << " + " << b << ");\n";
-        }
+// Loads of entry E's other-mode factor rows into registers u<k>_<b>e<E>;
+// pos is the expression of the entry's CSF position.
+void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>& oth, int e, const std::string& pos) {
+  const std::string E = std::to_string(e);
+  for (int k : oth) {
+    const int ld = c.ld[k];
+    const std::string rk = "r" + std::to_string(k) + "e" + E;
+    if (c.gather_f32) {  // fp32 copy of the row, widened to fp64 in registers
+      const bool v4 = ld % 4 == 0;
+      o << "    const float* " << rk << " = a.g[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos
+        << ") * " << ld << "ull;\n";
+      for (int b = 0; b < c.ranks[k]; b += (v4 ? 4 : 2)) {
+        const std::string v = "v" + std::to_string(k) + "_" + std::to_string(b) + "e" + E;
+        o << "    const " << (v4 ? "float4 " : "float2 ") << v << " = __ldg(reinterpret_cast<const "
+          << (v4 ? "float4" : "float2") << "*>(" << rk << " + " << b << "));\n";
+        const char* comp[4] = {"x", "y", "z", "w"};
+        for (int q = 0; q < (v4 ? 4 : 2) && b + q < c.ranks[k]; ++q)
+          o << "    const double " << u(k, b + q) << "e" << E << " = (double)" << v << "." << comp[q] << ";\n";
+      }
+      continue;
+    }
+    o << "    const double* " << rk << " = a.f[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos
+      << ") * " << ld << "ull;\n";
+    for (int b = 0; b < c.ranks[k]; b += 2) {
+      const std::string ua = u(k, b) + "e" + E;
+      if (b + 1 < c.ranks[k]) {
+        const std::string v = "v" + std::to_string(k) + "_" + std::to_string(b) + "e" + E;
+        o << "    const double2 " << v << " = __ldg(reinterpret_cast<const double2*>(" << rk << " + " << b << "));\n"
+          << "    const double " << ua << " = " << v << ".x, " << u(k, b + 1) << "e" << E << " = " << v << ".y;\n";
+      } else {
+        o << "    const double " << ua << " = __ldg(" << rk << " + " << b << ");\n";
       }
     }
-    for (int j = 0; j < c.ranks[n]; ++j) o << "    double d" << j << "e" << E << " = 0.0;\n";
   }
+}
+
+// d<j>e<E> = delta_j of entries E < ne (updates.hpp:35-52 restricted to the
+// unmasked cells): each prefix product formed once, each (prefix, beta_n)
+// group t = sum G u_last, then d[beta_n] += w t.  Every core value G[lin] is a
+// constant-bank operand shared by the ne entries.
+void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<int>& oth, const std::vector<Cell>& cells,
+                int ne) {
+  const int L = (int)oth.size();
+  for (int e = 0; e < ne; ++e)
+    for (int j = 0; j < c.ranks[n]; ++j) o << "    double d" << j << "e" << e << " = 0.0;\n";
   auto same_prefix = [&](const Cell& a, const Cell& b, int upto) {
     for (int q = 0; q <= upto; ++q)
       if (a.beta[oth[q]] != b.beta[oth[q]]) return false;
@@ -152,11 +175,10 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
   };
   size_t i = 0;
   while (i < cells.size()) {
-    // open the prefix levels of cells[i] (both entries)
-    for (int q = 0; q + 1 < L; ++q) {
+    for (int q = 0; q + 1 < L; ++q) {  // open the prefix levels of cells[i]
       const int k = oth[q], b = cells[i].beta[k];
       o << "    {";
-      for (int e = 0; e < 2; ++e) {
+      for (int e = 0; e < ne; ++e) {
         const std::string E = std::to_string(e);
         if (q == 0) o << " const double w0e" << E << " = " << u(k, b) << "e" << E << ";";
         else o << " const double w" << q << "e" << E << " = w" << (q - 1) << "e" << E << " * " << u(k, b) << "e" << E << ";";
@@ -169,33 +191,193 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     for (size_t g = i; g < e_end;) {
       const int bn = cells[g].beta[n];
       size_t h = g;
-      o << "      { double g = G[" << cells[h].lin << "]; double t0 = g * " << u(kl, cells[h].beta[kl]) << "e0, t1 = g * "
-        << u(kl, cells[h].beta[kl]) << "e1;";
-      for (++h; h < e_end && cells[h].beta[n] == bn; ++h)
-        o << " g = G[" << cells[h].lin << "]; t0 = fma(g, " << u(kl, cells[h].beta[kl]) << "e0, t0); t1 = fma(g, "
-          << u(kl, cells[h].beta[kl]) << "e1, t1);";
-      if (L >= 2)
-        o << " d" << bn << "e0 = fma(w" << (L - 2) << "e0, t0, d" << bn << "e0); d" << bn << "e1 = fma(w" << (L - 2)
-          << "e1, t1, d" << bn << "e1); }\n";
-      else
-        o << " d" << bn << "e0 += t0; d" << bn << "e1 += t1; }\n";
+      o << "      { double g = G[" << cells[h].lin << "];";
+      for (int e = 0; e < ne; ++e) o << " double t" << e << " = g * " << u(kl, cells[h].beta[kl]) << "e" << e << ";";
+      for (++h; h < e_end && cells[h].beta[n] == bn; ++h) {
+        o << " g = G[" << cells[h].lin << "];";
+        for (int e = 0; e < ne; ++e)
+          o << " t" << e << " = fma(g, " << u(kl, cells[h].beta[kl]) << "e" << e << ", t" << e << ");";
+      }
+      for (int e = 0; e < ne; ++e) {
+        if (L >= 2) o << " d" << bn << "e" << e << " = fma(w" << (L - 2) << "e" << e << ", t" << e << ", d" << bn << "e" << e << ");";
+        else o << " d" << bn << "e" << e << " += t" << e << ";";
+      }
+      o << " }\n";
       g = h;
     }
     for (int q = 0; q + 1 < L; ++q) o << "    }\n";
     i = e_end;
   }
+}
+
+void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
+  std::vector<int> oth;
+  const std::vector<Cell> cells = ordered_cells(c, n, oth);
+  // two entries per thread (E = 0, 1: t and t + 256 of the block's stride
+  // window): every core value is loaded once (uniform constant load) and
+  // feeds both entries' FMAs
+  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) vest_sd_" << n << "(const SparseDeltaArgs a) {\n"
+    << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
+    << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
+  emit_row_loads(o, c, oth, 0, "a.p0 + t0");
+  emit_row_loads(o, c, oth, 1, "a.p0 + t1");
+  emit_cells(o, c, n, oth, cells, 2);
   for (int j = 0; j < c.ranks[n]; ++j) o << "    a.out[" << j << "ull * a.stride + t0] = d" << j << "e0;\n";
   o << "    if (t1 != t0) {\n";
   for (int j = 0; j < c.ranks[n]; ++j) o << "      a.out[" << j << "ull * a.stride + t1] = d" << j << "e1;\n";
   o << "    }\n  }\n}\n";
 }
 
+// The fused factor-mode update (modes without the fused residual): one warp
+// per chunk of a row, one entry per lane per 32-entry round -- the
+// contraction above in registers, then (delta, x) staged transposed in shared
+// memory and the row's Gram accumulated on DMMA, the light row solved in the
+// kernel (heavy rows: partials for k_heavy).  The same arithmetic as
+// vest_sd_<n> + k_rowpass_delta (bit-identical) without the delta round trip
+// through HBM.
+const char* kFusedPrelude = R"CUDA(
+struct Chunk { unsigned row, beg, end, slot; };
+struct SparseFusedArgs {
+  const unsigned* oc[8]; const double* f[8]; const float* g[8];
+  const double* val; const Chunk* chunks; unsigned nchunks;
+  double* row_base; int ld_n; const unsigned char* fmask;
+  double* heavy_out; int stride_na; int reg; double lambda;
+};
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+constexpr int kXld = 36;
+template <int NC>
+__device__ __forceinline__ void gram_dmma(const double* X, double (&d)[3][2], int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int e = 4 * kk + tq;
+    const double f0 = X[g * kXld + e];
+    dmma884(d[0][0], d[0][1], f0, f0);
+    if constexpr (NC > 8) {
+      const double f1 = X[(8 + g) * kXld + e];
+      dmma884(d[1][0], d[1][1], f0, f1);
+      dmma884(d[2][0], d[2][1], f1, f1);
+    }
+  }
+}
+__device__ __forceinline__ void gram_coord(int t, int i, int lane, int& row, int& col) {
+  const int I = t == 2 ? 1 : 0, J = t == 0 ? 0 : 1;
+  row = 8 * I + (lane >> 2);
+  col = 8 * J + 2 * (lane & 3) + i;
+}
+__device__ __forceinline__ void solve_row(int J, int reg, double lambda, const double* G, const double* xd,
+                                          double* row, const unsigned char* mask, int lane) {
+  double v = lane < J ? row[lane] : 0.0;
+  for (int j = 0; j < J; ++j) {
+    if (mask[j]) continue;
+    const double prod = (lane < J && lane != j) ? G[j * J + lane] * v : 0.0;
+    const double s = warp_sum(prod);
+    const double lin = xd[j] - s;
+    const double gjj = G[j * J + j];
+    double nv = 0.0;
+    bool upd;
+    if (reg == 0) {
+      const double den = gjj + lambda;
+      upd = den != 0.0;
+      nv = lin / den;
+    } else {
+      const double g = -2.0 * lin;
+      const double d = 2.0 * gjj;
+      if (d == 0.0) {
+        upd = fabs(g) <= lambda;
+        nv = 0.0;
+      } else {
+        upd = true;
+        nv = g > lambda ? (lambda - g) / d : (g < -lambda ? -(lambda + g) / d : 0.0);
+      }
+    }
+    if (upd && lane == j) v = nv;
+  }
+  if (lane < J) row[lane] = v;
+}
+)CUDA";
+
+void emit_fused(std::ostringstream& o, const Ctx& c, int n) {
+  std::vector<int> oth;
+  const std::vector<Cell> cells = ordered_cells(c, n, oth);
+  const int J = c.ranks[n];
+  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) vest_sf_" << n << "(const SparseFusedArgs a) {\n"
+    << "  constexpr int J = " << J << ", NG = J * (J + 1) / 2;\n"
+    << "  __shared__ double smem_d[8][16 * kXld];\n"
+    << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
+    << "  const unsigned ci = blockIdx.x * 8 + warp;\n"
+    << "  if (ci >= a.nchunks) return;\n"
+    << "  const Chunk ch = a.chunks[ci];\n"
+    << "  double* wsm = smem_d[warp];\n"
+    << "  for (int t = lane; t < 16 * kXld; t += 32) wsm[t] = 0.0;\n"
+    << "  __syncwarp();\n"
+    << "  double tc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};\n"
+    << "  for (unsigned base = ch.beg; base < ch.end; base += 32) {\n"
+    << "    const bool valid = base + lane < ch.end;\n"
+    << "    const unsigned pos = valid ? base + lane : ch.beg;\n";
+  emit_row_loads(o, c, oth, 0, "pos");
+  emit_cells(o, c, n, oth, cells, 1);
+  for (int j = 0; j < J; ++j) o << "    wsm[" << j << " * kXld + lane] = valid ? d" << j << "e0 : 0.0;\n";
+  o << "    wsm[J * kXld + lane] = valid ? __ldg(a.val + pos) : 0.0;\n"
+    << "    __syncwarp();\n"
+    << "    gram_dmma<J + 1>(wsm, tc, lane);\n"
+    << "    __syncwarp();\n"
+    << "  }\n"
+    << "  double* Gs = wsm;\n"
+    << "  double* xd = wsm + J * J;\n"
+    << "#pragma unroll\n"
+    << "  for (int t = 0; t < (J + 1 > 8 ? 3 : 1); ++t) {\n"
+    << "#pragma unroll\n"
+    << "    for (int i = 0; i < 2; ++i) {\n"
+    << "      int row, col;\n"
+    << "      gram_coord(t, i, lane, row, col);\n"
+    << "      const double v = tc[t][i];\n"
+    << "      int slot = -1;\n"
+    << "      if (row <= col && col < J) slot = row * J - row * (row - 1) / 2 + (col - row);\n"
+    << "      else if (col == J && row < J) slot = NG + row;\n"
+    << "      if (slot < 0) continue;\n"
+    << "      if (ch.slot != 0xFFFFFFFFu) {\n"
+    << "        a.heavy_out[(unsigned long long)ch.slot * a.stride_na + slot] = v;\n"
+    << "      } else if (col == J) {\n"
+    << "        xd[row] = v;\n"
+    << "      } else {\n"
+    << "        Gs[row * J + col] = v;\n"
+    << "        Gs[col * J + row] = v;\n"
+    << "      }\n"
+    << "    }\n"
+    << "  }\n"
+    << "  if (ch.slot != 0xFFFFFFFFu) return;\n"
+    << "  __syncwarp();\n"
+    << "  solve_row(J, a.reg, a.lambda, Gs, xd, a.row_base + (unsigned long long)ch.row * a.ld_n,\n"
+    << "            a.fmask + (unsigned long long)ch.row * J, lane);\n"
+    << "}\n";
+}
+
+// the fused kernel's DMMA tile holds (delta, x): J + 1 <= 16
+bool fused_ok(const Ctx& c) {
+  for (int k = 0; k < c.N; ++k)
+    if (c.ranks[k] + 1 > 16) return false;
+  return true;
+}
+
 std::string gen_source(const Ctx& c) {
   std::ostringstream o;
   o << "struct SparseDeltaArgs { const unsigned* oc[" << VEST_MAXN << "]; const double* f[" << VEST_MAXN
-    << "]; double* out; unsigned long long p0, n, stride; };\n"
+    << "]; const float* g[" << VEST_MAXN << "]; double* out; unsigned long long p0, n, stride; };\n"
     << "extern \"C\" __constant__ double G[" << c.G << "];\n";
   for (int n = 0; n < c.N; ++n) emit_mode(o, c, n);
+  if (fused_ok(c)) {
+    o << kFusedPrelude;
+    for (int n = 0; n < c.N; ++n) emit_fused(o, c, n);
+  }
   return o.str();
 }
 
@@ -208,6 +390,7 @@ uint64_t mask_key(const Ctx& c) {
   mix((uint64_t)c.N);
   for (int k = 0; k < c.N; ++k) mix((uint64_t)c.ranks[k] << 8 | (uint64_t)c.ld[k]);
   for (uint8_t m : c.h_core_mask) mix(m);
+  mix(0xF32u + (uint64_t)c.gather_f32);
   return h;
 }
 
@@ -217,6 +400,7 @@ struct SparseState {
   uint64_t key = 0;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t k[VEST_MAXN] = {};
+  cudaKernel_t kf[VEST_MAXN] = {};  // fused factor-mode updates (vest_sf_<n>)
   double* G = nullptr;
   double compile_s = 0.0;
 };
@@ -320,6 +504,10 @@ static void ensure_module(Ctx& c) {
   for (int n = 0; n < c.N; ++n) {
     const std::string nm = "vest_sd_" + std::to_string(n);
     check(cudaLibraryGetKernel(&s->k[n], s->lib, nm.c_str()), "sparse delta kernel");
+    if (fused_ok(c)) {
+      const std::string nf = "vest_sf_" + std::to_string(n);
+      check(cudaLibraryGetKernel(&s->kf[n], s->lib, nf.c_str()), "fused factor kernel");
+    }
   }
   size_t gb = 0;
   check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->G), &gb, s->lib, "G"), "sparse delta core symbol");
@@ -334,9 +522,11 @@ void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
         "sparse delta core");
   SparseDeltaArgs a{};
   const DevCSF csf = c.csf_view(mode);
+  if (c.gather_f32) refresh_factor_shadows(c, mode);
   for (int k = 0; k < c.N; ++k) {
     a.oc[k] = csf.oc[k];
     a.f[k] = c.d_factor[k];
+    a.g[k] = c.d_factor32[k];
   }
   a.out = out;
   a.p0 = p0;
@@ -349,6 +539,64 @@ void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
   check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->k[mode]), dim3(grid), dim3(256), args, 0, c.stream),
         "sparse delta launch");
   count_launch();
+}
+
+struct SparseFusedArgs {
+  const uint32_t* oc[VEST_MAXN];
+  const double* f[VEST_MAXN];
+  const float* g[VEST_MAXN];
+  const double* val;
+  const Chunk* chunks;
+  uint32_t nchunks;
+  double* row_base;
+  int ld_n;
+  const uint8_t* fmask;
+  double* heavy_out;
+  int stride_na;
+  int reg;
+  double lambda;
+};
+
+bool sparse_fused_enabled(const Ctx& c) {
+  static const int env = [] {  // VEST_SPARSE_FUSED=0 selects vest_sd + k_rowpass_delta (A/B timing)
+    const char* e = getenv("VEST_SPARSE_FUSED");
+    return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+  }();
+  const int mode = c.sparse_fused >= 0 ? c.sparse_fused : env;
+  return mode != 0 && fused_ok(c);
+}
+
+// One factor mode through the fused kernel (statistics + light-row solves),
+// then k_heavy for rows split over several chunks.
+void sparse_fused(Ctx& c, int mode, const RowPassArgs& ra) {
+  ensure_module(c);
+  if (c.gather_f32) refresh_factor_shadows(c, mode);
+  if (ra.csf.nchunks > 0) {
+    SparseFusedArgs a{};
+    for (int k = 0; k < c.N; ++k) {
+      a.oc[k] = ra.csf.oc[k];
+      a.f[k] = c.d_factor[k];
+      a.g[k] = c.d_factor32[k];
+    }
+    a.val = ra.csf.val;
+    a.chunks = ra.csf.chunks;
+    a.nchunks = ra.csf.nchunks;
+    a.row_base = ra.m.factor[mode];
+    a.ld_n = ra.m.ld[mode];
+    a.fmask = ra.m.fmask[mode];
+    a.heavy_out = ra.heavy_out;
+    a.stride_na = ra.stride_na;
+    a.reg = ra.reg;
+    a.lambda = ra.lambda;
+    check(cudaMemcpyAsync(c.sparse->G, c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
+          "sparse delta core");
+    void* args[] = {&a};
+    check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->kf[mode]), dim3((ra.csf.nchunks + 7) / 8),
+                           dim3(256), args, 0, c.stream),
+          "fused factor launch");
+    count_launch();
+  }
+  check(launch_heavy_stats(ra, c.stream), "heavy rows");
 }
 
 // Host-only check (no GPU needed): generate and NVRTC-compile the
@@ -364,6 +612,7 @@ int sparse_compile_check(int N, const int* ranks, const uint8_t* core_mask, uint
       c.G *= ranks[k];
     }
     c.h_core_mask.assign(core_mask, core_mask + c.G);
+    if (const char* e = getenv("VEST_GATHER_F32")) c.gather_f32 = e[0] == '1';
     *bytes = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu").size();
     if (N >= 2) {  // the plan-specialised core passes of the same mask
       std::vector<int> nts;

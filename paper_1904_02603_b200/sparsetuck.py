@@ -288,6 +288,16 @@ class Device:
         """Mask-specialised delta contraction: -1 auto, 0 off, 1 on."""
         check(self._L.vest_ctx_set_sparse_delta(self.h, int(mode)))
 
+    def set_sparse_fused(self, mode: int):
+        """-1 auto, 0: mask-specialised delta through HBM + statistics kernel,
+        1: one fused kernel per factor mode (bit-identical)."""
+        check(self._L.vest_ctx_set_sparse_fused(self.h, int(mode)))
+
+    def set_gather_f32(self, on: bool):
+        """The generated (NVRTC) kernels gather fp32 copies of the factor rows
+        (fp64 arithmetic); for fp32 workloads (BASELINE config 4)."""
+        check(self._L.vest_ctx_set_gather_f32(self.h, 1 if on else 0))
+
     def set_core_gen(self, mode: int):
         """Plan-specialised core-sweep passes: -1 auto, 0 off, 1 on."""
         check(self._L.vest_ctx_set_core_gen(self.h, int(mode)))

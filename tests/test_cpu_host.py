@@ -37,10 +37,14 @@ def test_version_and_counter(L):
     assert L.vest_launch_count() == 0  # nothing launched without a device
 
 
+@pytest.mark.parametrize("f32", ["0", "1"])
 @pytest.mark.parametrize("ranks,keep", [([8, 8, 8, 8], 0.1), ([5, 5, 5], 1.0), ([3, 4], 0.5), ([2, 2, 3, 2, 2], 0.3)])
-def test_sparse_delta_source_compiles_for_sm100a(L, ranks, keep):
-    """The mask-specialised delta contraction (vest_sparse.cu) is generated and
-    NVRTC-compiled for sm_100a on the host -- no GPU involved."""
+def test_sparse_delta_source_compiles_for_sm100a(L, ranks, keep, f32, monkeypatch):
+    """The mask-specialised delta contraction (vest_sparse.cu) and the
+    plan-specialised core passes (vest_core_gen.cu) are generated and
+    NVRTC-compiled for sm_100a on the host -- no GPU involved -- with fp64 and
+    fp32 factor gathers."""
+    monkeypatch.setenv("VEST_GATHER_F32", f32)
     g = int(np.prod(ranks))
     mask = (np.random.default_rng(44).random(g) >= keep).astype(np.uint8)
     r = np.asarray(ranks, np.uint64)

@@ -7,6 +7,7 @@ tensor's contents change in place).  Checked against the C restatement
 import numpy as np
 import pytest
 
+from parity import assert_close
 from test_gpu_oracle import oracle_session, random_instance
 
 pytestmark = pytest.mark.gpu
@@ -66,6 +67,8 @@ def test_partial_reconstruct_bit_identical(dims, ranks, nnz, mask):
 def test_scratch_overloads(reg):
     dims, ranks = [40, 6, 5], [4, 3, 3]
     coords, values, m = random_instance(dims, ranks, 400, 47, mask_frac=0.2)
+    keep = coords[:, 0] != 7  # row 7 of mode 0 has no entries
+    coords, values = coords[keep], values[keep]
     x = st.make_tensor(dims, coords, values)
     idx = st.build_mode_index(x)
     ref = oracle_session(dims, ranks, coords, values, m)
@@ -81,7 +84,7 @@ def test_scratch_overloads(reg):
         fn(m, x, idx, 0, i, 0.05, s)
         ref.update_factor_row(reg, 0, i, 0.05)
         _, _, fs, _ = ref.get_model()
-        assert np.array_equal(m.factors[0][i], fs[0][i])
+        assert_close(m.factors[0][i], fs[0][i], f"row {i}")  # the solve's arithmetic order differs
         if reg == 0 and i == empty:
             assert np.all(s.gram == 7.0)
         else:
@@ -91,6 +94,8 @@ def test_scratch_overloads(reg):
     # the rest of the model is untouched by a row update
     for n in (1, 2):
         assert np.array_equal(m.factors[n], ref.get_model()[2][n])
+    others = np.setdiff1d(np.arange(dims[0]), [busy, empty])
+    assert np.array_equal(m.factors[0][others], ref.get_model()[2][0][others])
 
 
 def test_context_cache_follows_in_place_edits():
