@@ -334,15 +334,18 @@ def roofline_for(c, fams, steps, ms_total, peak_tf, hbm_peak, core_live, nnz_loc
         sweeps = steps
         fl = c_fl * nnz_local * sweeps / max(core_n, 1)
         by = c_by * nnz_local * sweeps / max(core_n, 1)
-        kernel = "core-sweep block pass (per pass; one sweep's algorithmic work spread over its passes)"
+        kernel = ("core-sweep block pass (per pass; one sweep's algorithmic work spread over its passes; "
+                  + ("vest_cp_* plan-specialised)" if len(ranks) > 3 else "all-prefix statistics/group passes)"))
         fam = "core_pass"
         share = core_ms / ms_total
     ach = fl / (avg * 1e-3) / 1e12
     ach_b = by / (avg * 1e-3) / 1e9
+    prof = traffic_db.get(fam) or {}
     return {
         "bound": "fp64", "kernel": kernel, "family": fam, "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
         "frac": ach / peak_tf, "peak_source": "measured live: vest_measure_fp64_peak (DFMA microbenchmark)",
-        "traffic": traffic_db.get(fam), "flops_per_launch": fl, "avg_launch_ms": avg, "step_share": share,
+        "traffic": prof.get("traffic"), "flops_per_launch": fl, "avg_launch_ms": avg, "step_share": share,
+        "ncu": {k: v for k, v in prof.items() if k != "traffic"} or None,
         "hbm": {"achieved": ach_b, "peak": hbm_peak, "unit": "GB/s", "frac": ach_b / hbm_peak,
                 "bytes_per_launch": by, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
     }
@@ -451,6 +454,19 @@ def run_ours(args, rank, world, local_rank):
         nnz_local = c["nnz"]
     m0 = model_for(c)
     core_live = int(np.count_nonzero(m0.core_mask == 0))
+    gf32 = bool(c.get("gather_f32")) and not args.fp64_gathers
+    alt = None
+    if gf32:
+        # BASELINE config 4 is the fp32 configuration: the generated kernels
+        # gather fp32 copies of the factor rows (fp64 arithmetic; north_star's
+        # stated fp32 tolerance 1e-4, tests/test_gpu_generated.py).  The same
+        # steps with fp64 gathers are timed first and reported beside it.
+        dev.set_gather_f32(False)
+        dev.set_model(m0)
+        ms64, _, fams64, _ = measure(dev, c, args.steps, args.warmup, world, dist, local_rank, L, _lib, torch)
+        alt = {"value": c["nnz"] * args.steps / (ms64 * 1e-3), "ms_per_step": ms64 / args.steps,
+               "gathers": "fp64", "kernel_families_ms": fams64}
+        dev.set_gather_f32(True)
     dev.set_model(m0)
     clk = Clocks(local_rank).__enter__()  # sampling covers warm-up and the timed region
     ms, res, fams, launches = measure(dev, c, args.steps, args.warmup, world, dist, local_rank, L, _lib, torch)
@@ -505,7 +521,10 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded; BASELINE config {cfg_id} shape)",
-        "config": workload_config(cfg_id, world),
+        "config": dict(workload_config(cfg_id, world),
+                       gathers=("fp32 copies of the factor rows in the generated kernels (fp64 arithmetic and "
+                                "storage; north_star fp32 tolerance 1e-4)" if gf32 else "fp64")),
+        "fp64_gathers": alt,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "path": "vest_cd_iteration_host: host model in/out (pinned)"},
         "gpu_launches": launches,
@@ -549,7 +568,7 @@ CONFIGS = {
             zipf=[1.1, 1.1, 0.0], values_kind=1, iters=10, prune=[], core_keep=1.0),
     4: dict(desc="4-mode 1M^4, 200M uniform, N(0,1) as float, R 8^4 core pruned to 10% nonzero, lambda 0.01; "
                  "10 iterations", dims=[1_000_000] * 4, nnz=200_000_000, ranks=[8, 8, 8, 8], lam=0.01, zipf=None,
-            values_kind=2, iters=10, prune=[], core_keep=0.1),
+            values_kind=2, iters=10, prune=[], core_keep=0.1, gather_f32=True),
     5: dict(desc="5-mode 100k^5, 100M Zipf(1.0) per mode, fp64 U[0,1), R 5^5; 90/10 split; prune-rate sweep "
                  "0.1..0.9 with train/test RE", dims=[100_000] * 5, nnz=100_000_000, ranks=[5] * 5, lam=0.01,
             zipf=[1.0] * 5, values_kind=0, iters=5, prune=[], core_keep=1.0, sweep=True),
@@ -624,6 +643,8 @@ def run_config(cfg_id, iters_override=None):
         mask = (rng.random(m.core.shape) >= c["core_keep"]).astype(np.uint8)
         m.core[mask == 1] = 0.0
         m.core_mask = mask
+    if c.get("gather_f32") and os.environ.get("VEST_GATHER_F32") is None:
+        dev.set_gather_f32(True)
     dev.set_model(m)
     stream = torch.cuda.ExternalStream(dev.stream())
     iters = iters_override or c["iters"]
@@ -685,6 +706,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--fp64-gathers", action="store_true", help="config 4: fp64 factor gathers only")
     ap.add_argument("--workload", type=int, default=HEADLINE, help="BASELINE config of the headline line")
     ap.add_argument("--secondary", type=int, default=SECONDARY,
                     help="BASELINE config measured after the headline as an extra key (0: none)")

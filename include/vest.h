@@ -89,7 +89,8 @@ int vest_ctx_set_core_gen(vest_ctx* ctx, int mode);
 int vest_ctx_set_gather_f32(vest_ctx* ctx, int on);
 /* With the mask-specialised delta: fuse the contraction with the row
  * statistics and solves in one kernel (modes other than the one carrying the
- * fused residual).  -1 auto (on), 0 off (delta through HBM, A/B), 1 on. */
+ * fused residual; bit-identical).  -1 auto (= off: the one-entry-per-lane
+ * fused kernel measured slower than the two-kernel path), 0 off, 1 on. */
 int vest_ctx_set_sparse_fused(vest_ctx* ctx, int mode);
 /* Host-only: generate and NVRTC-compile that contraction for ranks and a core
  * mask (no GPU needed); *cubin_bytes = size of the sm_100a cubin. */

@@ -26,7 +26,6 @@
 
 namespace vest {
 
-
 struct CoreGenArgs {
   const uint32_t* oc[VEST_MAXN];
   const double* f[VEST_MAXN];

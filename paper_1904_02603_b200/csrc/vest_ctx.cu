@@ -398,10 +398,15 @@ __global__ void k_factor_f32(const double* __restrict__ src, float* __restrict__
 }
 
 void refresh_factor_shadows(Ctx& c, int skip_mode) {
+  if (!c.d_factor32[0]) {  // one contiguous buffer, modes in order (one L2 access-policy window covers them)
+    uint64_t off[VEST_MAXN + 1] = {};
+    for (int k = 0; k < c.N; ++k) off[k + 1] = off[k] + ((c.dims[k] * (uint64_t)c.ld[k] + 63) & ~63ull);
+    float* base = static_cast<float*>(dalloc(c, std::max<uint64_t>(off[c.N], 1) * sizeof(float)));
+    for (int k = 0; k < c.N; ++k) c.d_factor32[k] = base + off[k];
+  }
   for (int k = 0; k < c.N; ++k) {
     if (k == skip_mode) continue;
     const uint64_t n = c.dims[k] * (uint64_t)c.ld[k];
-    if (!c.d_factor32[k]) c.d_factor32[k] = static_cast<float*>(dalloc(c, std::max<uint64_t>(n, 1) * sizeof(float)));
     k_factor_f32<<<592, 256, 0, c.stream>>>(c.d_factor[k], c.d_factor32[k], n);
     count_launch();
   }
@@ -1013,10 +1018,10 @@ int vest_ctx_destroy(vest_ctx* h) {
     cudaFree(md.d_empty);
     cudaFree(md.d_heavy_chunks);
     cudaFree(c.d_factor[n]);
-    cudaFree(c.d_factor32[n]);
     cudaFree(c.d_fmask[n]);
     cudaFree(c.d_resp_f[n]);
   }
+  cudaFree(c.d_factor32[0]);  // one buffer for every mode's shadow
   cudaFree(c.d_core);
   cudaFree(c.d_core_mask);
   cudaFree(c.d_cellbeta);

@@ -385,7 +385,8 @@ extern "C" int vest_measure_fp64_peak(int device, double* tflops) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int blocks = sms * 8, threads = 256, iters = 4096;
+  // ~4 ms per launch (short launches under-report the pipe by their ramp/tail)
+  const int blocks = sms * 8, threads = 256, iters = 32768;
   k_dfma_peak<<<blocks, threads>>>(out, 256, 0.999999, 1e-7);  // warm up clocks
   double best = 0.0;
   for (int rep = 0; rep < 5; ++rep) {

@@ -253,7 +253,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 constexpr int kXld = 36;
-template <int NC>
+// Gram of the staged columns (delta_0..delta_{J-1}, x): tile (1,1) only when
+// delta has rows >= 8 (J > 8); for J == 8 it would hold x.x, which no one reads
+template <int NC, bool T11>
 __device__ __forceinline__ void gram_dmma(const double* X, double (&d)[3][2], int lane) {
   const int g = lane >> 2, tq = lane & 3;
 #pragma unroll
@@ -264,10 +266,11 @@ __device__ __forceinline__ void gram_dmma(const double* X, double (&d)[3][2], in
     if constexpr (NC > 8) {
       const double f1 = X[(8 + g) * kXld + e];
       dmma884(d[1][0], d[1][1], f0, f1);
-      dmma884(d[2][0], d[2][1], f1, f1);
+      if constexpr (T11) dmma884(d[2][0], d[2][1], f1, f1);
     }
   }
 }
+
 __device__ __forceinline__ void gram_coord(int t, int i, int lane, int& row, int& col) {
   const int I = t == 2 ? 1 : 0, J = t == 0 ? 0 : 1;
   row = 8 * I + (lane >> 2);
@@ -328,7 +331,7 @@ void emit_fused(std::ostringstream& o, const Ctx& c, int n) {
   for (int j = 0; j < J; ++j) o << "    wsm[" << j << " * kXld + lane] = valid ? d" << j << "e0 : 0.0;\n";
   o << "    wsm[J * kXld + lane] = valid ? __ldg(a.val + pos) : 0.0;\n"
     << "    __syncwarp();\n"
-    << "    gram_dmma<J + 1>(wsm, tc, lane);\n"
+    << "    gram_dmma<J + 1, (J > 8)>(wsm, tc, lane);\n"
     << "    __syncwarp();\n"
     << "  }\n"
     << "  double* Gs = wsm;\n"
@@ -563,7 +566,7 @@ bool sparse_fused_enabled(const Ctx& c) {
     return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
   }();
   const int mode = c.sparse_fused >= 0 ? c.sparse_fused : env;
-  return mode != 0 && fused_ok(c);
+  return mode == 1 && fused_ok(c);  // auto = off: measured slower than vest_sd + k_rowpass_delta
 }
 
 // One factor mode through the fused kernel (statistics + light-row solves),

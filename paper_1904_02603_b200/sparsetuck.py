@@ -289,8 +289,8 @@ class Device:
         check(self._L.vest_ctx_set_sparse_delta(self.h, int(mode)))
 
     def set_sparse_fused(self, mode: int):
-        """-1 auto, 0: mask-specialised delta through HBM + statistics kernel,
-        1: one fused kernel per factor mode (bit-identical)."""
+        """-1 auto (= 0), 0: mask-specialised delta through HBM + statistics
+        kernel, 1: one fused kernel per factor mode (bit-identical, slower)."""
         check(self._L.vest_ctx_set_sparse_fused(self.h, int(mode)))
 
     def set_gather_f32(self, on: bool):
