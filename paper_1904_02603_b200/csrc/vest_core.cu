@@ -1149,12 +1149,15 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
 // The sampled live-cell Gram (k_core_hsample) for block bi of a general plan,
 // into c.d_gemm_out as [H packed | C]; returns its length, or -1 when the
 // dense block GEMM is cheaper (dense blocks) or the block is too wide.
-int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
+// The sampled live-cell Gram's entry table of block bi (H[q,q'] / C[q] of the
+// block's live cells -> statistics row | c | c'), or empty when the dense block
+// GEMM is the cheaper path.
+static std::vector<uint32_t> hsample_table(const Ctx& c, const Blocks& b, int bi) {
   const int m = c.N - 1, Jm = c.ranks[m];
   const int nf = b.len[bi], nl = b.nlive[bi];
   const int E = nl * (nl + 1) / 2 + nl;
   const int NS = nf * (nf + 1) / 2, NAm = Jm * (Jm + 1) / 2;
-  if (E > kHsPer * kHsThreads || 4 * E >= (NS + nf) * (NAm + Jm)) return -1;
+  if (E > kHsPer * kHsThreads || 4 * E >= (NS + nf) * (NAm + Jm)) return {};
   std::vector<int> lq;
   for (int f = 0; f < nf; ++f)
     for (int q = 0; q < Jm; ++q)
@@ -1169,8 +1172,37 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
     }
     tab[nl * (nl + 1) / 2 + i] = (uint32_t)(NS + fi) | (uint32_t)ci << 16 | 255u << 24;
   }
-  ensure(c, reinterpret_cast<double**>(&c.d_hstab), &c.hstab_cap, (size_t)(E + 1) / 2 + 1);
-  check(cudaMemcpyAsync(c.d_hstab, tab.data(), (size_t)E * 4, cudaMemcpyHostToDevice, c.stream), "hsample table");
+  return tab;
+}
+
+// Every block's table in one device buffer, uploaded only when the plan
+// changes (a copy from a host buffer must not be recorded into an iteration
+// graph; the tables depend on the core mask only).
+static void upload_hsample_tables(Ctx& c, const Blocks& b) {
+  std::vector<uint32_t> all;
+  std::vector<int64_t> off(b.start.size(), -1);
+  for (size_t bi = 0; bi < b.start.size(); ++bi) {
+    const std::vector<uint32_t> t = hsample_table(c, b, (int)bi);
+    if (t.empty()) continue;
+    off[bi] = (int64_t)all.size();
+    all.insert(all.end(), t.begin(), t.end());
+  }
+  c.hstab_off = off;
+  if (c.d_hstab && c.h_hstab == all) return;
+  ensure(c, reinterpret_cast<double**>(&c.d_hstab), &c.hstab_cap, (all.size() + 1) / 2 + 1);
+  if (!all.empty())
+    check(cudaMemcpyAsync(c.d_hstab, all.data(), all.size() * 4, cudaMemcpyHostToDevice, c.stream), "hsample tables");
+  check(cudaStreamSynchronize(c.stream), "hsample tables");
+  c.h_hstab = all;
+}
+
+int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
+  const int m = c.N - 1, Jm = c.ranks[m];
+  const int nf = b.len[bi], nl = b.nlive[bi];
+  const int E = nl * (nl + 1) / 2 + nl;
+  const int NS = nf * (nf + 1) / 2;
+  if (bi >= (int)c.hstab_off.size() || c.hstab_off[bi] < 0) return -1;
+  const uint32_t* tab = c.d_hstab + c.hstab_off[bi];
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
   const ModeData& md = c.modes[m];
@@ -1184,7 +1216,7 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
   ProfScope ps(c, kProfCoreGemm);
   check(cudaFuncSetAttribute(k_core_hsample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "hsample smem");
   k_core_hsample<<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks, md.nchunks,
-                                                        c.d_factor[m], c.ld[m], Jm, c.d_hstab, E, c.d_gemm_part);
+                                                        c.d_factor[m], c.ld[m], Jm, tab, E, c.d_gemm_part);
   k_gemm_reduce1<<<dim3((E + 255) / 256, groups), 256, 0, c.stream>>>(c.d_gemm_part, nparts, E, groups, raw);
   k_sum_groups<<<(E + 255) / 256, 256, 0, c.stream>>>(raw, E, groups, c.d_gemm_out);
   count_launch(3);
@@ -1220,10 +1252,15 @@ void pack_operands(Ctx& c, const void* sops) {
 
 }  // namespace
 
+// 3-mode all-prefix sweep, or the general sweep through the plan-specialised
+// passes (their modules are built by the time the key has repeated)
 bool core_sweep_capturable(const Ctx& c) {
   const void* sops = structured_ops(c);
-  return sops && !legacy_block_passes() && find_core_all_ops(c.N, c.ranks);
+  if (sops) return !legacy_block_passes() && find_core_all_ops(c.N, c.ranks);
+  return use_core_gen(c);
 }
+
+bool core_sweep_general(const Ctx& c) { return structured_ops(c) == nullptr; }
 
 // the general plan's blocks (host-only compile check of the generated passes)
 std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c) { return block_lists(plan_general(c, pick_block(c))); }
@@ -1271,6 +1308,7 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
   // plan-specialised passes (vest_core_gen.cu) for the general plans
   const bool gen = !sops && use_core_gen(c);
   if (gen) core_gen_prepare(c, block_lists(b), plan_key(c, b, F));
+  if (!sops) upload_hsample_tables(c, b);
   for (int bi = 0; bi <= nb; ++bi) {
     const bool last = bi == nb;
     if (gen) {
@@ -1294,8 +1332,11 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
     count_launch();
     check(cudaGetLastError(), "core solve");
   }
-  c.sum_sq = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);
-  c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  const double ss = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);  // captured: read after the replay
+  if (!c.capturing) {
+    c.sum_sq = ss;
+    c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  }
   c.r_valid = true;
   c.r_fresh = true;
 }

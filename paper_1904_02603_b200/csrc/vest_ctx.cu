@@ -1283,12 +1283,20 @@ static void graph_replay(Ctx& c) {
   launch_counter() += c.graph_launches;
   note_sweep(c);
   check(cudaStreamSynchronize(c.stream), "graph sync");
+  c.table_valid = false;
+  if (c.graph_general) {  // the general sweep ends with r current and its sum read back
+    c.r_valid = true;
+    c.r_fresh = true;
+    c.r_pending[0] = c.r_pending[1] = -1;
+    c.sum_sq = c.h_small[0];
+    c.re = std::sqrt(c.sum_sq) / c.x_norm;
+    return;
+  }
   c.r_valid = false;
   c.r_fresh = false;
   c.r_pending[0] = c.graph_pending[0];
   c.r_pending[1] = c.graph_pending[1];
   c.r_pending_ops = c.graph_pending_ops;
-  c.table_valid = false;
   sum_from_quadratic_form(c);
 }
 
@@ -1330,6 +1338,7 @@ int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
         c.graph_key = key;
         c.graph_launches = launch_counter() - l0;
         launch_counter() = l0;  // counted when replayed
+        c.graph_general = core_sweep_general(c);
         c.graph_pending[0] = c.r_pending[0];
         c.graph_pending[1] = c.r_pending[1];
         c.graph_pending_ops = c.r_pending_ops;

@@ -211,11 +211,14 @@ struct Ctx {
   int graph_seen = 0;
   uint64_t graph_launches = 0;       // kernels per replay (launch accounting)
   int graph_pending[2] = {-1, -1};   // r_pending after the captured iteration
+  bool graph_general = false;        // the captured sweep is the general one (sum of squares in h_small[0])
   const void* graph_pending_ops = nullptr;
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
   int sparse_fused = -1;           // ... fused with the statistics (modes without the fused residual): -1 auto
   double* d_delta = nullptr;       size_t delta_cap = 0;    // delta[j][pos] of one mode (sparse path)
-  uint32_t* d_hstab = nullptr;     size_t hstab_cap = 0;    // live-cell Gram entry table (k_core_hsample)
+  uint32_t* d_hstab = nullptr;     size_t hstab_cap = 0;    // live-cell Gram entry tables (k_core_hsample)
+  std::vector<uint32_t> h_hstab;   // what d_hstab holds (every block of the plan)
+  std::vector<int64_t> hstab_off;  // per block: offset in d_hstab, -1 = dense block GEMM
   bool force_generic = false;
   int core_block = 0;  // fibers per block (0 = auto)
   const ShapeOps* ops = nullptr;
@@ -292,7 +295,8 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
 void update_factor_rows(Ctx& c, int mode, const uint32_t* rows, uint32_t nrows, int reg, double lambda);
 void compute_residual(Ctx& c);  // fresh r = x - B(alpha), sum_sq, re
 void core_sweep(Ctx& c, int reg, double lambda);
-bool core_sweep_capturable(const Ctx& c);  // the sweep takes the all-prefix path (no host syncs inside)
+bool core_sweep_capturable(const Ctx& c);  // the sweep has no host syncs inside (all-prefix or generated passes)
+bool core_sweep_general(const Ctx& c);     // the sweep is the general (not the 3-mode all-prefix) one
 uint64_t core_mask_hash(const Ctx& c);
 void responsibilities(Ctx& c);
 void prune(Ctx& c, double pr, uint64_t* counts);

@@ -34,6 +34,7 @@ double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n) {
   comm_allreduce(c, c.d_small, 1);  // residual sums are global over the shards
   check(cudaMemcpyAsync(c.h_small, c.d_small, sizeof(double), cudaMemcpyDeviceToHost, c.stream),
         "sum readback");
+  if (c.capturing) return 0.0;  // a captured read-back: the replay's caller reads h_small[0]
   check(cudaStreamSynchronize(c.stream), "sum sync");
   return c.h_small[0];
 }

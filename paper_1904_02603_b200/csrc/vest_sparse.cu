@@ -210,13 +210,24 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
   }
 }
 
+// CTAs per SM the delta kernel is register-budgeted for (VEST_SD_MINB: A/B;
+// 2 = 128 registers with some stack, 1 = up to 255 registers at half the warps)
+int sd_min_blocks() {
+  static const int v = [] {
+    const char* e = getenv("VEST_SD_MINB");
+    return e ? std::max(1, std::min(4, atoi(e))) : 2;
+  }();
+  return v;
+}
+
 void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
   std::vector<int> oth;
   const std::vector<Cell> cells = ordered_cells(c, n, oth);
   // two entries per thread (E = 0, 1: t and t + 256 of the block's stride
   // window): every core value is loaded once (uniform constant load) and
   // feeds both entries' FMAs
-  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) vest_sd_" << n << "(const SparseDeltaArgs a) {\n"
+  o << "extern \"C\" __global__ void __launch_bounds__(256, " << sd_min_blocks() << ") vest_sd_" << n
+    << "(const SparseDeltaArgs a) {\n"
     << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
     << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
   emit_row_loads(o, c, oth, 0, "a.p0 + t0");
@@ -537,7 +548,7 @@ void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
   a.stride = n;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  const unsigned grid = (unsigned)std::min<uint64_t>((n + 511) / 512, (uint64_t)sms * 4);
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 511) / 512, (uint64_t)sms * 2 * sd_min_blocks());
   void* args[] = {&a};
   check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->k[mode]), dim3(grid), dim3(256), args, 0, c.stream),
         "sparse delta launch");

@@ -497,15 +497,23 @@ def test_iteration_re_after_core_fully_pruned(ranks):
         assert re_ref == 1.0 and abs(re - re_ref) <= 1e-12, (re, re_ref)
 
 
-@pytest.mark.parametrize("ranks", [[5, 5, 5], [10, 10, 5]])
-def test_iteration_graph_replay_bit_identical(ranks):
-    """From the fifth iteration with an unchanged mask on, a 3-mode iteration is
-    captured once as a CUDA graph and replayed; it must reproduce the stream
-    path bit for bit (the stream path is forced by profiling, which disables
-    graphs), and a prune in between drops back to the stream path."""
+@pytest.mark.parametrize("dims,ranks,mf", [([60, 50, 40], [5, 5, 5], 0.0), ([60, 50, 40], [10, 10, 5], 0.0),
+                                           ([20, 18, 16, 14], [8, 8, 8, 8], 0.9),
+                                           ([9, 8, 8, 7, 7], [5, 5, 5, 5, 5], 0.0)])
+def test_iteration_graph_replay_bit_identical(dims, ranks, mf):
+    """From the fifth iteration with an unchanged mask on, an iteration is
+    captured once as a CUDA graph and replayed -- the 3-mode all-prefix sweep
+    and the general sweep (4-mode masked core: mask-specialised delta + plan-
+    specialised passes; 5-mode dense) -- and must reproduce the stream path
+    bit for bit (the stream path is forced by profiling, which disables
+    graphs); a prune in between drops back to the stream path."""
     from paper_1904_02603_b200 import _lib
-    dims = [60, 50, 40]
-    coords, values, m = random_instance(dims, ranks, 6000, 81, lo=0.0, hi=1.0)
+    coords, values, m = random_instance(dims, ranks, 6000 if len(dims) == 3 else 4000, 81, lo=0.0, hi=1.0,
+                                        mask_frac=0.0)
+    if mf > 0:
+        cm = (np.random.default_rng(5).random(m.core.shape) < mf).astype(np.uint8)
+        m.core[cm == 1] = 0.0
+        m.core_mask = cm
     x = st.make_tensor(dims, coords, values)
     out = []
     for profile in (0, 1):
@@ -524,5 +532,5 @@ def test_iteration_graph_replay_bit_identical(ranks):
     assert ra == rb
     assert la == lb  # replays are counted like the launches they contain
     assert np.array_equal(ma.core, mb.core)
-    for n in range(3):
+    for n in range(len(dims)):
         assert np.array_equal(ma.factors[n], mb.factors[n])
