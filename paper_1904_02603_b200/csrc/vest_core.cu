@@ -552,6 +552,10 @@ __device__ __forceinline__ void hs_cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void hs_cp16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 
 __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __restrict__ stats, int stride, int width,
                                                              const Chunk* __restrict__ chunks, uint32_t nchunks,
@@ -561,7 +565,10 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
   extern __shared__ double hs[];
   // two batch buffers [kHsBatch][width] + [kHsBatch][Jm]: the next batch's rows
   // are copied by cp.async while this batch is accumulated
-  const int bufw = kHsBatch * (width + Jm);
+  // statistics rows are staged in 16-byte pieces (stride and the smem row
+  // width are even)
+  const int wpad = (width + 1) & ~1;
+  const int bufw = kHsBatch * (wpad + Jm);
   const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
   const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
   uint32_t my[kHsPer];
@@ -575,10 +582,11 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
   auto stage = [&](uint32_t cb, int buf) {
     const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
     double* ss = hs + buf * bufw;
-    double* sa = ss + kHsBatch * width;
-    for (int b = 0; b < nb; ++b) {
-      const double* src = stats + (size_t)(cb + b) * stride;
-      for (int w = threadIdx.x; w < width; w += kHsThreads) hs_cp8(ss + b * width + w, src + w);
+    double* sa = ss + kHsBatch * wpad;
+    const int half = wpad / 2;
+    for (int t = threadIdx.x; t < nb * half; t += kHsThreads) {
+      const int b = t / half, w = 2 * (t - b * half);
+      hs_cp16(ss + b * wpad + w, stats + (size_t)(cb + b) * stride + w);
     }
     for (int t = threadIdx.x; t < nb * Jm; t += kHsThreads) {
       const int b = t / Jm, q = t - b * Jm;
@@ -598,13 +606,13 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
     }
     __syncthreads();
     const double* ss = hs + buf * bufw;
-    const double* sa = ss + kHsBatch * width;
+    const double* sa = ss + kHsBatch * wpad;
     for (int b = 0; b < nb; ++b) {
 #pragma unroll
       for (int j = 0; j < kHsPer; ++j) {
         if (my[j] == 0xffffffffu) continue;
         const uint32_t cj = my[j] >> 24;
-        double v = ss[b * width + (my[j] & 0xffffu)] * sa[b * Jm + ((my[j] >> 16) & 255u)];
+        double v = ss[b * wpad + (my[j] & 0xffffu)] * sa[b * Jm + ((my[j] >> 16) & 255u)];
         if (cj != 255u) v *= sa[b * Jm + cj];
         acc[j] += v;
       }
@@ -1212,7 +1220,7 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
   ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)E);
   double* raw = c.d_gemm_part + (size_t)nparts * E;
   const int width = NS + nf;
-  const size_t sm = (size_t)2 * kHsBatch * (width + Jm) * sizeof(double);
+  const size_t sm = (size_t)2 * kHsBatch * (((width + 1) & ~1) + Jm) * sizeof(double);
   ProfScope ps(c, kProfCoreGemm);
   check(cudaFuncSetAttribute(k_core_hsample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "hsample smem");
   k_core_hsample<<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks, md.nchunks,
@@ -1300,7 +1308,7 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
     }
   }
   if (sops) pack_operands(c, sops);
-  const int stride = F * (F + 1) / 2 + F;
+  const int stride = (F * (F + 1) / 2 + F + 1) & ~1;  // even: 16-byte aligned statistics rows
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
   ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
   ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);

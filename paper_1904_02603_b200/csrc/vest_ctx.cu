@@ -897,6 +897,7 @@ int vest_ctx_set_comm(vest_ctx* h, const vest_comm* comm) {
     c.comm_free = nullptr;
   }
   c.comm = CommHooks{};
+  c.comm_capturable = false;  // host callbacks block: never inside a graph
   if (comm) {
     c.comm.user = comm->user;
     c.comm.allreduce_sum = comm->allreduce_sum;
@@ -1243,8 +1244,8 @@ static bool graph_off() {
 }
 
 static bool graph_eligible(const Ctx& c) {
-  return !graph_off() && !c.prof_on && !c.comm.allreduce_sum && !c.comm.allgather_rows &&
-         core_sweep_capturable(c) && c.mask_sweeps >= 3;
+  const bool hooks_ok = (!c.comm.allreduce_sum && !c.comm.allgather_rows) || c.comm_capturable;
+  return !graph_off() && !c.prof_on && hooks_ok && core_sweep_capturable(c) && c.mask_sweeps >= 3;
 }
 
 static uint64_t graph_key_of(const Ctx& c, int reg, double lambda) {

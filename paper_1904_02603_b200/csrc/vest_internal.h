@@ -133,6 +133,7 @@ struct Ctx {
   uint64_t local_nnz[VEST_MAXN] = {};
   bool skewed[VEST_MAXN] = {};  // a row holds > 0.1 % of the entries (gathers of its row are hot)
   CommHooks comm;
+  bool comm_capturable = false;  // the hooks only enqueue on the stream (native NCCL): graphs allowed
   bool prof_on = false;
   std::vector<ProfEvent> prof_events;
   double prof_ms[8] = {};

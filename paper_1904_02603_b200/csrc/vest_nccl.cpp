@@ -170,6 +170,7 @@ void ctx_set_nccl(Ctx& c, int rank, int world, const void* id, const uint64_t* b
   c.comm.allreduce_sum = hook_allreduce;
   c.comm.allgather_rows = st_broadcast ? hook_allgather_rows : hook_allgather_rows_padded;
   c.comm_free = free_state;
+  c.comm_capturable = true;  // NCCL collectives are stream operations: an iteration graph may hold them
 }
 
 void nccl_unique_id(void* out) {

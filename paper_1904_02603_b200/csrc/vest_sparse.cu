@@ -125,11 +125,18 @@ std::vector<Cell> ordered_cells(const Ctx& c, int n, std::vector<int>& oth) {
 
 // Loads of entry E's other-mode factor rows into registers u<k>_<b>e<E>;
 // pos is the expression of the entry's CSF position.
-void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>& oth, int e, const std::string& pos) {
+void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>& oth, int e, const std::string& pos,
+                    int lazy = 0) {
   const std::string E = std::to_string(e);
   for (int k : oth) {
     const int ld = c.ld[k];
     const std::string rk = "r" + std::to_string(k) + "e" + E;
+    const int lvl = (int)(std::find(oth.begin(), oth.end(), k) - oth.begin());
+    if (lvl < lazy && lvl + 1 < (int)oth.size()) {  // read where the prefix opens (emit_cells), not held in registers
+      o << "    const " << (c.gather_f32 ? "float" : "double") << "* " << rk << " = a." << (c.gather_f32 ? "g" : "f")
+        << "[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos << ") * " << ld << "ull;\n";
+      continue;
+    }
     if (c.gather_f32) {  // fp32 copy of the row, widened to fp64 in registers
       const bool v4 = ld % 4 == 0;
       o << "    const float* " << rk << " = a.g[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos
@@ -164,7 +171,7 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
 // group t = sum G u_last, then d[beta_n] += w t.  Every core value G[lin] is a
 // constant-bank operand shared by the ne entries.
 void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<int>& oth, const std::vector<Cell>& cells,
-                int ne) {
+                int ne, int lazy = 0) {
   const int L = (int)oth.size();
   for (int e = 0; e < ne; ++e)
     for (int j = 0; j < c.ranks[n]; ++j) o << "    double d" << j << "e" << e << " = 0.0;\n";
@@ -180,8 +187,10 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
       o << "    {";
       for (int e = 0; e < ne; ++e) {
         const std::string E = std::to_string(e);
-        if (q == 0) o << " const double w0e" << E << " = " << u(k, b) << "e" << E << ";";
-        else o << " const double w" << q << "e" << E << " = w" << (q - 1) << "e" << E << " * " << u(k, b) << "e" << E << ";";
+        const std::string val = q < lazy ? "(double)__ldg(r" + std::to_string(k) + "e" + E + " + " + std::to_string(b) + ")"
+                                         : u(k, b) + "e" + E;
+        if (q == 0) o << " const double w0e" << E << " = " << val << ";";
+        else o << " const double w" << q << "e" << E << " = w" << (q - 1) << "e" << E << " * " << val << ";";
       }
       o << "\n";
     }
@@ -210,6 +219,18 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
   }
 }
 
+// VEST_SD_LAZY (A/B): the outermost prefix mode's factor values are read
+// (L1 hits) where their prefix opens instead of held in registers
+// (default 1: fewer live registers, less spill traffic at 2 entries per
+// thread; config 4 measured 270.0 / 267.5 / 272.1 ms per iteration at 0 / 1 / 2)
+int sd_lazy() {  // prefix levels read lazily: 0, 1 (outermost) or 2 (the two outer levels)
+  static const int v = [] {
+    const char* e = getenv("VEST_SD_LAZY");
+    return e ? std::max(0, std::min(2, atoi(e))) : 1;
+  }();
+  return v;
+}
+
 // CTAs per SM the delta kernel is register-budgeted for (VEST_SD_MINB: A/B;
 // 2 = 128 registers with some stack, 1 = up to 255 registers at half the warps)
 int sd_min_blocks() {
@@ -230,9 +251,10 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     << "(const SparseDeltaArgs a) {\n"
     << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
     << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
-  emit_row_loads(o, c, oth, 0, "a.p0 + t0");
-  emit_row_loads(o, c, oth, 1, "a.p0 + t1");
-  emit_cells(o, c, n, oth, cells, 2);
+  const int lazy = oth.size() >= 2 ? std::min<int>(sd_lazy(), (int)oth.size() - 1) : 0;
+  emit_row_loads(o, c, oth, 0, "a.p0 + t0", lazy);
+  emit_row_loads(o, c, oth, 1, "a.p0 + t1", lazy);
+  emit_cells(o, c, n, oth, cells, 2, lazy);
   for (int j = 0; j < c.ranks[n]; ++j) o << "    a.out[" << j << "ull * a.stride + t0] = d" << j << "e0;\n";
   o << "    if (t1 != t0) {\n";
   for (int j = 0; j < c.ranks[n]; ++j) o << "      a.out[" << j << "ull * a.stride + t1] = d" << j << "e1;\n";

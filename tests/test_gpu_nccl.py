@@ -1,8 +1,8 @@
 """The native NCCL exchange path (vest_ctx_set_nccl, sharded.NcclNative) on one
 GPU: a world-size-1 NCCL communicator installed in a shard context runs every
-exchange point of the sweep (ncclAllReduce, grouped ncclBroadcast on the
-library's stream) and must leave the results bit-identical to the unsharded
-context.  (World sizes > 1 run under torchrun on multi-GPU boxes; the sharded
+exchange point of the sweep (ncclAllReduce, the padded ncclAllGather on the
+library's stream; from the fifth iteration inside the iteration's CUDA graph)
+and must leave the results bit-identical to the unsharded context.  (World sizes > 1 run under torchrun on multi-GPU boxes; the sharded
 algebra itself is covered by test_gpu_sharded.py and test_dist_gloo.py.)"""
 import os
 import socket
@@ -38,8 +38,10 @@ def nccl_group():
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("rows", ["allgather", "broadcast"])
 @pytest.mark.parametrize("ranks", [[10, 10, 10], [3, 4, 2], [4, 3, 2, 3]])
-def test_native_nccl_world1_bit_identical(nccl_group, ranks):
+def test_native_nccl_world1_bit_identical(nccl_group, ranks, rows, monkeypatch):
+    monkeypatch.setenv("VEST_NCCL_ROWS", rows)  # row exchange: padded all-gather or per-rank broadcasts
     rng = np.random.default_rng(3)
     dims = [50, 40, 30, 12][: len(ranks)]
     cells = np.sort(rng.choice(int(np.prod(dims)), size=5000, replace=False))
@@ -49,7 +51,9 @@ def test_native_nccl_world1_bit_identical(nccl_group, ranks):
     ref.init_random(4)
     dev = sh.ShardDevice(x, ranks, 0, 1, sh.NcclNative())
     dev.init_random(4)
-    for it in range(3):
+    # 8 iterations: from the fifth the iteration (NCCL collectives included)
+    # is replayed as a CUDA graph on both contexts
+    for it in range(8):
         a = ref.cd_iteration(0, 0.02)
         b = dev.cd_iteration(0, 0.02)
         assert a == b, (it, a, b)
