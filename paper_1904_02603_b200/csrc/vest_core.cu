@@ -552,23 +552,25 @@ __device__ __forceinline__ void hs_cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
-__device__ __forceinline__ void hs_cp16(double* dst, const double* src) {
+__device__ __forceinline__ void hs_cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
 
-__global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __restrict__ stats, int stride, int width,
+template <class T>
+__global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict__ stats, int stride, int width,
                                                              const Chunk* __restrict__ chunks, uint32_t nchunks,
                                                              const double* __restrict__ A, int ld, int Jm,
                                                              const uint32_t* __restrict__ tab, int E,
                                                              double* __restrict__ partial) {
-  extern __shared__ double hs[];
-  // two batch buffers [kHsBatch][width] + [kHsBatch][Jm]: the next batch's rows
-  // are copied by cp.async while this batch is accumulated
+  extern __shared__ double hs_raw[];
+  // two batch buffers [kHsBatch][width] (T) + [kHsBatch][Jm] (double): the next
+  // batch's rows are copied by cp.async while this batch is accumulated;
   // statistics rows are staged in 16-byte pieces (stride and the smem row
-  // width are even)
-  const int wpad = (width + 1) & ~1;
-  const int bufw = kHsBatch * (wpad + Jm);
+  // width are multiples of 16 bytes)
+  constexpr int V = 16 / sizeof(T);
+  const int wpad = (width + V - 1) / V * V;
+  const int bufw = kHsBatch * wpad;  // T elements per statistics buffer
   const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
   const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
   uint32_t my[kHsPer];
@@ -579,13 +581,15 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
     my[j] = e < E ? __ldg(tab + e) : 0xffffffffu;
     acc[j] = 0.0;
   }
+  T* const sstat = reinterpret_cast<T*>(hs_raw);                     // [2][kHsBatch][wpad]
+  double* const sarow = reinterpret_cast<double*>(sstat + 2 * bufw);  // [2][kHsBatch][Jm]
   auto stage = [&](uint32_t cb, int buf) {
     const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
-    double* ss = hs + buf * bufw;
-    double* sa = ss + kHsBatch * wpad;
-    const int half = wpad / 2;
-    for (int t = threadIdx.x; t < nb * half; t += kHsThreads) {
-      const int b = t / half, w = 2 * (t - b * half);
+    T* ss = sstat + buf * bufw;
+    double* sa = sarow + buf * kHsBatch * Jm;
+    const int pieces = wpad / V;
+    for (int t = threadIdx.x; t < nb * pieces; t += kHsThreads) {
+      const int b = t / pieces, w = V * (t - b * pieces);
       hs_cp16(ss + b * wpad + w, stats + (size_t)(cb + b) * stride + w);
     }
     for (int t = threadIdx.x; t < nb * Jm; t += kHsThreads) {
@@ -605,14 +609,14 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const double* __res
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const double* ss = hs + buf * bufw;
-    const double* sa = ss + kHsBatch * wpad;
+    const T* ss = sstat + buf * bufw;
+    const double* sa = sarow + buf * kHsBatch * Jm;
     for (int b = 0; b < nb; ++b) {
 #pragma unroll
       for (int j = 0; j < kHsPer; ++j) {
         if (my[j] == 0xffffffffu) continue;
         const uint32_t cj = my[j] >> 24;
-        double v = ss[b * wpad + (my[j] & 0xffffu)] * sa[b * Jm + ((my[j] >> 16) & 255u)];
+        double v = (double)ss[b * wpad + (my[j] & 0xffffu)] * sa[b * Jm + ((my[j] >> 16) & 255u)];
         if (cj != 255u) v *= sa[b * Jm + cj];
         acc[j] += v;
       }
@@ -1160,12 +1164,19 @@ int block_gemm(Ctx& c, int nf, int kind, int stride) {
 // The sampled live-cell Gram's entry table of block bi (H[q,q'] / C[q] of the
 // block's live cells -> statistics row | c | c'), or empty when the dense block
 // GEMM is the cheaper path.
+static bool hsample_eligible(const Ctx& c, int nf, int nl) {
+  const int Jm = c.ranks[c.N - 1];
+  const int E = nl * (nl + 1) / 2 + nl;
+  const int NS = nf * (nf + 1) / 2, NAm = Jm * (Jm + 1) / 2;
+  return E <= kHsPer * kHsThreads && 4 * E < (NS + nf) * (NAm + Jm);
+}
+
 static std::vector<uint32_t> hsample_table(const Ctx& c, const Blocks& b, int bi) {
   const int m = c.N - 1, Jm = c.ranks[m];
   const int nf = b.len[bi], nl = b.nlive[bi];
   const int E = nl * (nl + 1) / 2 + nl;
-  const int NS = nf * (nf + 1) / 2, NAm = Jm * (Jm + 1) / 2;
-  if (E > kHsPer * kHsThreads || 4 * E >= (NS + nf) * (NAm + Jm)) return {};
+  const int NS = nf * (nf + 1) / 2;
+  if (!hsample_eligible(c, nf, nl)) return {};
   std::vector<int> lq;
   for (int f = 0; f < nf; ++f)
     for (int q = 0; q < Jm; ++q)
@@ -1220,11 +1231,22 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
   ensure(c, &c.d_gemm_out, &c.gemm_out_cap, (size_t)E);
   double* raw = c.d_gemm_part + (size_t)nparts * E;
   const int width = NS + nf;
-  const size_t sm = (size_t)2 * kHsBatch * (((width + 1) & ~1) + Jm) * sizeof(double);
   ProfScope ps(c, kProfCoreGemm);
-  check(cudaFuncSetAttribute(k_core_hsample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "hsample smem");
-  k_core_hsample<<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks, md.nchunks,
-                                                        c.d_factor[m], c.ld[m], Jm, tab, E, c.d_gemm_part);
+  if (c.stats_f32) {
+    const size_t sm = (size_t)2 * kHsBatch * (((width + 3) & ~3) * sizeof(float) + Jm * sizeof(double));
+    check(cudaFuncSetAttribute(k_core_hsample<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+          "hsample smem");
+    k_core_hsample<float><<<nparts, kHsThreads, sm, c.stream>>>(reinterpret_cast<const float*>(c.d_chunk_stats), stride,
+                                                                 width, md.d_chunks, md.nchunks, c.d_factor[m], c.ld[m],
+                                                                 Jm, tab, E, c.d_gemm_part);
+  } else {
+    const size_t sm = (size_t)2 * kHsBatch * (((width + 1) & ~1) + Jm) * sizeof(double);
+    check(cudaFuncSetAttribute(k_core_hsample<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+          "hsample smem");
+    k_core_hsample<double><<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks,
+                                                                  md.nchunks, c.d_factor[m], c.ld[m], Jm, tab, E,
+                                                                  c.d_gemm_part);
+  }
   k_gemm_reduce1<<<dim3((E + 255) / 256, groups), 256, 0, c.stream>>>(c.d_gemm_part, nparts, E, groups, raw);
   k_sum_groups<<<(E + 255) / 256, 256, 0, c.stream>>>(raw, E, groups, c.d_gemm_out);
   count_launch(3);
@@ -1308,7 +1330,14 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
     }
   }
   if (sops) pack_operands(c, sops);
-  const int stride = (F * (F + 1) / 2 + F + 1) & ~1;  // even: 16-byte aligned statistics rows
+  // fp32 mode with every block on the sampled Gram: the passes write fp32 chunk
+  // statistics (half the traffic to k_core_hsample); rows 16-byte aligned
+  c.stats_f32 = false;
+  if (!sops && c.gather_f32 && use_core_gen(c)) {
+    c.stats_f32 = true;
+    for (size_t bi = 0; bi < b.start.size(); ++bi) c.stats_f32 = c.stats_f32 && hsample_eligible(c, b.len[bi], b.nlive[bi]);
+  }
+  const int stride = c.stats_f32 ? (F * (F + 1) / 2 + F + 3) & ~3 : (F * (F + 1) / 2 + F + 1) & ~1;
   ensure(c, &c.d_chunk_stats, &c.chunk_stats_cap, (size_t)c.modes[m].nchunks * stride);
   ensure(c, &c.d_dg, &c.dg_cap, (size_t)kFMax * VEST_MAXJ);
   ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, c.modes[m].nchunks + 1);

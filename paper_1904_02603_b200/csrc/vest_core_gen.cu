@@ -189,7 +189,7 @@ extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
         if (lane == 0) a.chunk_sq[ci] = sq;
         sq = 0.0;
       } else {
-        double* out = a.stats + (unsigned long long)ci * a.stride;
+        @STATS_T@* out = reinterpret_cast<@STATS_T@*>(a.stats) + (unsigned long long)ci * a.stride;
         constexpr int NS = NF * (NF + 1) / 2;
         const int g = lane >> 2, tq = lane & 3;
         int t = 0;
@@ -200,8 +200,8 @@ extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
               const int row = 8 * I + g, col = 8 * J + 2 * tq + i;
-              if (row <= col && col < NF) out[row * NF - row * (row - 1) / 2 + (col - row)] = d[t][i];
-              else if (col == NC - 1 && row < NF) out[NS + row] = d[t][i];
+              if (row <= col && col < NF) out[row * NF - row * (row - 1) / 2 + (col - row)] = (@STATS_T@)d[t][i];
+              else if (col == NC - 1 && row < NF) out[NS + row] = (@STATS_T@)d[t][i];
               d[t][i] = 0.0;
             }
             ++t;
@@ -339,6 +339,7 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@JM@", std::to_string(c.ranks[M]));
     replace_all(p, "@LDM@", std::to_string(c.ld[M]));
     replace_all(p, "@RSLOT@", std::to_string(rslot));
+    replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
     replace_all(p, "@ISSUE@", iss.str());
     replace_all(p, "@LOADU@", lu.str());
     replace_all(p, "@PREV@", pv.str());

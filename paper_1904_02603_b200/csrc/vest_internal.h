@@ -159,6 +159,7 @@ struct Ctx {
   // use (refresh_factor_shadows).
   float* d_factor32[VEST_MAXN] = {};
   int gather_f32 = 0;
+  bool stats_f32 = false;  // the current general sweep's chunk statistics are fp32 (fp32 mode, sampled Gram)
   uint8_t* d_fmask[VEST_MAXN] = {};
   double* d_core = nullptr;
   uint8_t* d_core_mask = nullptr;

@@ -221,14 +221,16 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
 
 // VEST_SD_LAZY (A/B): the outermost prefix mode's factor values are read
 // (L1 hits) where their prefix opens instead of held in registers
-// (default 1: fewer live registers, less spill traffic at 2 entries per
-// thread; config 4 measured 270.0 / 267.5 / 272.1 ms per iteration at 0 / 1 / 2)
-int sd_lazy() {  // prefix levels read lazily: 0, 1 (outermost) or 2 (the two outer levels)
-  static const int v = [] {
+// (default: 1 with fp32 gathers -- fewer live registers, less spill traffic
+// at 2 entries per thread; config 4: 270.0 / 267.5 / 272.1 ms per iteration at
+// 0 / 1 / 2 -- and 0 with fp64 gathers, where the lazy reads cost more: factor
+// modes 83.5 -> 95.6 ms)
+int sd_lazy(const Ctx& c) {  // prefix levels read lazily: 0, 1 (outermost) or 2 (the two outer levels)
+  static const int env = [] {
     const char* e = getenv("VEST_SD_LAZY");
-    return e ? std::max(0, std::min(2, atoi(e))) : 1;
+    return e ? std::max(0, std::min(2, atoi(e))) : -1;
   }();
-  return v;
+  return env >= 0 ? env : (c.gather_f32 ? 1 : 0);
 }
 
 // CTAs per SM the delta kernel is register-budgeted for (VEST_SD_MINB: A/B;
@@ -251,7 +253,7 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     << "(const SparseDeltaArgs a) {\n"
     << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
     << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
-  const int lazy = oth.size() >= 2 ? std::min<int>(sd_lazy(), (int)oth.size() - 1) : 0;
+  const int lazy = oth.size() >= 2 ? std::min<int>(sd_lazy(c), (int)oth.size() - 1) : 0;
   emit_row_loads(o, c, oth, 0, "a.p0 + t0", lazy);
   emit_row_loads(o, c, oth, 1, "a.p0 + t1", lazy);
   emit_cells(o, c, n, oth, cells, 2, lazy);
@@ -649,6 +651,7 @@ int sparse_compile_check(int N, const int* ranks, const uint8_t* core_mask, uint
     }
     c.h_core_mask.assign(core_mask, core_mask + c.G);
     if (const char* e = getenv("VEST_GATHER_F32")) c.gather_f32 = e[0] == '1';
+    c.stats_f32 = c.gather_f32;  // the fp32-statistics form of the passes too
     *bytes = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu").size();
     if (N >= 2) {  // the plan-specialised core passes of the same mask
       std::vector<int> nts;

@@ -340,6 +340,22 @@ def test_fullsize_steady_state_kernels(cfg):
     check_gs(t, before.core, after.core, live, lam, f"config {cfg}")
     res = dev.compute_residuals()
     assert abs(res.re - t["re"]) <= 1e-6 * t["re"], (res.re, t["re"])
+    if cfg == 4:
+        # the fp32 mode bench.py times for config 4 (fp32 factor gathers, fp32
+        # chunk statistics; fp64 arithmetic): the same sweep and a factor mode
+        # within north_star's stated fp32 tolerance of the fp64 results
+        dev.set_gather_f32(True)
+        dev.set_model(before)
+        dev.update_core(0, lam)
+        f32 = dev.get_model()
+        assert_close(f32.core, after.core, "config 4 core sweep, fp32 mode", tol=1e-4)
+        dev.set_model(before)
+        dev.update_factor_mode(1, 0, lam)
+        f1_fp32 = dev.get_model().factors[1].copy()
+        dev.set_gather_f32(False)
+        dev.set_model(before)
+        dev.update_factor_mode(1, 0, lam)
+        assert_close(f1_fp32, dev.get_model().factors[1], "config 4 factor mode 1, fp32 mode", tol=1e-4)
     dev.close()
 
 
