@@ -90,7 +90,7 @@ __device__ __forceinline__ void gram_nt(const double* X, double (&d)[NT * (NT + 
 
 // one pass: KIND 0 (prev update + cur statistics) or 2 (prev update + r^2)
 const char* kPass = R"CUDA(
-extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
+extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenArgs a) {
   constexpr int M = @M@, LDR = @LDR@, NT = @NT@, NC = NT * 8, NTT = NT * (NT + 1) / 2;
   constexpr int NF = @NF@, PNF = @PNF@, KIND = @KIND@, JM = @JM@, RSLOT = @RSLOT@;
   extern __shared__ __align__(16) double smem[];
@@ -218,6 +218,16 @@ extern "C" __global__ void __launch_bounds__(128) @NAME@(const CoreGenArgs a) {
 }
 )CUDA";
 
+// CTAs per SM the passes are register-budgeted for (VEST_CP_MINB: A/B; 1 lets
+// the compiler take 160 registers = 3 CTAs/SM by registers)
+int cp_min_blocks() {
+  static const int v = [] {
+    const char* e = getenv("VEST_CP_MINB");
+    return e ? std::max(1, std::min(6, atoi(e))) : 1;
+  }();
+  return v;
+}
+
 void replace_all(std::string& s, const std::string& from, const std::string& to) {
   for (size_t p = 0; (p = s.find(from, p)) != std::string::npos; p += to.size()) s.replace(p, from.size(), to);
 }
@@ -339,6 +349,7 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@JM@", std::to_string(c.ranks[M]));
     replace_all(p, "@LDM@", std::to_string(c.ld[M]));
     replace_all(p, "@RSLOT@", std::to_string(rslot));
+    replace_all(p, "@MINB@", std::to_string(cp_min_blocks()));
     replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
     replace_all(p, "@ISSUE@", iss.str());
     replace_all(p, "@LOADU@", lu.str());
