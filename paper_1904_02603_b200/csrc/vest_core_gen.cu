@@ -218,12 +218,13 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
 }
 )CUDA";
 
-// CTAs per SM the passes are register-budgeted for (VEST_CP_MINB: A/B; 1 lets
-// the compiler take 160 registers = 3 CTAs/SM by registers)
+// CTAs per SM the passes are register-budgeted for (VEST_CP_MINB: A/B).
+// Config 4, fp32 mode, ms per iteration: no bound 259, 1: 254, 3: 250 (kept),
+// 4 (128 registers): 318.
 int cp_min_blocks() {
   static const int v = [] {
     const char* e = getenv("VEST_CP_MINB");
-    return e ? std::max(1, std::min(6, atoi(e))) : 1;
+    return e ? std::max(1, std::min(6, atoi(e))) : 3;
   }();
   return v;
 }
