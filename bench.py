@@ -604,6 +604,8 @@ def run_shard_emulation(cfg_id, world, iters):
     out = {"config": cfg_id, "world": world, "ranks": {}}
     for rank in sorted({0, world - 1}):
         dev = sh.ShardDevice(x, c["ranks"], rank, world, sh.NullComm(), bounds=bounds)
+        if c.get("gather_f32") and os.environ.get("VEST_GATHER_F32") is None:
+            dev.set_gather_f32(True)
         dev.set_model(m)
         stream = torch.cuda.ExternalStream(dev.stream())
         times = []
