@@ -645,9 +645,15 @@ __global__ void k_sum_groups(const double* raw, int n, int groups, double* out) 
 // (nl x nl, H_qq' = T[{f,f'}][{c,c'}]); then one warp runs the nl sequential
 // steps, each a handful of shared-memory reads plus one coalesced row update
 // of the remaining cells' c.  Masked cells keep dg = 0 (updates.hpp:199-202).
+// With s_out (packed statistics only): the sum of squared residuals after this
+// block's update from the statistics, s' = s - 2 dg.C + dg^T H dg (s = *s_in,
+// the sum before it; C the block's right-hand side before the Gauss-Seidel
+// corrections): s_out[0] = s', s_out[1] = s (the deferred last pass,
+// sum_from_quadratic_form).
 __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, int Jm, int nl, const uint32_t* fib,
                                                     double* core, const uint8_t* core_mask, int reg,
-                                                    double lambda, double* dg_out, int packed) {
+                                                    double lambda, double* dg_out, int packed,
+                                                    const double* s_in = nullptr, double* s_out = nullptr) {
   extern __shared__ double sm[];
   const int NAm = Jm * (Jm + 1) / 2;
   const int nT = nf * (nf + 1) / 2 * NAm;
@@ -723,6 +729,27 @@ __global__ void __launch_bounds__(256) k_core_solve(const double* tc, int nf, in
       for (int l2 = l + 1 + lane; l2 < nl; l2 += 32) cc[l2] = fma(-dg, hr[l2], cc[l2]);
     }
     __syncwarp();
+  }
+  if (s_out && packed) {
+    __syncwarp();  // dg_out (lane 0's writes) visible to the warp
+    double lin = 0.0, quad = 0.0;
+    for (int l = lane; l < nl; l += 32) {
+      const double dl = dg_out[lq[l]];
+      if (dl == 0.0) continue;
+      lin = fma(dl, tc[nh + l], lin);
+      double hd = 0.0;
+      for (int l2 = 0; l2 < nl; ++l2) hd = fma(H[l * nl + l2], dg_out[lq[l2]], hd);
+      quad = fma(dl, hd, quad);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lin += __shfl_xor_sync(0xffffffffu, lin, o);
+      quad += __shfl_xor_sync(0xffffffffu, quad, o);
+    }
+    if (lane == 0) {
+      s_out[0] = *s_in - 2.0 * lin + quad;
+      s_out[1] = *s_in;
+    }
   }
   for (int l = lane; l < nl; l += 32) {
     const int q = lq[l];
@@ -1292,6 +1319,31 @@ bool core_sweep_capturable(const Ctx& c) {
 
 bool core_sweep_general(const Ctx& c) { return structured_ops(c) == nullptr; }
 
+// VEST_DEFER_LAST=0: run the general sweep's final residual pass eagerly (A/B)
+bool defer_last_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_DEFER_LAST");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// Apply the general sweep's deferred last block to r (its final pass: previous
+// block's update + per-chunk r^2) and sum r^2 exactly.
+void core_apply_pending_general(Ctx& c) {
+  const int m = c.N - 1;
+  {
+    ProfScope ps(c, kProfResid);
+    core_gen_pass(c, c.r_pending[0], c.d_dg, c.d_chunk_stats, c.pending_stride, c.d_chunk_sum);
+  }
+  c.sum_sq = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);
+  c.re = std::sqrt(c.sum_sq) / c.x_norm;
+  c.r_valid = true;
+  c.r_fresh = true;
+  c.r_pending[0] = c.r_pending[1] = -1;
+  c.r_pending_general = false;
+}
+
 // the general plan's blocks (host-only compile check of the generated passes)
 std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c) { return block_lists(plan_general(c, pick_block(c))); }
 
@@ -1344,10 +1396,18 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
   const int nb = (int)b.start.size();
   // plan-specialised passes (vest_core_gen.cu) for the general plans
   const bool gen = !sops && use_core_gen(c);
+  // every block on the sampled Gram (packed statistics): the last block's
+  // residual update is deferred -- the sum of squares after it follows from its
+  // statistics, and r is brought up to date only if something reads it (the
+  // next iteration's last factor mode rewrites it anyway)
+  c.defer_last = gen && defer_last_enabled();
+  for (size_t bi = 0; c.defer_last && bi < b.start.size(); ++bi)
+    c.defer_last = hsample_eligible(c, b.len[bi], b.nlive[bi]);
   if (gen) core_gen_prepare(c, block_lists(b), plan_key(c, b, F));
   if (!sops) upload_hsample_tables(c, b);
   for (int bi = 0; bi <= nb; ++bi) {
     const bool last = bi == nb;
+    if (last && c.defer_last) break;
     if (gen) {
       ProfScope ps(c, kProfCorePass);
       core_gen_pass(c, bi, c.d_dg, c.d_chunk_stats, stride, c.d_chunk_sum);
@@ -1364,10 +1424,28 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
     const size_t nq = (size_t)nf * Jm, nl = (size_t)b.nlive[bi];
     const size_t sm = (nl * nl + 3 * nl) * sizeof(double) + nq * sizeof(int);
     check(cudaFuncSetAttribute(k_core_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "solve smem");
+    const bool quad = c.defer_last && bi == nb - 1;
+    if (quad) sum_chunks_device(c, c.d_chunk_sum, c.modes[m].nchunks, c.d_small + 2);  // s before the last block
     k_core_solve<<<1, 256, sm, c.stream>>>(c.d_gemm_out, nf, Jm, (int)nl, c.d_fibers + b.start[bi], c.d_core,
-                                           c.d_core_mask, reg, lambda, c.d_dg, packed);
+                                           c.d_core_mask, reg, lambda, c.d_dg, packed, quad ? c.d_small + 2 : nullptr,
+                                           quad ? c.d_small : nullptr);
     count_launch();
     check(cudaGetLastError(), "core solve");
+  }
+  if (c.defer_last) {
+    check(cudaMemcpyAsync(c.h_small, c.d_small, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "sum readback");
+    c.r_valid = false;
+    c.r_fresh = false;
+    c.r_pending[0] = nb;  // the skipped final pass
+    c.r_pending[1] = -1;
+    c.r_pending_ops = nullptr;
+    c.r_pending_general = true;
+    c.pending_stride = stride;
+    if (!c.capturing) {  // a captured iteration reads the sums after the graph launch
+      check(cudaStreamSynchronize(c.stream), "sum sync");
+      sum_from_quadratic_form(c);
+    }
+    return;
   }
   const double ss = reduce_chunk_sums(c, c.d_chunk_sum, c.modes[m].nchunks);  // captured: read after the replay
   if (!c.capturing) {

@@ -93,6 +93,7 @@ const char* kPass = R"CUDA(
 extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenArgs a) {
   constexpr int M = @M@, LDR = @LDR@, NT = @NT@, NC = NT * 8, NTT = NT * (NT + 1) / 2;
   constexpr int NF = @NF@, PNF = @PNF@, KIND = @KIND@, JM = @JM@, RSLOT = @RSLOT@;
+  constexpr bool WSQ = @WSQ@;  // statistics pass that also sums r^2 (after the previous block's update)
   extern __shared__ __align__(16) double smem[];
   __shared__ double sq_q[4][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -172,9 +173,8 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
       r -= t;
       a.r[pos] = r;
     }
-    if (KIND == 2) {
-      sq = fma(r, r, sq);
-    } else {
+    if (KIND == 2 || WSQ) sq = fma(r, r, sq);
+    if (KIND != 2) {
 @CUR@
       X[(NC - 1) * 36 + lane] = r;
       __syncwarp();
@@ -183,12 +183,13 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
     __syncwarp();
     if (nxt.ci != cur.ci) {
       const unsigned ci = cur.ci;
-      if (KIND == 2) {
+      if (KIND == 2 || WSQ) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
         if (lane == 0) a.chunk_sq[ci] = sq;
         sq = 0.0;
-      } else {
+      }
+      if (KIND != 2) {
         @STATS_T@* out = reinterpret_cast<@STATS_T@*>(a.stats) + (unsigned long long)ci * a.stride;
         constexpr int NS = NF * (NF + 1) / 2;
         const int g = lane >> 2, tq = lane & 3;
@@ -347,6 +348,7 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@NF@", std::to_string(nf));
     replace_all(p, "@PNF@", std::to_string(pnf));
     replace_all(p, "@KIND@", i == nb ? "2" : "0");
+    replace_all(p, "@WSQ@", c.defer_last && i == nb - 1 ? "true" : "false");
     replace_all(p, "@JM@", std::to_string(c.ranks[M]));
     replace_all(p, "@LDM@", std::to_string(c.ld[M]));
     replace_all(p, "@RSLOT@", std::to_string(rslot));

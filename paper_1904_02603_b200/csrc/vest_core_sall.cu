@@ -1096,6 +1096,7 @@ void core_sweep_sall(Ctx& c, const void* ops_, int reg, double lambda, const std
   c.r_pending[0] = prev[0];
   c.r_pending[1] = prev[1];
   c.r_pending_ops = ops_;
+  c.r_pending_general = false;
   if (!c.capturing) {  // a captured iteration reads the sum after the graph launch
     check(cudaStreamSynchronize(c.stream), "sum sync");
     sum_from_quadratic_form(c);
@@ -1122,6 +1123,10 @@ void sum_from_quadratic_form(Ctx& c) {
 // Apply the deferred last-group update to r (and recompute sum r^2 exactly).
 bool core_apply_pending(Ctx& c) {
   if (c.r_pending[0] < 0) return false;
+  if (c.r_pending_general) {
+    core_apply_pending_general(c);
+    return true;
+  }
   const CoreAllOps* ops = static_cast<const CoreAllOps*>(c.r_pending_ops);
   const DevCSF csf = c.csf_view(c.N - 1);
   if (csf.nchunks > 0) {

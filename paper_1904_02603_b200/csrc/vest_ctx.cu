@@ -1285,7 +1285,7 @@ static void graph_replay(Ctx& c) {
   note_sweep(c);
   check(cudaStreamSynchronize(c.stream), "graph sync");
   c.table_valid = false;
-  if (c.graph_general) {  // the general sweep ends with r current and its sum read back
+  if (c.graph_general && !c.graph_pending_general) {  // a general sweep that ended with r current
     c.r_valid = true;
     c.r_fresh = true;
     c.r_pending[0] = c.r_pending[1] = -1;
@@ -1293,11 +1293,14 @@ static void graph_replay(Ctx& c) {
     c.re = std::sqrt(c.sum_sq) / c.x_norm;
     return;
   }
+  // r lacks the sweep's last block (3-mode group or general block): the sums
+  // read back are [s', s] of the quadratic form
   c.r_valid = false;
   c.r_fresh = false;
   c.r_pending[0] = c.graph_pending[0];
   c.r_pending[1] = c.graph_pending[1];
   c.r_pending_ops = c.graph_pending_ops;
+  c.r_pending_general = c.graph_pending_general;
   sum_from_quadratic_form(c);
 }
 
@@ -1340,6 +1343,7 @@ int vest_cd_iteration(vest_ctx* h, int reg, double lambda, double* re) {
         c.graph_launches = launch_counter() - l0;
         launch_counter() = l0;  // counted when replayed
         c.graph_general = core_sweep_general(c);
+        c.graph_pending_general = c.r_pending_general && c.r_pending[0] >= 0;
         c.graph_pending[0] = c.r_pending[0];
         c.graph_pending[1] = c.r_pending[1];
         c.graph_pending_ops = c.r_pending_ops;

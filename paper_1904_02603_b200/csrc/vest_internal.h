@@ -171,6 +171,9 @@ struct Ctx {
   bool r_fresh = false;   // r matches the current model (sum_sq not computed)
   int r_pending[2] = {-1, -1};  // r still lacks the last core group's update (prefixes; d_dg holds the dg)
   const void* r_pending_ops = nullptr;
+  bool r_pending_general = false;  // the pending update is the general sweep's last block (r_pending[0] = its pass)
+  int pending_stride = 0;          // ... whose passes used this statistics stride
+  bool defer_last = false;         // the current general sweep defers its last residual pass
   double sum_sq = 0.0, re = 0.0;
 
   double* d_resp_core = nullptr;
@@ -214,6 +217,7 @@ struct Ctx {
   uint64_t graph_launches = 0;       // kernels per replay (launch accounting)
   int graph_pending[2] = {-1, -1};   // r_pending after the captured iteration
   bool graph_general = false;        // the captured sweep is the general one (sum of squares in h_small[0])
+  bool graph_pending_general = false;  // ... and deferred its last residual pass
   const void* graph_pending_ops = nullptr;
   int sparse_delta = -1;           // mask-specialised delta: -1 auto, 0 off, 1 on
   int sparse_fused = -1;           // ... fused with the statistics (modes without the fused residual): -1 auto
@@ -299,12 +303,15 @@ void compute_residual(Ctx& c);  // fresh r = x - B(alpha), sum_sq, re
 void core_sweep(Ctx& c, int reg, double lambda);
 bool core_sweep_capturable(const Ctx& c);  // the sweep has no host syncs inside (all-prefix or generated passes)
 bool core_sweep_general(const Ctx& c);     // the sweep is the general (not the 3-mode all-prefix) one
+bool defer_last_enabled();                 // vest_core.cu
+void core_apply_pending_general(Ctx& c);   // vest_core.cu: the general sweep's deferred last pass
 uint64_t core_mask_hash(const Ctx& c);
 void responsibilities(Ctx& c);
 void prune(Ctx& c, double pr, uint64_t* counts);
 void sparsity(Ctx& c, double* zero_frac, double* masked_frac);
 void normalize_columns(Ctx& c);
 double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n);
+void sum_chunks_device(Ctx& c, const double* d_in, uint64_t n, double* out);  // vest_ops.cu
 void comm_allreduce(Ctx& c, double* p, uint64_t n);
 void ctx_set_nccl(Ctx& c, int rank, int world, const void* id, const uint64_t* bounds);  // vest_nccl.cpp
 void nccl_unique_id(void* out);

@@ -28,6 +28,13 @@ __global__ void __launch_bounds__(1024) k_sum(const double* in, uint64_t n, doub
   }
 }
 
+// the sum into a device slot (global over the shards), no host read-back
+void sum_chunks_device(Ctx& c, const double* d_in, uint64_t n, double* out) {
+  k_sum<<<1, 1024, 0, c.stream>>>(d_in, n, out);
+  count_launch();
+  comm_allreduce(c, out, 1);
+}
+
 double reduce_chunk_sums(Ctx& c, const double* d_in, uint64_t n) {
   k_sum<<<1, 1024, 0, c.stream>>>(d_in, n, c.d_small);
   count_launch();
