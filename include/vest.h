@@ -82,10 +82,11 @@ int vest_ctx_sparse_delta_active(const vest_ctx* ctx);
  * shapes, from the second sweep with the same core mask on), 0 off
  * (table-driven kernel), 1 on. */
 int vest_ctx_set_core_gen(vest_ctx* ctx, int mode);
-/* Gather precision of the generated (NVRTC) kernels: on = their factor-row
- * gathers read fp32 copies of the factors (arithmetic stays fp64; the
- * factors themselves stay fp64).  For fp32 workloads (BASELINE config 4:
- * north_star's 1e-4 fp32 tolerance); default off (fp64 gathers). */
+/* fp32 mode of the generated (NVRTC) kernels: on = their factor-row gathers
+ * read fp32 copies of the factors, and the delta values and per-slice
+ * statistics they hand on are stored as fp32 (arithmetic stays fp64; the
+ * factors and the core stay fp64).  For fp32 workloads (BASELINE config 4:
+ * north_star's 1e-4 fp32 tolerance); default off. */
 int vest_ctx_set_gather_f32(vest_ctx* ctx, int on);
 /* With the mask-specialised delta: fuse the contraction with the row
  * statistics and solves in one kernel (modes other than the one carrying the

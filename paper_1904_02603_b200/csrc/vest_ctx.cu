@@ -459,7 +459,7 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
       ensure(c, &c.d_delta, &c.delta_cap, (size_t)J * (p1 - p0) + 1);
       ProfScope ps(c, fuse_d ? kProfFactorFused : kProfFactor);
       sparse_delta(c, mode, p0, p1 - p0, c.d_delta);
-      check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream),
+      check(launch_rowpass_delta(a, kStats, a.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream, c.gather_f32 != 0),
             "factor update (delta)");
       if (reg == 1) l1_empty_rows(c, mode, lambda);
     }
@@ -477,7 +477,8 @@ void update_factor_mode(Ctx& c, int mode, int reg, double lambda, bool fuse_resi
         ensure(c, &c.d_chunk_sum, &c.chunk_sum_cap, mdd.nchunks + 1);
         b.chunk_out = c.d_chunk_sum;
         ProfScope ps(c, kProfResid);
-        check(launch_rowpass_delta(b, kResid, b.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream), "heavy-row residual");
+        check(launch_rowpass_delta(b, kResid, b.csf.nchunks, c.d_delta, p1 - p0, p0, c.stream, c.gather_f32 != 0),
+              "heavy-row residual");
       }
       c.r_fresh = true;
     }

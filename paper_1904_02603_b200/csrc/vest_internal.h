@@ -279,8 +279,8 @@ constexpr double kQuadCancel = 1e-4;   // s'/s below this: recompute the sum fro
 cudaError_t launch_heavy_stats(const RowPassArgs& a, cudaStream_t s);  // k_heavy after a chunk-statistics pass
 bool sparse_fused_enabled(const Ctx& c);                               // vest_sparse.cu
 void sparse_fused(Ctx& c, int mode, const RowPassArgs& a);             // fused delta + statistics + solves
-cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
-                                 uint64_t dstride, uint64_t p0, cudaStream_t s);
+cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const void* delta,
+                                 uint64_t dstride, uint64_t p0, cudaStream_t s, bool f32);  // delta fp32 or fp64
 bool sparse_delta_enabled(const Ctx& c);
 bool sparse_delta_eligible(const Ctx& c);
 void note_sweep(Ctx& c);  // a factor sweep starts (mode 0): count sweeps per core mask

@@ -724,8 +724,8 @@ cudaError_t launch_tiny(const RowPassArgs& a, const uint32_t* rows, uint32_t nro
 // k_heavy) and, for the last mode, writes the fused residual
 // r = x - delta . a_row of the solved row (tucker_model.hpp:168-183: B(alpha)
 // = delta_n(alpha) . a_n[i_n]); kResid does the same for rows k_heavy solved.
-template <int JN, int KIND>
-__global__ void __launch_bounds__(kRowWarps * 32, 2) k_rowpass_delta(RowPassArgs a, const double* __restrict__ delta,
+template <int JN, int KIND, class DT>
+__global__ void __launch_bounds__(kRowWarps * 32, 2) k_rowpass_delta(RowPassArgs a, const DT* __restrict__ delta,
                                                                      uint64_t dstride, uint64_t p0) {
   static_assert(JN + 1 <= 16, "DMMA tile: J <= 15");
   __shared__ double smem_d[kRowWarps][16 * kXld];
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rowpass_delta(RowPassArgs
     for (uint32_t pos = ch.beg + lane; pos < ch.end; pos += 32) {
       double rec = 0.0;
 #pragma unroll
-      for (int j = 0; j < JN; ++j) rec = fma(__ldg(delta + j * dstride + (pos - p0)), arow[j], rec);
+      for (int j = 0; j < JN; ++j) rec = fma((double)__ldg(delta + j * dstride + (pos - p0)), arow[j], rec);
       const double r = __ldg(a.csf.val + pos) - rec;
       a.r_out[pos] = r;
       sq = fma(r, r, sq);
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rowpass_delta(RowPassArgs
       const uint32_t pos = base + lane;
       const bool valid = pos < ch.end;
 #pragma unroll
-      for (int j = 0; j < JN; ++j) wsm[j * kXld + lane] = valid ? __ldg(delta + j * dstride + (pos - p0)) : 0.0;
+      for (int j = 0; j < JN; ++j) wsm[j * kXld + lane] = valid ? (double)__ldg(delta + j * dstride + (pos - p0)) : 0.0;
       wsm[JN * kXld + lane] = valid ? __ldg(a.csf.val + pos) : 0.0;
       __syncwarp();
       gram_dmma<JN + 1, 1>(wsm, tc, lane);
@@ -802,19 +802,19 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rowpass_delta(RowPassArgs
     for (uint32_t pos = ch.beg + lane; pos < ch.end; pos += 32) {
       double rec = 0.0;
 #pragma unroll
-      for (int j = 0; j < JN; ++j) rec = fma(__ldg(delta + j * dstride + (pos - p0)), arow[j], rec);
+      for (int j = 0; j < JN; ++j) rec = fma((double)__ldg(delta + j * dstride + (pos - p0)), arow[j], rec);
       a.r_out[pos] = __ldg(a.csf.val + pos) - rec;
     }
   }
 }
 
-template <int JN>
-cudaError_t launch_delta_j(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta, uint64_t dstride,
-                           uint64_t p0, cudaStream_t s) {
+template <int JN, class DT>
+cudaError_t launch_delta_jt(const RowPassArgs& a, int kind, uint32_t nchunks, const DT* delta, uint64_t dstride,
+                            uint64_t p0, cudaStream_t s) {
   const dim3 grid((nchunks + kRowWarps - 1) / kRowWarps);
   if (nchunks > 0) {
-    if (kind == kStats) k_rowpass_delta<JN, kStats><<<grid, kRowWarps * 32, 0, s>>>(a, delta, dstride, p0);
-    else k_rowpass_delta<JN, kResid><<<grid, kRowWarps * 32, 0, s>>>(a, delta, dstride, p0);
+    if (kind == kStats) k_rowpass_delta<JN, kStats, DT><<<grid, kRowWarps * 32, 0, s>>>(a, delta, dstride, p0);
+    else k_rowpass_delta<JN, kResid, DT><<<grid, kRowWarps * 32, 0, s>>>(a, delta, dstride, p0);
     count_launch();
   }
   if (kind == kStats && a.csf.nheavy > 0) {
@@ -824,6 +824,13 @@ cudaError_t launch_delta_j(const RowPassArgs& a, int kind, uint32_t nchunks, con
   return cudaGetLastError();
 }
 
+template <int JN>
+cudaError_t launch_delta_j(const RowPassArgs& a, int kind, uint32_t nchunks, const void* delta, uint64_t dstride,
+                           uint64_t p0, cudaStream_t s, bool f32) {
+  return f32 ? launch_delta_jt<JN>(a, kind, nchunks, static_cast<const float*>(delta), dstride, p0, s)
+             : launch_delta_jt<JN>(a, kind, nchunks, static_cast<const double*>(delta), dstride, p0, s);
+}
+
 cudaError_t launch_heavy_stats(const RowPassArgs& a, cudaStream_t s) {
   if (a.csf.nheavy == 0) return cudaSuccess;
   k_heavy<<<(a.csf.nheavy + 7) / 8, 256, 0, s>>>(a, kStats);
@@ -831,12 +838,12 @@ cudaError_t launch_heavy_stats(const RowPassArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const double* delta,
-                                 uint64_t dstride, uint64_t p0, cudaStream_t s) {
+cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunks, const void* delta,
+                                 uint64_t dstride, uint64_t p0, cudaStream_t s, bool f32) {
   switch (a.m.J[a.mode]) {
 #define VEST_DJ(JJ) \
   case JJ:          \
-    return launch_delta_j<JJ>(a, kind, nchunks, delta, dstride, p0, s);
+    return launch_delta_j<JJ>(a, kind, nchunks, delta, dstride, p0, s, f32);
     VEST_DJ(1) VEST_DJ(2) VEST_DJ(3) VEST_DJ(4) VEST_DJ(5) VEST_DJ(6) VEST_DJ(7) VEST_DJ(8)
     VEST_DJ(9) VEST_DJ(10) VEST_DJ(11) VEST_DJ(12) VEST_DJ(13) VEST_DJ(14) VEST_DJ(15)
 #undef VEST_DJ

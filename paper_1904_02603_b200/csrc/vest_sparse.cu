@@ -257,9 +257,12 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
   emit_row_loads(o, c, oth, 0, "a.p0 + t0", lazy);
   emit_row_loads(o, c, oth, 1, "a.p0 + t1", lazy);
   emit_cells(o, c, n, oth, cells, 2, lazy);
-  for (int j = 0; j < c.ranks[n]; ++j) o << "    a.out[" << j << "ull * a.stride + t0] = d" << j << "e0;\n";
+  // delta SoA for k_rowpass_delta: fp64, or fp32 in the fp32 mode (gather_f32)
+  const std::string dst = c.gather_f32 ? "reinterpret_cast<float*>(a.out)" : "a.out";
+  const std::string cv = c.gather_f32 ? "(float)" : "";
+  for (int j = 0; j < c.ranks[n]; ++j) o << "    " << dst << "[" << j << "ull * a.stride + t0] = " << cv << "d" << j << "e0;\n";
   o << "    if (t1 != t0) {\n";
-  for (int j = 0; j < c.ranks[n]; ++j) o << "      a.out[" << j << "ull * a.stride + t1] = d" << j << "e1;\n";
+  for (int j = 0; j < c.ranks[n]; ++j) o << "      " << dst << "[" << j << "ull * a.stride + t1] = " << cv << "d" << j << "e1;\n";
   o << "    }\n  }\n}\n";
 }
 
