@@ -126,7 +126,7 @@ std::vector<Cell> ordered_cells(const Ctx& c, int n, std::vector<int>& oth) {
 // Loads of entry E's other-mode factor rows into registers u<k>_<b>e<E>;
 // pos is the expression of the entry's CSF position.
 void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>& oth, int e, const std::string& pos,
-                    int lazy = 0) {
+                    int lazy = 0, bool f32 = false) {
   const std::string E = std::to_string(e);
   for (int k : oth) {
     const int ld = c.ld[k];
@@ -137,7 +137,7 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
         << "[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos << ") * " << ld << "ull;\n";
       continue;
     }
-    if (c.gather_f32) {  // fp32 copy of the row, widened to fp64 in registers
+    if (c.gather_f32) {  // fp32 copy of the row, widened to fp64 in registers (kept fp32 in the fp32 contraction)
       const bool v4 = ld % 4 == 0;
       o << "    const float* " << rk << " = a.g[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos
         << ") * " << ld << "ull;\n";
@@ -147,7 +147,8 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
           << (v4 ? "float4" : "float2") << "*>(" << rk << " + " << b << "));\n";
         const char* comp[4] = {"x", "y", "z", "w"};
         for (int q = 0; q < (v4 ? 4 : 2) && b + q < c.ranks[k]; ++q)
-          o << "    const double " << u(k, b + q) << "e" << E << " = (double)" << v << "." << comp[q] << ";\n";
+          o << "    const " << (f32 ? "float " : "double ") << u(k, b + q) << "e" << E << " = " << (f32 ? "" : "(double)")
+            << v << "." << comp[q] << ";\n";
       }
       continue;
     }
@@ -171,10 +172,11 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
 // group t = sum G u_last, then d[beta_n] += w t.  Every core value G[lin] is a
 // constant-bank operand shared by the ne entries.
 void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<int>& oth, const std::vector<Cell>& cells,
-                int ne, int lazy = 0) {
+                int ne, int lazy = 0, bool f32 = false) {
   const int L = (int)oth.size();
+  const std::string T = f32 ? "float" : "double", Gs = f32 ? "Gf[" : "G[", fma_ = f32 ? "fmaf(" : "fma(";
   for (int e = 0; e < ne; ++e)
-    for (int j = 0; j < c.ranks[n]; ++j) o << "    double d" << j << "e" << e << " = 0.0;\n";
+    for (int j = 0; j < c.ranks[n]; ++j) o << "    " << T << " d" << j << "e" << e << " = " << (f32 ? "0.0f" : "0.0") << ";\n";
   auto same_prefix = [&](const Cell& a, const Cell& b, int upto) {
     for (int q = 0; q <= upto; ++q)
       if (a.beta[oth[q]] != b.beta[oth[q]]) return false;
@@ -187,10 +189,10 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
       o << "    {";
       for (int e = 0; e < ne; ++e) {
         const std::string E = std::to_string(e);
-        const std::string val = q < lazy ? "(double)__ldg(r" + std::to_string(k) + "e" + E + " + " + std::to_string(b) + ")"
+        const std::string val = q < lazy ? "(" + T + ")__ldg(r" + std::to_string(k) + "e" + E + " + " + std::to_string(b) + ")"
                                          : u(k, b) + "e" + E;
-        if (q == 0) o << " const double w0e" << E << " = " << val << ";";
-        else o << " const double w" << q << "e" << E << " = w" << (q - 1) << "e" << E << " * " << val << ";";
+        if (q == 0) o << " const " << T << " w0e" << E << " = " << val << ";";
+        else o << " const " << T << " w" << q << "e" << E << " = w" << (q - 1) << "e" << E << " * " << val << ";";
       }
       o << "\n";
     }
@@ -200,15 +202,15 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
     for (size_t g = i; g < e_end;) {
       const int bn = cells[g].beta[n];
       size_t h = g;
-      o << "      { double g = G[" << cells[h].lin << "];";
-      for (int e = 0; e < ne; ++e) o << " double t" << e << " = g * " << u(kl, cells[h].beta[kl]) << "e" << e << ";";
+      o << "      { " << T << " g = " << Gs << cells[h].lin << "];";
+      for (int e = 0; e < ne; ++e) o << " " << T << " t" << e << " = g * " << u(kl, cells[h].beta[kl]) << "e" << e << ";";
       for (++h; h < e_end && cells[h].beta[n] == bn; ++h) {
-        o << " g = G[" << cells[h].lin << "];";
+        o << " g = " << Gs << cells[h].lin << "];";
         for (int e = 0; e < ne; ++e)
-          o << " t" << e << " = fma(g, " << u(kl, cells[h].beta[kl]) << "e" << e << ", t" << e << ");";
+          o << " t" << e << " = " << fma_ << "g, " << u(kl, cells[h].beta[kl]) << "e" << e << ", t" << e << ");";
       }
       for (int e = 0; e < ne; ++e) {
-        if (L >= 2) o << " d" << bn << "e" << e << " = fma(w" << (L - 2) << "e" << e << ", t" << e << ", d" << bn << "e" << e << ");";
+        if (L >= 2) o << " d" << bn << "e" << e << " = " << fma_ << "w" << (L - 2) << "e" << e << ", t" << e << ", d" << bn << "e" << e << ");";
         else o << " d" << bn << "e" << e << " += t" << e << ";";
       }
       o << " }\n";
@@ -243,27 +245,58 @@ int sd_min_blocks() {
   return v;
 }
 
+// The contraction in fp32 arithmetic (fp32 mode only, VEST_SD_F32=0 for the
+// fp64 one): the fp32 copies of the factor rows, the core rounded to fp32
+// (constant bank Gf) and FFMA -- twice the FP64 rate and half the registers
+// per value.  delta is written as fp32 in the fp32 mode either way; the
+// statistics, solves and residuals after it stay fp64 (k_rowpass_delta).
+bool sd_f32(const Ctx& c) {
+  static const int env = [] {
+    const char* e = getenv("VEST_SD_F32");
+    return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+  }();
+  return c.gather_f32 && env != 0;
+}
+
+// entries per thread of the delta kernel (VEST_SD_NE: A/B; 2 in fp64, 3 in fp32 --
+// config 4 fp32 mode, ms per iteration at 2 / 3 / 4: 190.2 / 186.8 / 193.4)
+int sd_entries(const Ctx& c) {
+  static const int env = [] {
+    const char* e = getenv("VEST_SD_NE");
+    return e ? std::max(1, std::min(8, atoi(e))) : 0;
+  }();
+  return env > 0 ? env : (sd_f32(c) ? 3 : 2);
+}
+
 void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
   std::vector<int> oth;
   const std::vector<Cell> cells = ordered_cells(c, n, oth);
-  // two entries per thread (E = 0, 1: t and t + 256 of the block's stride
-  // window): every core value is loaded once (uniform constant load) and
-  // feeds both entries' FMAs
+  const bool f32 = sd_f32(c);
+  const int ne = sd_entries(c);
+  const std::string NB = std::to_string(256 * ne);
+  // ne entries per thread (e: t0 + 256 e of the block's stride window): every
+  // core value is loaded once (uniform constant load) and feeds all ne
+  // entries' FMAs
   o << "extern \"C\" __global__ void __launch_bounds__(256, " << sd_min_blocks() << ") vest_sd_" << n
     << "(const SparseDeltaArgs a) {\n"
-    << "  for (unsigned long long t0 = blockIdx.x * 512ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * 512ull) {\n"
-    << "    const unsigned long long t1 = t0 + 256ull < a.n ? t0 + 256ull : t0;\n";
+    << "  for (unsigned long long t0 = blockIdx.x * " << NB << "ull + threadIdx.x; t0 < a.n; t0 += gridDim.x * " << NB
+    << "ull) {\n";
+  for (int e = 1; e < ne; ++e)
+    o << "    const unsigned long long t" << e << " = t0 + " << 256 * e << "ull < a.n ? t0 + " << 256 * e << "ull : t0;\n";
   const int lazy = oth.size() >= 2 ? std::min<int>(sd_lazy(c), (int)oth.size() - 1) : 0;
-  emit_row_loads(o, c, oth, 0, "a.p0 + t0", lazy);
-  emit_row_loads(o, c, oth, 1, "a.p0 + t1", lazy);
-  emit_cells(o, c, n, oth, cells, 2, lazy);
+  for (int e = 0; e < ne; ++e) emit_row_loads(o, c, oth, e, "a.p0 + t" + std::to_string(e), lazy, f32);
+  emit_cells(o, c, n, oth, cells, ne, lazy, f32);
   // delta SoA for k_rowpass_delta: fp64, or fp32 in the fp32 mode (gather_f32)
   const std::string dst = c.gather_f32 ? "reinterpret_cast<float*>(a.out)" : "a.out";
-  const std::string cv = c.gather_f32 ? "(float)" : "";
-  for (int j = 0; j < c.ranks[n]; ++j) o << "    " << dst << "[" << j << "ull * a.stride + t0] = " << cv << "d" << j << "e0;\n";
-  o << "    if (t1 != t0) {\n";
-  for (int j = 0; j < c.ranks[n]; ++j) o << "      " << dst << "[" << j << "ull * a.stride + t1] = " << cv << "d" << j << "e1;\n";
-  o << "    }\n  }\n}\n";
+  const std::string cv = c.gather_f32 && !f32 ? "(float)" : "";
+  for (int e = 0; e < ne; ++e) {
+    const std::string E = std::to_string(e);
+    if (e > 0) o << "    if (t" << E << " != t0) {\n";
+    for (int j = 0; j < c.ranks[n]; ++j)
+      o << "      " << dst << "[" << j << "ull * a.stride + t" << E << "] = " << cv << "d" << j << "e" << E << ";\n";
+    if (e > 0) o << "    }\n";
+  }
+  o << "  }\n}\n";
 }
 
 // The fused factor-mode update (modes without the fused residual): one warp
@@ -414,6 +447,12 @@ std::string gen_source(const Ctx& c) {
   o << "struct SparseDeltaArgs { const unsigned* oc[" << VEST_MAXN << "]; const double* f[" << VEST_MAXN
     << "]; const float* g[" << VEST_MAXN << "]; double* out; unsigned long long p0, n, stride; };\n"
     << "extern \"C\" __constant__ double G[" << c.G << "];\n";
+  if (sd_f32(c))  // the core rounded to fp32 for the fp32 contraction (staged in Gf_src, copied to the bank)
+    o << "extern \"C\" __constant__ float Gf[" << c.G << "];\n"
+      << "extern \"C\" __device__ float Gf_src[" << c.G << "];\n"
+      << "extern \"C\" __global__ void vest_core_f32(const double* s) {\n"
+      << "  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < " << c.G << "; i += gridDim.x * blockDim.x) Gf_src[i] = (float)s[i];\n"
+      << "}\n";
   for (int n = 0; n < c.N; ++n) emit_mode(o, c, n);
   if (fused_ok(c)) {
     o << kFusedPrelude;
@@ -432,6 +471,7 @@ uint64_t mask_key(const Ctx& c) {
   for (int k = 0; k < c.N; ++k) mix((uint64_t)c.ranks[k] << 8 | (uint64_t)c.ld[k]);
   for (uint8_t m : c.h_core_mask) mix(m);
   mix(0xF32u + (uint64_t)c.gather_f32);
+  mix(0x5DF32u + (uint64_t)sd_f32(c) * 16 + (uint64_t)sd_entries(c));
   return h;
 }
 
@@ -443,6 +483,9 @@ struct SparseState {
   cudaKernel_t k[VEST_MAXN] = {};
   cudaKernel_t kf[VEST_MAXN] = {};  // fused factor-mode updates (vest_sf_<n>)
   double* G = nullptr;
+  float* Gf = nullptr;  // fp32 contraction: the bank copy and its staging buffer
+  float* Gf_src = nullptr;
+  cudaKernel_t core_f32 = nullptr;
   double compile_s = 0.0;
 };
 
@@ -552,6 +595,11 @@ static void ensure_module(Ctx& c) {
   }
   size_t gb = 0;
   check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->G), &gb, s->lib, "G"), "sparse delta core symbol");
+  if (sd_f32(c)) {
+    check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->Gf), &gb, s->lib, "Gf"), "sparse delta core symbol");
+    check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->Gf_src), &gb, s->lib, "Gf_src"), "sparse delta core symbol");
+    check(cudaLibraryGetKernel(&s->core_f32, s->lib, "vest_core_f32"), "sparse delta core kernel");
+  }
   c.sparse = s;
 }
 
@@ -559,8 +607,19 @@ static void ensure_module(Ctx& c) {
 void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
   ensure_module(c);
   if (n == 0) return;
-  check(cudaMemcpyAsync(c.sparse->G, c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
-        "sparse delta core");
+  if (c.sparse->Gf) {  // fp32 contraction: the core rounded to fp32 into its constant bank
+    const double* src = c.d_core;
+    void* cargs[] = {&src};
+    check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->core_f32), dim3((c.G + 255) / 256), dim3(256), cargs,
+                           0, c.stream),
+          "sparse delta core (fp32)");
+    count_launch();
+    check(cudaMemcpyAsync(c.sparse->Gf, c.sparse->Gf_src, sizeof(float) * c.G, cudaMemcpyDeviceToDevice, c.stream),
+          "sparse delta core (fp32)");
+  } else {
+    check(cudaMemcpyAsync(c.sparse->G, c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
+          "sparse delta core");
+  }
   SparseDeltaArgs a{};
   const DevCSF csf = c.csf_view(mode);
   if (c.gather_f32) refresh_factor_shadows(c, mode);
@@ -575,7 +634,8 @@ void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
   a.stride = n;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  const unsigned grid = (unsigned)std::min<uint64_t>((n + 511) / 512, (uint64_t)sms * 2 * sd_min_blocks());
+  const uint64_t per_cta = 256ull * sd_entries(c);
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + per_cta - 1) / per_cta, (uint64_t)sms * 2 * sd_min_blocks());
   void* args[] = {&a};
   check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->k[mode]), dim3(grid), dim3(256), args, 0, c.stream),
         "sparse delta launch");

@@ -49,8 +49,10 @@ def test_fused_factor_update_bit_identical(dims, ranks, mf, skew, reg, lam):
 
 @pytest.mark.parametrize("dims,ranks,mf", [([30, 28, 26, 24], [8, 8, 8, 8], 0.9), ([20, 18, 16, 14, 12], [5] * 5, 0.0)])
 def test_gather_f32_within_fp32_tolerance(dims, ranks, mf):
-    """fp64 arithmetic on fp32-rounded factor operands (both generated kernel
-    families): model and RE within 1e-4 of the fp64 oracle after 3 iterations;
+    """The fp32 mode (both generated kernel families): fp32-rounded factor
+    operands, the mask-specialised delta contracted in fp32 arithmetic
+    (VEST_SD_F32), fp64 statistics and solves -- model and RE within 1e-4 of
+    the fp64 oracle after 3 iterations;
     the fp32 shadows follow every factor update (no stale copies)."""
     nnz = 8000
     coords, values, m = random_instance(dims, ranks, nnz, 67, mask_frac=mf)
