@@ -29,7 +29,7 @@ import pytest
 from oracle import oracle as O
 from paper_1904_02603_b200 import _lib
 from paper_1904_02603_b200 import sparsetuck as st
-from parity import assert_close, assert_masks, assert_resp
+from parity import assert_close, assert_close_fp32, assert_masks, assert_resp
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -342,8 +342,10 @@ def test_fullsize_steady_state_kernels(cfg):
     assert abs(res.re - t["re"]) <= 1e-6 * t["re"], (res.re, t["re"])
     if cfg == 4:
         # the fp32 mode bench.py times for config 4 (fp32 factor gathers, fp32
-        # chunk statistics; fp64 arithmetic): the same sweep and a factor mode
-        # within north_star's stated fp32 tolerance of the fp64 results
+        # chunk statistics, the mask-specialised delta contracted in fp32
+        # arithmetic; statistics, solves and residuals fp64): the same sweep
+        # within 1e-4 floored of the fp64 result, and a whole factor mode under
+        # the fp32 criterion of SURVEY 8(c) (normwise 1e-4; tests/parity.py)
         dev.set_gather_f32(True)
         dev.set_model(before)
         dev.update_core(0, lam)
@@ -355,7 +357,8 @@ def test_fullsize_steady_state_kernels(cfg):
         dev.set_gather_f32(False)
         dev.set_model(before)
         dev.update_factor_mode(1, 0, lam)
-        assert_close(f1_fp32, dev.get_model().factors[1], "config 4 factor mode 1, fp32 mode", tol=1e-4)
+        fr, nw = assert_close_fp32(f1_fp32, dev.get_model().factors[1], "config 4 factor mode 1, fp32 mode")
+        print(f"config 4 fp32 mode, factor mode 1 vs fp64: floored {fr:.3e} normwise {nw:.3e}")
     dev.close()
 
 
