@@ -809,6 +809,51 @@ inline double evaluate_test(const TuckerModel& m, const SparseTensor& test) {
   return re;
 }
 
+// Prune-rate sweep (BASELINE config 5's protocol: rates 0.1..0.9 on a train /
+// test split; the manual counterpart of the auto mode's elbow search,
+// pruning.hpp:45-81).  For each rate, from the SAME trained model: score
+// responsibilities on the training entries (pruning.hpp:181-191),
+// prune_step(rate) (pruning.hpp:234-247), then the relative error on the
+// training entries (tucker_model.hpp:186-188) and on the held-out entries
+// (trainer.hpp:188-190).  Every rate starts from the same model, so the
+// responsibility table is scored once and reused by each rate's prune_step; the evaluations are the inner loop.  The caller's model is not
+// modified.
+struct RateResult {
+  double rate = 0.0;
+  PruneCounts pruned;
+  double sparsity = 0.0;
+  double train_re = 0.0;
+  double test_re = 0.0;
+};
+
+inline std::vector<RateResult> prune_rate_sweep(const TuckerModel& m, const SparseTensor& train,
+                                                const SparseTensor& test, std::span<const double> rates) {
+  if (m.dims != train.dims || m.dims != test.dims) throw std::invalid_argument("model/tensor shape mismatch");
+  for (double pr : rates)
+    if (!(pr >= 0.0 && pr < 1.0)) throw std::invalid_argument("prune rate must be in [0, 1)");
+  const ResponsibilityTable t = compute_responsibilities(m, train, ModeIndex{}, Residuals{});
+  const auto hold = b200_detail::bind(m, train);  // the same cached context
+  vest_ctx* h = hold->h;
+  std::vector<const double*> f(m.order());
+  for (std::size_t n = 0; n < m.order(); ++n) f[n] = t.factors[n].data();
+  std::vector<RateResult> out;
+  for (double pr : rates) {
+    b200_detail::push(h, m);
+    std::vector<std::uint64_t> c(1 + m.order());
+    b200_detail::check(vest_prune_step(h, pr, t.core.data(), f.data(), c.data()));
+    RateResult r;
+    r.rate = pr;
+    r.pruned.core = c[0];
+    for (std::size_t n = 0; n < m.order(); ++n) r.pruned.factors.push_back(c[1 + n]);
+    double masked = 0.0;
+    b200_detail::check(vest_sparsity(h, &r.sparsity, &masked));
+    b200_detail::check(vest_compute_residuals(h, nullptr, nullptr, nullptr, &r.train_re));
+    b200_detail::check(vest_evaluate(h, test.coords.data(), test.values.data(), test.nnz(), &r.test_re));
+    out.push_back(std::move(r));
+  }
+  return out;
+}
+
 // ------------------------------------------------------------ data formats --
 // load_coo / save_coo (sparse_tensor.hpp:139-228), save_model / load_model
 // (model_io.hpp:22-104): vest_io.cpp, parallel, byte-compatible files and the

@@ -543,10 +543,12 @@ __global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, i
 // ~43 live cells of 31 fibers x 8) the GEMM over [S | R] x [a a^T | a] forms
 // every (fiber pair, c pair) -- ~20x the entries the solve reads.  Each thread
 // owns up to kHsPer entries of H (upper triangle over the live cells) or C,
-// tab[e] = s-index | c << 16 | c' << 24 (c' = 255: a C entry, R x a_c), and
-// accumulates s * a_c * a_c' over its CTA's chunks in order (batches of chunk
-// statistics rows staged in shared memory); CTA partials are summed in a
-// fixed order afterwards (deterministic).
+// tab[e] = s-index | a-index << 16, the a-index naming one of the chunk's
+// weights aa = [a_c a_c' (c <= c', row-major triangle) | a_c] (the C entries,
+// R x a_c) that the CTA forms once per staged chunk, and accumulates s * aa
+// over its CTA's chunks in order (batches of chunk statistics rows staged in
+// shared memory); CTA partials are summed in a fixed order afterwards
+// (deterministic).
 constexpr int kHsBatch = 8, kHsPer = 8, kHsThreads = 256;
 __device__ __forceinline__ void hs_cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
@@ -583,6 +585,8 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict
   }
   T* const sstat = reinterpret_cast<T*>(hs_raw);                     // [2][kHsBatch][wpad]
   double* const sarow = reinterpret_cast<double*>(sstat + 2 * bufw);  // [2][kHsBatch][Jm]
+  const int AW = Jm * (Jm + 1) / 2 + Jm;
+  double* const saa = sarow + 2 * kHsBatch * Jm;                       // [kHsBatch][AW]
   auto stage = [&](uint32_t cb, int buf) {
     const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
     T* ss = sstat + buf * bufw;
@@ -598,6 +602,18 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  // weight slot p of a chunk -> (c, c') (c' < 0: the single a_c of a C entry)
+  __shared__ int hs_pc[VEST_MAXJ * (VEST_MAXJ + 1) / 2 + VEST_MAXJ];
+  for (int p = threadIdx.x; p < AW; p += kHsThreads) {
+    int c = 0, q = p, c2 = -1;
+    if (p >= AW - Jm) {
+      c = p - (AW - Jm);
+    } else {
+      while (q >= Jm - c) q -= Jm - c, ++c;
+      c2 = c + q;
+    }
+    hs_pc[p] = c | c2 << 8;
+  }
   if (c0 < c1) stage(c0, 0);
   int buf = 0;
   for (uint32_t cb = c0; cb < c1; cb += kHsBatch) {
@@ -611,17 +627,20 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict
     __syncthreads();
     const T* ss = sstat + buf * bufw;
     const double* sa = sarow + buf * kHsBatch * Jm;
+    for (int t = threadIdx.x; t < nb * AW; t += kHsThreads) {
+      const int b = t / AW, pc = hs_pc[t - b * AW];
+      const double a0 = sa[b * Jm + (pc & 255)];
+      saa[t] = pc >= 0 ? a0 * sa[b * Jm + (pc >> 8)] : a0;
+    }
+    __syncthreads();
     for (int b = 0; b < nb; ++b) {
 #pragma unroll
       for (int j = 0; j < kHsPer; ++j) {
         if (my[j] == 0xffffffffu) continue;
-        const uint32_t cj = my[j] >> 24;
-        double v = (double)ss[b * wpad + (my[j] & 0xffffu)] * sa[b * Jm + ((my[j] >> 16) & 255u)];
-        if (cj != 255u) v *= sa[b * Jm + cj];
-        acc[j] += v;
+        acc[j] = fma((double)ss[b * wpad + (my[j] & 0xffffu)], saa[b * AW + (my[j] >> 16)], acc[j]);
       }
     }
-    __syncthreads();  // the buffer is re-staged two batches from now
+    __syncthreads();  // the buffers are re-staged / rewritten from the next batch on
     buf ^= 1;
   }
 #pragma unroll
@@ -1214,9 +1233,10 @@ static std::vector<uint32_t> hsample_table(const Ctx& c, const Blocks& b, int bi
     const int fi = lq[i] / Jm, ci = lq[i] % Jm;
     for (int j = i; j < nl; ++j) {
       const int fj = lq[j] / Jm, cj = lq[j] % Jm;  // fi <= fj (row-major live order)
-      tab[tri_h(i, j, nl)] = (uint32_t)tri_h(fi, fj, nf) | (uint32_t)ci << 16 | (uint32_t)cj << 24;
+      tab[tri_h(i, j, nl)] =
+          (uint32_t)tri_h(fi, fj, nf) | (uint32_t)tri_h(std::min(ci, cj), std::max(ci, cj), Jm) << 16;
     }
-    tab[nl * (nl + 1) / 2 + i] = (uint32_t)(NS + fi) | (uint32_t)ci << 16 | 255u << 24;
+    tab[nl * (nl + 1) / 2 + i] = (uint32_t)(NS + fi) | (uint32_t)(Jm * (Jm + 1) / 2 + ci) << 16;
   }
   return tab;
 }
@@ -1260,14 +1280,16 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
   const int width = NS + nf;
   ProfScope ps(c, kProfCoreGemm);
   if (c.stats_f32) {
-    const size_t sm = (size_t)2 * kHsBatch * (((width + 3) & ~3) * sizeof(float) + Jm * sizeof(double));
+    const size_t sm = (size_t)2 * kHsBatch * (((width + 3) & ~3) * sizeof(float) + Jm * sizeof(double)) +
+                      (size_t)kHsBatch * (Jm * (Jm + 1) / 2 + Jm) * sizeof(double);
     check(cudaFuncSetAttribute(k_core_hsample<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
           "hsample smem");
     k_core_hsample<float><<<nparts, kHsThreads, sm, c.stream>>>(reinterpret_cast<const float*>(c.d_chunk_stats), stride,
                                                                  width, md.d_chunks, md.nchunks, c.d_factor[m], c.ld[m],
                                                                  Jm, tab, E, c.d_gemm_part);
   } else {
-    const size_t sm = (size_t)2 * kHsBatch * (((width + 1) & ~1) + Jm) * sizeof(double);
+    const size_t sm = (size_t)2 * kHsBatch * (((width + 1) & ~1) + Jm) * sizeof(double) +
+                      (size_t)kHsBatch * (Jm * (Jm + 1) / 2 + Jm) * sizeof(double);
     check(cudaFuncSetAttribute(k_core_hsample<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
           "hsample smem");
     k_core_hsample<double><<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks,

@@ -95,7 +95,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
   constexpr int NF = @NF@, PNF = @PNF@, KIND = @KIND@, JM = @JM@, RSLOT = @RSLOT@;
   constexpr bool WSQ = @WSQ@;  // statistics pass that also sums r^2 (after the previous block's update)
   extern __shared__ __align__(16) double smem[];
-  __shared__ double sq_q[4][32];
+  __shared__ @PT@ sq_q[4][32];  // previous block's per-fiber a . dg of the chunk's row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* const stage = smem + (unsigned long long)warp * (32 * LDR + NC * 36);  // one round's rows
   double* const X = stage + 32 * LDR;
@@ -137,7 +137,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
 #pragma unroll
         for (int q = 0; q < JM; ++q) t = fma(__ldg(arow + q), __ldg(a.prev_dg + lane * JM + q), t);
       }
-      sq_q[warp][lane] = t;
+      sq_q[warp][lane] = (@PT@)t;
       __syncwarp();
     }
   };
@@ -168,9 +168,9 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
     const Cur nn = next(nxt);
     coords(nn, inx);
     if (PNF > 0 && valid) {
-      double t = 0.0;
+      @PT@ t = 0;
 @PREV@
-      r -= t;
+      r -= (double)t;
       a.r[pos] = r;
     }
     if (KIND == 2 || WSQ) sq = fma(r, r, sq);
@@ -230,6 +230,18 @@ int cp_min_blocks() {
   return v;
 }
 
+// fp32 mode: the fiber products (previous block's residual update, current
+// block's Gram columns) in fp32 arithmetic on the fp32 row copies -- they leave
+// the FP64 pipe to the DMMA Gram and halve the registers holding the rows; the
+// Gram, the statistics and r stay fp64 (VEST_CP_F32=0: fp64 products, A/B).
+bool cp_f32(const Ctx& c) {
+  static const bool env = [] {
+    const char* e = getenv("VEST_CP_F32");
+    return !(e && e[0] == '0');
+  }();
+  return c.gather_f32 && env;
+}
+
 void replace_all(std::string& s, const std::string& from, const std::string& to) {
   for (size_t p = 0; (p = s.find(from, p)) != std::string::npos; p += to.size()) s.replace(p, from.size(), to);
 }
@@ -247,7 +259,8 @@ void fiber_beta(const Ctx& c, uint32_t p, int* beta) {
 
 // straight-line products of a block's fibers; emit(f, expr) consumes each
 void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream& o,
-              const std::function<std::string(int, const std::string&)>& emit, std::vector<bool>& used) {
+              const std::function<std::string(int, const std::string&)>& emit, std::vector<bool>& used,
+              const char* T = "double") {
   const int M = c.N - 1;
   int prev[VEST_MAXN];
   bool open = false;
@@ -258,9 +271,9 @@ void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream
     for (int k = 0; k + 1 < M && same; ++k) same = beta[k] == prev[k];
     if (!same) {
       if (open) o << "      }\n";
-      o << "      { const double w = ";
+      o << "      { const " << T << " w = ";
       if (M == 1) {
-        o << "1.0";
+        o << "1";
       } else {
         for (int k = 0; k + 1 < M; ++k) {
           o << (k ? " * " : "") << uname(k, beta[k]);
@@ -312,12 +325,14 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     nts.push_back(NT);
     std::vector<bool> used(VEST_MAXN * 16, false);
     std::ostringstream pv, cv;
-    products(c, prev, pv, [](int f, const std::string& e) {
-      return "t = fma(" + e + ", sq_q[warp][" + std::to_string(f) + "], t);";
-    }, used);
-    products(c, cur, cv, [](int f, const std::string& e) {
-      return "X[" + std::to_string(f * 36) + " + lane] = " + e + ";";
-    }, used);
+    const bool pf32 = cp_f32(c);
+    const char* PT = pf32 ? "float" : "double";
+    products(c, prev, pv, [pf32](int f, const std::string& e) {
+      return std::string(pf32 ? "t = fmaf(" : "t = fma(") + e + ", sq_q[warp][" + std::to_string(f) + "], t);";
+    }, used, PT);
+    products(c, cur, cv, [pf32](int f, const std::string& e) {
+      return "X[" + std::to_string(f * 36) + " + lane] = " + (pf32 ? "(double)(" + e + ")" : e) + ";";
+    }, used, PT);
     std::ostringstream iss, lu;
     for (int k = 0; k < M; ++k) {
       if (f32) {  // fp32 row copies: ld floats, 16-byte pieces when ld % 4 == 0, else 8-byte
@@ -329,8 +344,8 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
         iss << "      }\n";
         for (int b = 0; b < c.ranks[k]; ++b)
           if (used[k * 16 + b])
-            lu << "    const double " << uname(k, b) << " = (double)reinterpret_cast<const float*>(st + " << soff[k]
-               << ")[" << b << "];\n";
+            lu << "    const " << PT << " " << uname(k, b) << " = " << (pf32 ? "" : "(double)")
+               << "reinterpret_cast<const float*>(st + " << soff[k] << ")[" << b << "];\n";
         continue;
       }
       iss << "      { const double* row = a.f[" << k << "] + (unsigned long long)idx[" << k << "] * " << c.ld[k] << ";\n";
@@ -354,6 +369,7 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@RSLOT@", std::to_string(rslot));
     replace_all(p, "@MINB@", std::to_string(cp_min_blocks()));
     replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
+    replace_all(p, "@PT@", PT);
     replace_all(p, "@ISSUE@", iss.str());
     replace_all(p, "@LOADU@", lu.str());
     replace_all(p, "@PREV@", pv.str());

@@ -144,6 +144,70 @@ int main() {
     }
     CHECK(std::abs(reconstruction_error(m, x) - r.report.iterations[5].re) <= 1e-9 * r.report.iterations[5].re);
   }
+  // prune_rate_sweep (BASELINE config 5's protocol): per rate, prune the same
+  // trained model and report train / held-out error -- against the oracle's
+  // compute_responsibilities + prune_step + residuals on the same split
+  {
+    std::mt19937_64 rng(23);
+    std::vector<Coord> coords;
+    std::vector<double> values;
+    std::uniform_int_distribution<int> pi(0, 29), pj(0, 24), pk(0, 19);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    std::vector<char> seen(30 * 25 * 20, 0);
+    while (values.size() < 4000) {
+      const int i = pi(rng), j = pj(rng), k = pk(rng);
+      if (seen[(i * 25 + j) * 20 + k]) continue;
+      seen[(i * 25 + j) * 20 + k] = 1;
+      coords.insert(coords.end(), {Coord(i), Coord(j), Coord(k)});
+      values.push_back(u(rng));
+    }
+    const auto x = make_tensor({30, 25, 20}, coords, values);
+    const auto [tr, te] = split_train_test(x, 0.1, 3);
+    TuckerModel m = init_random(x.dims, {4, 3, 5}, 2);
+    const ModeIndex idx = build_mode_index(tr);
+    for (int t = 0; t < 3; ++t) {
+      update_all_factors(m, tr, idx, Regularizer::LF, 0.01, 1);
+      update_core_lf(m, tr, 0.01, 1);
+    }
+    const TuckerModel keep = m;
+    const std::vector<double> rates = {0.1, 0.5, 0.9};
+    const auto sweep = prune_rate_sweep(m, tr, te, rates);
+    CHECK(sweep.size() == 3);
+    CHECK(m.core == keep.core && m.factors == keep.factors && m.core_mask == keep.core_mask);
+    vo_session* s = nullptr;
+    const std::uint64_t d[3] = {30, 25, 20}, rk[3] = {4, 3, 5};
+    CHECK(vo_create(3, d, tr.nnz(), tr.coords.data(), tr.values.data(), rk, &s) == 0);
+    double te_norm = 0.0;
+    for (double v : te.values) te_norm += v * v;
+    te_norm = std::sqrt(te_norm);
+    double last_sparsity = -1.0;
+    for (std::size_t i = 0; i < sweep.size(); ++i) {
+      const double* f[3] = {keep.factors[0].data(), keep.factors[1].data(), keep.factors[2].data()};
+      const std::uint8_t* fm[3] = {keep.factor_masks[0].data(), keep.factor_masks[1].data(), keep.factor_masks[2].data()};
+      CHECK(vo_set_model(s, keep.core.data(), keep.core_mask.data(), f, fm) == 0);
+      double ss = 0, xn = 0, re = 0;
+      vo_compute_residuals(s, 1, nullptr, &ss, &xn, &re);
+      vo_compute_responsibilities(s, 1, nullptr, nullptr);
+      std::uint64_t cnt[4] = {};
+      vo_prune_step(s, rates[i], nullptr, nullptr, cnt);
+      vo_compute_residuals(s, 1, nullptr, &ss, &xn, &re);
+      std::vector<double> pred(te.nnz());
+      vo_reconstruct(s, te.coords.data(), te.nnz(), pred.data());
+      double err = 0.0;
+      for (std::size_t e = 0; e < te.nnz(); ++e) err += (te.values[e] - pred[e]) * (te.values[e] - pred[e]);
+      const double test_re = std::sqrt(err) / te_norm;
+      const RateResult& g = sweep[i];
+      CHECK(g.rate == rates[i]);
+      CHECK(g.pruned.core == cnt[0] && g.pruned.factors[0] == cnt[1] && g.pruned.factors[1] == cnt[2] &&
+            g.pruned.factors[2] == cnt[3]);
+      CHECK(std::abs(g.train_re - re) <= 1e-6 * re);
+      CHECK(std::abs(g.test_re - test_re) <= 1e-6 * test_re);
+      CHECK(std::abs(g.sparsity - vo_sparsity(s)) <= 1e-15);
+      CHECK(g.sparsity > last_sparsity);
+      last_sparsity = g.sparsity;
+    }
+    vo_destroy(s);
+  }
   {  // data formats: model directory and COO text round trips (vest_io.cpp)
     TuckerModel m = init_random({40, 30, 20}, {3, 2, 4}, 9);
     m.core[1] = 0.0;
