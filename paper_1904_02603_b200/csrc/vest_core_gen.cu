@@ -62,7 +62,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp16(unsigned s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+  asm volatile("cp.async.@CPMOD@.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp8(unsigned s, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(g) : "memory");
@@ -114,7 +114,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
   auto coords = [&](const Cur& c, unsigned (&idx)[M]) {
     const bool v = c.ci < a.nchunks && c.base + lane < c.end;
 #pragma unroll
-    for (int k = 0; k < M; ++k) idx[k] = v ? __ldg(a.oc[k] + c.base + lane) : 0u;
+    for (int k = 0; k < M; ++k) idx[k] = v ? @LDC@(a.oc[k] + c.base + lane) : 0u;
   };
   const unsigned sbase = su32(stage);
   auto issue = [&](const Cur& c, int b, const unsigned (&idx)[M]) {
@@ -171,7 +171,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
       @PT@ t = 0;
 @PREV@
       r -= (double)t;
-      a.r[pos] = r;
+      @STR@;
     }
     if (KIND == 2 || WSQ) sq = fma(r, r, sq);
     if (KIND != 2) {
@@ -313,8 +313,18 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
   const int rslot = o++;
   while (o % 4 != 2) ++o;
   const int ldr = o;
+  // cache hints (VEST_CP_HINT=0/1, VEST_CP_CG=0/1: A/B): the coordinate and
+  // residual streams are touched once per pass (ld/st.global.cs, evict-first)
+  // and the row gathers skip the L1 (cp.async.cg), so the L2 keeps the fp32
+  // factor copies -- the only data a pass reuses
+  static const bool hint = [] { const char* e = getenv("VEST_CP_HINT"); return e ? e[0] == '1' : true; }();
+  static const bool cg = [] { const char* e = getenv("VEST_CP_CG"); return e ? e[0] == '1' : true; }();
   std::ostringstream src;
-  src << kPrelude;
+  {
+    std::string pre = kPrelude;
+    replace_all(pre, "@CPMOD@", cg ? "cg" : "ca");
+    src << pre;
+  }
   const int nb = (int)blocks.size();
   for (int i = 0; i <= nb; ++i) {
     const std::vector<uint32_t> none;
@@ -370,6 +380,8 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@MINB@", std::to_string(cp_min_blocks()));
     replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
     replace_all(p, "@PT@", PT);
+    replace_all(p, "@LDC@", hint ? "__ldcs" : "__ldg");
+    replace_all(p, "@STR@", hint ? "__stcs(a.r + pos, r)" : "a.r[pos] = r");
     replace_all(p, "@ISSUE@", iss.str());
     replace_all(p, "@LOADU@", lu.str());
     replace_all(p, "@PREV@", pv.str());

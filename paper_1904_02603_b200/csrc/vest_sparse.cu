@@ -125,6 +125,18 @@ std::vector<Cell> ordered_cells(const Ctx& c, int n, std::vector<int>& oth) {
 
 // Loads of entry E's other-mode factor rows into registers u<k>_<b>e<E>;
 // pos is the expression of the entry's CSF position.
+// Cache hints of the delta kernel (VEST_SD_HINT=0/1, A/B): the CSF coordinate
+// stream is read once (ld.global.cs, evict-first) and delta is written once
+// for the next kernel (st.global.cs), so the gathered factor rows -- the only
+// data with reuse -- keep the L2.
+bool sd_hint() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_SD_HINT");
+    return e ? e[0] == '1' : true;
+  }();
+  return v;
+}
+
 void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>& oth, int e, const std::string& pos,
                     int lazy = 0, bool f32 = false) {
   const std::string E = std::to_string(e);
@@ -134,12 +146,12 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
     const int lvl = (int)(std::find(oth.begin(), oth.end(), k) - oth.begin());
     if (lvl < lazy && lvl + 1 < (int)oth.size()) {  // read where the prefix opens (emit_cells), not held in registers
       o << "    const " << (c.gather_f32 ? "float" : "double") << "* " << rk << " = a." << (c.gather_f32 ? "g" : "f")
-        << "[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos << ") * " << ld << "ull;\n";
+        << "[" << k << "] + (unsigned long long)" << (sd_hint() ? "__ldcs" : "__ldg") << "(a.oc[" << k << "] + " << pos << ") * " << ld << "ull;\n";
       continue;
     }
     if (c.gather_f32) {  // fp32 copy of the row, widened to fp64 in registers (kept fp32 in the fp32 contraction)
       const bool v4 = ld % 4 == 0;
-      o << "    const float* " << rk << " = a.g[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos
+      o << "    const float* " << rk << " = a.g[" << k << "] + (unsigned long long)" << (sd_hint() ? "__ldcs" : "__ldg") << "(a.oc[" << k << "] + " << pos
         << ") * " << ld << "ull;\n";
       for (int b = 0; b < c.ranks[k]; b += (v4 ? 4 : 2)) {
         const std::string v = "v" + std::to_string(k) + "_" + std::to_string(b) + "e" + E;
@@ -152,7 +164,7 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
       }
       continue;
     }
-    o << "    const double* " << rk << " = a.f[" << k << "] + (unsigned long long)__ldg(a.oc[" << k << "] + " << pos
+    o << "    const double* " << rk << " = a.f[" << k << "] + (unsigned long long)" << (sd_hint() ? "__ldcs" : "__ldg") << "(a.oc[" << k << "] + " << pos
       << ") * " << ld << "ull;\n";
     for (int b = 0; b < c.ranks[k]; b += 2) {
       const std::string ua = u(k, b) + "e" + E;
@@ -293,7 +305,10 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     const std::string E = std::to_string(e);
     if (e > 0) o << "    if (t" << E << " != t0) {\n";
     for (int j = 0; j < c.ranks[n]; ++j)
-      o << "      " << dst << "[" << j << "ull * a.stride + t" << E << "] = " << cv << "d" << j << "e" << E << ";\n";
+      if (sd_hint())
+        o << "      __stcs(" << dst << " + " << j << "ull * a.stride + t" << E << ", " << cv << "d" << j << "e" << E << ");\n";
+      else
+        o << "      " << dst << "[" << j << "ull * a.stride + t" << E << "] = " << cv << "d" << j << "e" << E << ";\n";
     if (e > 0) o << "    }\n";
   }
   o << "  }\n}\n";
