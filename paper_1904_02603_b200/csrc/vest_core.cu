@@ -550,6 +550,10 @@ __global__ void k_gemm_reduce2(const double* raw, int n, int groups, int kind, i
 // shared memory); CTA partials are summed in a fixed order afterwards
 // (deterministic).
 constexpr int kHsBatch = 8, kHsPer = 8, kHsThreads = 256;
+// shared-memory row pitches are compile-time (the widest block, the largest
+// rank), so the accumulation loop's addresses are register + immediate
+constexpr int kHsWP = (kFMax * (kFMax + 1) / 2 + kFMax + 3) & ~3;
+constexpr int kHsAWP = VEST_MAXJ * (VEST_MAXJ + 1) / 2 + VEST_MAXJ;
 __device__ __forceinline__ void hs_cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
@@ -571,8 +575,8 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict
   // statistics rows are staged in 16-byte pieces (stride and the smem row
   // width are multiples of 16 bytes)
   constexpr int V = 16 / sizeof(T);
-  const int wpad = (width + V - 1) / V * V;
-  const int bufw = kHsBatch * wpad;  // T elements per statistics buffer
+  constexpr int wpad = kHsWP;
+  constexpr int bufw = kHsBatch * wpad;  // T elements per statistics buffer
   const uint32_t per = (nchunks + gridDim.x - 1) / gridDim.x;
   const uint32_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
   uint32_t my[kHsPer];
@@ -586,12 +590,12 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict
   T* const sstat = reinterpret_cast<T*>(hs_raw);                     // [2][kHsBatch][wpad]
   double* const sarow = reinterpret_cast<double*>(sstat + 2 * bufw);  // [2][kHsBatch][Jm]
   const int AW = Jm * (Jm + 1) / 2 + Jm;
-  double* const saa = sarow + 2 * kHsBatch * Jm;                       // [kHsBatch][AW]
+  double* const saa = sarow + 2 * kHsBatch * Jm;                       // [kHsBatch][kHsAWP]
   auto stage = [&](uint32_t cb, int buf) {
     const int nb = (int)min((uint32_t)kHsBatch, c1 - cb);
     T* ss = sstat + buf * bufw;
     double* sa = sarow + buf * kHsBatch * Jm;
-    const int pieces = wpad / V;
+    const int pieces = (width + V - 1) / V;
     for (int t = threadIdx.x; t < nb * pieces; t += kHsThreads) {
       const int b = t / pieces, w = V * (t - b * pieces);
       hs_cp16(ss + b * wpad + w, stats + (size_t)(cb + b) * stride + w);
@@ -630,14 +634,25 @@ __global__ void __launch_bounds__(kHsThreads) k_core_hsample(const T* __restrict
     for (int t = threadIdx.x; t < nb * AW; t += kHsThreads) {
       const int b = t / AW, pc = hs_pc[t - b * AW];
       const double a0 = sa[b * Jm + (pc & 255)];
-      saa[t] = pc >= 0 ? a0 * sa[b * Jm + (pc >> 8)] : a0;
+      saa[b * kHsAWP + (t - b * AW)] = pc >= 0 ? a0 * sa[b * Jm + (pc >> 8)] : a0;
     }
     __syncthreads();
-    for (int b = 0; b < nb; ++b) {
+    if (nb == kHsBatch) {
 #pragma unroll
       for (int j = 0; j < kHsPer; ++j) {
         if (my[j] == 0xffffffffu) continue;
-        acc[j] = fma((double)ss[b * wpad + (my[j] & 0xffffu)], saa[b * AW + (my[j] >> 16)], acc[j]);
+        const T* pj = ss + (my[j] & 0xffffu);
+        const double* qj = saa + (my[j] >> 16);
+#pragma unroll
+        for (int b = 0; b < kHsBatch; ++b) acc[j] = fma((double)pj[b * wpad], qj[b * kHsAWP], acc[j]);
+      }
+    } else {
+      for (int b = 0; b < nb; ++b) {
+#pragma unroll
+        for (int j = 0; j < kHsPer; ++j) {
+          if (my[j] == 0xffffffffu) continue;
+          acc[j] = fma((double)ss[b * wpad + (my[j] & 0xffffu)], saa[b * kHsAWP + (my[j] >> 16)], acc[j]);
+        }
       }
     }
     __syncthreads();  // the buffers are re-staged / rewritten from the next batch on
@@ -1280,16 +1295,16 @@ int block_hsample(Ctx& c, const Blocks& b, int bi, int stride) {
   const int width = NS + nf;
   ProfScope ps(c, kProfCoreGemm);
   if (c.stats_f32) {
-    const size_t sm = (size_t)2 * kHsBatch * (((width + 3) & ~3) * sizeof(float) + Jm * sizeof(double)) +
-                      (size_t)kHsBatch * (Jm * (Jm + 1) / 2 + Jm) * sizeof(double);
+    const size_t sm = (size_t)2 * kHsBatch * (kHsWP * sizeof(float) + Jm * sizeof(double)) +
+                      (size_t)kHsBatch * kHsAWP * sizeof(double);
     check(cudaFuncSetAttribute(k_core_hsample<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
           "hsample smem");
     k_core_hsample<float><<<nparts, kHsThreads, sm, c.stream>>>(reinterpret_cast<const float*>(c.d_chunk_stats), stride,
                                                                  width, md.d_chunks, md.nchunks, c.d_factor[m], c.ld[m],
                                                                  Jm, tab, E, c.d_gemm_part);
   } else {
-    const size_t sm = (size_t)2 * kHsBatch * (((width + 1) & ~1) + Jm) * sizeof(double) +
-                      (size_t)kHsBatch * (Jm * (Jm + 1) / 2 + Jm) * sizeof(double);
+    const size_t sm = (size_t)2 * kHsBatch * (kHsWP + Jm) * sizeof(double) +
+                      (size_t)kHsBatch * kHsAWP * sizeof(double);
     check(cudaFuncSetAttribute(k_core_hsample<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
           "hsample smem");
     k_core_hsample<double><<<nparts, kHsThreads, sm, c.stream>>>(c.d_chunk_stats, stride, width, md.d_chunks,

@@ -45,6 +45,7 @@ struct CoreGenState {
   std::vector<cudaKernel_t> k;  // pass i: prev = i - 1, cur = i (i < nb); pass nb: final
   std::vector<int> nt;
   int ldr = 0;
+  bool xf32 = false;  // Gram columns staged as fp32 (fp32 products)
 };
 
 namespace {
@@ -70,15 +71,19 @@ __device__ __forceinline__ void cp8(unsigned s, const void* g) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-template <int NT>
-__device__ __forceinline__ void gram_nt(const double* X, double (&d)[NT * (NT + 1) / 2][2], int lane) {
+// X: the round's Gram columns [column][36] (fp64, or fp32 when the products are
+// fp32 -- half the shared-memory traffic of the fragment loads and column
+// stores); the residual column (last) is always read in fp64 from Xr
+template <int NT, class XT>
+__device__ __forceinline__ void gram_nt(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane) {
   const int g = lane >> 2, tq = lane & 3;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const int e = 4 * kk + tq;
     double f[NT];
 #pragma unroll
-    for (int i = 0; i < NT; ++i) f[i] = X[(8 * i + g) * 36 + e];
+    for (int i = 0; i < NT; ++i) f[i] = (double)X[(8 * i + g) * 36 + e];
+    if (g == 7) f[NT - 1] = Xr[e];
     int t = 0;
 #pragma unroll
     for (int I = 0; I < NT; ++I)
@@ -97,9 +102,11 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
   extern __shared__ __align__(16) double smem[];
   __shared__ @PT@ sq_q[4][32];  // previous block's per-fiber a . dg of the chunk's row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* const stage = smem + (unsigned long long)warp * (32 * LDR + NC * 36);  // one round's rows
-  double* const X = stage + 32 * LDR;
-  for (int t = lane; t < NC * 36; t += 32) X[t] = 0.0;
+  double* const stage = smem + (unsigned long long)warp * (32 * LDR + @XD@ + 32);  // one round's rows
+  @XT@* const X = reinterpret_cast<@XT@*>(stage + 32 * LDR);
+  double* const Xr = stage + 32 * LDR + @XD@;  // the residual column, fp64
+  for (int t = lane; t < NC * 36; t += 32) X[t] = 0;
+  Xr[lane] = 0.0;
   const unsigned wstride = gridDim.x * 4;
   struct Cur { unsigned ci, end, base, row; };
   auto first = [&](unsigned ci) {
@@ -176,9 +183,9 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
     if (KIND == 2 || WSQ) sq = fma(r, r, sq);
     if (KIND != 2) {
 @CUR@
-      X[(NC - 1) * 36 + lane] = r;
+      Xr[lane] = r;
       __syncwarp();
-      gram_nt<NT>(X, d, lane);
+      gram_nt<NT>(X, Xr, d, lane);
     }
     __syncwarp();
     if (nxt.ci != cur.ci) {
@@ -220,14 +227,15 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
 )CUDA";
 
 // CTAs per SM the passes are register-budgeted for (VEST_CP_MINB: A/B).
-// Config 4, fp32 mode, ms per iteration: no bound 259, 1: 254, 3: 250 (kept),
-// 4 (128 registers): 318.
-int cp_min_blocks() {
+// Config 4, ms per iteration -- fp64 products: no bound 259, 1: 254, 3: 250
+// (kept), 4 (128 registers, spills): 318; fp32 products with fp32-staged Gram
+// columns (150 registers unbounded, no spills at 128): 3: 170.2, 4: 168.0 (kept).
+int cp_min_blocks(bool products_f32) {
   static const int v = [] {
     const char* e = getenv("VEST_CP_MINB");
-    return e ? std::max(1, std::min(6, atoi(e))) : 3;
+    return e ? std::max(1, std::min(6, atoi(e))) : 0;
   }();
-  return v;
+  return v > 0 ? v : (products_f32 ? 4 : 3);
 }
 
 // fp32 mode: the fiber products (previous block's residual update, current
@@ -341,7 +349,7 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
       return std::string(pf32 ? "t = fmaf(" : "t = fma(") + e + ", sq_q[warp][" + std::to_string(f) + "], t);";
     }, used, PT);
     products(c, cur, cv, [pf32](int f, const std::string& e) {
-      return "X[" + std::to_string(f * 36) + " + lane] = " + (pf32 ? "(double)(" + e + ")" : e) + ";";
+      return "X[" + std::to_string(f * 36) + " + lane] = " + e + ";";
     }, used, PT);
     std::ostringstream iss, lu;
     for (int k = 0; k < M; ++k) {
@@ -377,9 +385,11 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@JM@", std::to_string(c.ranks[M]));
     replace_all(p, "@LDM@", std::to_string(c.ld[M]));
     replace_all(p, "@RSLOT@", std::to_string(rslot));
-    replace_all(p, "@MINB@", std::to_string(cp_min_blocks()));
+    replace_all(p, "@MINB@", std::to_string(cp_min_blocks(pf32)));
     replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
     replace_all(p, "@PT@", PT);
+    replace_all(p, "@XT@", PT);
+    replace_all(p, "@XD@", std::to_string(pf32 ? NT * 8 * 18 : NT * 8 * 36));
     replace_all(p, "@LDC@", hint ? "__ldcs" : "__ldg");
     replace_all(p, "@STR@", hint ? "__stcs(a.r + pos, r)" : "a.r[pos] = r");
     replace_all(p, "@ISSUE@", iss.str());
@@ -404,6 +414,7 @@ bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, 
   s->key = plan_key;
   s->ldr = ldr;
   s->nt = nts;
+  s->xf32 = cp_f32(c);
   check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "core gen load");
   s->k.resize(nb + 1);
   for (int i = 0; i <= nb; ++i) {
@@ -436,7 +447,7 @@ void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stri
   a.nchunks = csf.nchunks;
   a.stride = stride;
   const int NT = s.nt[i];
-  const size_t sm = (unsigned long long)4 * (32 * s.ldr + NT * 8 * 36) * sizeof(double);
+  const size_t sm = (unsigned long long)4 * (32 * s.ldr + NT * 8 * (s.xf32 ? 18 : 36) + 32) * sizeof(double);
   const void* fn = reinterpret_cast<const void*>(s.k[i]);
   check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "core gen smem");
   int per_sm = 0, sms = 0;
