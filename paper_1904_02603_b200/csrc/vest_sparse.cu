@@ -184,8 +184,9 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
 // group t = sum G u_last, then d[beta_n] += w t.  Every core value G[lin] is a
 // constant-bank operand shared by the ne entries.
 void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<int>& oth, const std::vector<Cell>& cells,
-                int ne, int lazy = 0, bool f32 = false) {
+                int ne, int lazy = 0, bool f32 = false, const std::string& mid = std::string()) {
   const int L = (int)oth.size();
+  bool mid_done = mid.empty();
   const std::string T = f32 ? "float" : "double", Gs = f32 ? "Gf[" : "G[", fma_ = f32 ? "fmaf(" : "fma(";
   for (int e = 0; e < ne; ++e)
     for (int j = 0; j < c.ranks[n]; ++j) o << "    " << T << " d" << j << "e" << e << " = " << (f32 ? "0.0f" : "0.0") << ";\n";
@@ -230,6 +231,10 @@ void emit_cells(std::ostringstream& o, const Ctx& c, int n, const std::vector<in
     }
     for (int q = 0; q + 1 < L; ++q) o << "    }\n";
     i = e_end;
+    if (!mid_done && 4 * i >= cells.size()) {  // a quarter into the contraction
+      o << mid;
+      mid_done = true;
+    }
   }
 }
 
@@ -270,6 +275,20 @@ bool sd_f32(const Ctx& c) {
   return c.gather_f32 && env != 0;
 }
 
+// Next-iteration row prefetch (VEST_SD_PF=1, A/B; off): the thread reads the
+// coordinates of its next grid-stride entries at the top of the iteration and,
+// a quarter into the contraction, prefetches their factor rows into the L2
+// (prefetch.global.L2).  Measured slower (config 4 factor modes 41.4 -> 50.6
+// ms per iteration): the prefetches wait on their coordinate loads inside the
+// contraction and double the gather requests.
+bool sd_prefetch() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_SD_PF");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // entries per thread of the delta kernel (VEST_SD_NE: A/B; 2 in fp64, 3 in fp32 --
 // config 4 fp32 mode, ms per iteration at 2 / 3 / 4: 190.2 / 186.8 / 193.4)
 int sd_entries(const Ctx& c) {
@@ -297,7 +316,19 @@ void emit_mode(std::ostringstream& o, const Ctx& c, int n) {
     o << "    const unsigned long long t" << e << " = t0 + " << 256 * e << "ull < a.n ? t0 + " << 256 * e << "ull : t0;\n";
   const int lazy = oth.size() >= 2 ? std::min<int>(sd_lazy(c), (int)oth.size() - 1) : 0;
   for (int e = 0; e < ne; ++e) emit_row_loads(o, c, oth, e, "a.p0 + t" + std::to_string(e), lazy, f32);
-  emit_cells(o, c, n, oth, cells, ne, lazy, f32);
+  std::ostringstream mid;
+  if (sd_prefetch() && c.gather_f32) {
+    o << "    const unsigned long long tn = t0 + gridDim.x * " << NB << "ull;\n";
+    for (int e = 0; e < ne; ++e)
+      for (int k : oth) {
+        const std::string nm = "n" + std::to_string(k) + "e" + std::to_string(e);
+        o << "    const unsigned " << nm << " = tn + " << 256 * e << "ull < a.n ? __ldcs(a.oc[" << k << "] + a.p0 + tn + "
+          << 256 * e << "ull) : 0xffffffffu;\n";
+        mid << "    if (" << nm << " != 0xffffffffu) asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(a.g[" << k
+            << "] + (unsigned long long)" << nm << " * " << c.ld[k] << "ull));\n";
+      }
+  }
+  emit_cells(o, c, n, oth, cells, ne, lazy, f32, mid.str());
   // delta SoA for k_rowpass_delta: fp64, or fp32 in the fp32 mode (gather_f32)
   const std::string dst = c.gather_f32 ? "reinterpret_cast<float*>(a.out)" : "a.out";
   const std::string cv = c.gather_f32 && !f32 ? "(float)" : "";
