@@ -75,10 +75,12 @@ __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0
 // fp32 -- half the shared-memory traffic of the fragment loads and column
 // stores); the residual column (last) is always read in fp64 from Xr
 template <int NT, class XT>
-__device__ __forceinline__ void gram_nt(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane) {
+__device__ __forceinline__ void gram_nt(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane,
+                                        int nv) {
   const int g = lane >> 2, tq = lane & 3;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
+    if (4 * kk >= nv) break;  // a chunk's last round: k-steps past its entries are all zero (warp-uniform)
     const int e = 4 * kk + tq;
     double f[NT];
 #pragma unroll
@@ -185,7 +187,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
 @CUR@
       Xr[lane] = r;
       __syncwarp();
-      gram_nt<NT>(X, Xr, d, lane);
+      gram_nt<NT>(X, Xr, d, lane, (int)min(32u, cur.end - cur.base));
     }
     __syncwarp();
     if (nxt.ci != cur.ci) {
@@ -322,11 +324,15 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
   while (o % 4 != 2) ++o;
   const int ldr = o;
   // cache hints (VEST_CP_HINT=0/1, VEST_CP_CG=0/1: A/B): the coordinate and
-  // residual streams are touched once per pass (ld/st.global.cs, evict-first)
-  // and the row gathers skip the L1 (cp.async.cg), so the L2 keeps the fp32
-  // factor copies -- the only data a pass reuses
+  // residual streams are touched once per pass (ld/st.global.cs, evict-first);
+  // the row gathers skip the L1 (cp.async.cg: config 4 passes 102.7 -> 99.9 ms)
+  // unless a gathered mode is skewed -- a Zipf head row is read by every SM at
+  // once and only the L1 keeps those reads off one L2 line (config 5 with .cg:
+  // passes 129 -> 465 ms per iteration)
   static const bool hint = [] { const char* e = getenv("VEST_CP_HINT"); return e ? e[0] == '1' : true; }();
-  static const bool cg = [] { const char* e = getenv("VEST_CP_CG"); return e ? e[0] == '1' : true; }();
+  static const int cg_env = [] { const char* e = getenv("VEST_CP_CG"); return e ? (e[0] == '1' ? 1 : 0) : -1; }();
+  bool cg = cg_env != 0;
+  for (int k = 0; k < M && cg_env < 0; ++k) cg = cg && !c.skewed[k];
   std::ostringstream src;
   {
     std::string pre = kPrelude;

@@ -5,5 +5,5 @@
 out=$1; shift
 for v in "$@"; do
   echo "== $v" >> "$out"
-  env $v timeout 900 python bench.py --config 4 --iters ${AB_ITERS:-4} 2>&1 | grep '^{' | sed "s/^{/{\"env\": \"$v\", /" >> "$out"
+  env $v timeout 900 python bench.py --config ${AB_CONFIG:-4} --iters ${AB_ITERS:-4} 2>&1 | grep '^{' | sed "s/^{/{\"env\": \"$v\", /" >> "$out"
 done
