@@ -46,6 +46,7 @@ struct CoreGenState {
   std::vector<int> nt;
   int ldr = 0;
   bool xf32 = false;  // Gram columns staged as fp32 (fp32 products)
+  int nbuf = 1;       // staged rounds in flight
 };
 
 namespace {
@@ -104,9 +105,10 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
   extern __shared__ __align__(16) double smem[];
   __shared__ @PT@ sq_q[4][32];  // previous block's per-fiber a . dg of the chunk's row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* const stage = smem + (unsigned long long)warp * (32 * LDR + @XD@ + 32);  // one round's rows
-  @XT@* const X = reinterpret_cast<@XT@*>(stage + 32 * LDR);
-  double* const Xr = stage + 32 * LDR + @XD@;  // the residual column, fp64
+  constexpr int NBUF = @NBUF@;  // staged rounds in flight (1: next round, 2: the two next rounds)
+  double* const stage = smem + (unsigned long long)warp * (NBUF * 32 * LDR + @XD@ + 32);  // NBUF rounds' rows
+  @XT@* const X = reinterpret_cast<@XT@*>(stage + NBUF * 32 * LDR);
+  double* const Xr = stage + NBUF * 32 * LDR + @XD@;  // the residual column, fp64
   for (int t = lane; t < NC * 36; t += 32) X[t] = 0;
   Xr[lane] = 0.0;
   const unsigned wstride = gridDim.x * 4;
@@ -154,27 +156,36 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
   if (cur.ci >= a.nchunks) return;
   { unsigned i0[M]; coords(cur, i0); issue(cur, 0, i0); }
   Cur nxt = next(cur);
+  Cur ahead = nxt;  // the round whose gathers are issued next
+  if (NBUF == 2) {
+    unsigned i1[M];
+    coords(nxt, i1);
+    issue(nxt, 1, i1);
+    ahead = next(nxt);
+  }
   unsigned inx[M];
-  coords(nxt, inx);
+  coords(ahead, inx);
   prologue(cur);
+  int p = 0;
   double d[NTT][2];
 #pragma unroll
   for (int t = 0; t < NTT; ++t) d[t][0] = d[t][1] = 0.0;
   double sq = 0.0;
   while (true) {
-    // this round's rows -> registers, then the next round's gathers into the
-    // same (single) stage while this round computes: half the shared memory
-    // of a double buffer, 12 instead of 8 resident warps per SM
-    cp_wait0();
+    // this round's rows -> registers, then the gathers of the round NBUF ahead
+    // into the buffer just read, while this round computes (NBUF 1: half the
+    // shared memory, more resident warps; NBUF 2: a gather has two rounds of
+    // compute to land)
+    if (NBUF == 2) cp_wait1(); else cp_wait0();
     __syncwarp();
-    const double* st = stage + lane * LDR;
+    const double* st = stage + (p * 32 + lane) * LDR;
     const unsigned pos = cur.base + lane;
     const bool valid = pos < cur.end;
     double r = st[RSLOT];
 @LOADU@
     __syncwarp();
-    issue(nxt, 0, inx);
-    const Cur nn = next(nxt);
+    issue(ahead, p, inx);
+    const Cur nn = next(ahead);
     coords(nn, inx);
     if (PNF > 0 && valid) {
       @PT@ t = 0;
@@ -222,7 +233,8 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
       prologue(nxt);
     }
     cur = nxt;
-    nxt = nn;
+    if (NBUF == 2) { nxt = ahead; p ^= 1; } else { nxt = nn; }
+    ahead = nn;
   }
   cp_wait0();
 }
@@ -250,6 +262,18 @@ bool cp_f32(const Ctx& c) {
     return !(e && e[0] == '0');
   }();
   return c.gather_f32 && env;
+}
+
+// Staged rounds in flight (VEST_CP_DEPTH=1/2, A/B; 1 kept): with two, a gather
+// has two rounds of compute to land -- config 4 passes 95.9 vs 94.8 ms per
+// iteration with one: the gathers are not what the DMMA pipe waits for (ncu:
+// DMMA pipe 71 %, long_scoreboard 0.9 of 11.5 stall cycles per instruction).
+int cp_depth(const Ctx&) {
+  static const int env = [] {
+    const char* e = getenv("VEST_CP_DEPTH");
+    return e ? std::max(1, std::min(2, atoi(e))) : 1;
+  }();
+  return env;
 }
 
 void replace_all(std::string& s, const std::string& from, const std::string& to) {
@@ -395,6 +419,7 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
     replace_all(p, "@PT@", PT);
     replace_all(p, "@XT@", PT);
+    replace_all(p, "@NBUF@", std::to_string(cp_depth(c)));
     replace_all(p, "@XD@", std::to_string(pf32 ? NT * 8 * 18 : NT * 8 * 36));
     replace_all(p, "@LDC@", hint ? "__ldcs" : "__ldg");
     replace_all(p, "@STR@", hint ? "__stcs(a.r + pos, r)" : "a.r[pos] = r");
@@ -421,6 +446,7 @@ bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, 
   s->ldr = ldr;
   s->nt = nts;
   s->xf32 = cp_f32(c);
+  s->nbuf = cp_depth(c);
   check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "core gen load");
   s->k.resize(nb + 1);
   for (int i = 0; i <= nb; ++i) {
@@ -453,7 +479,7 @@ void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stri
   a.nchunks = csf.nchunks;
   a.stride = stride;
   const int NT = s.nt[i];
-  const size_t sm = (unsigned long long)4 * (32 * s.ldr + NT * 8 * (s.xf32 ? 18 : 36) + 32) * sizeof(double);
+  const size_t sm = (unsigned long long)4 * (s.nbuf * 32 * s.ldr + NT * 8 * (s.xf32 ? 18 : 36) + 32) * sizeof(double);
   const void* fn = reinterpret_cast<const void*>(s.k[i]);
   check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "core gen smem");
   int per_sm = 0, sms = 0;
