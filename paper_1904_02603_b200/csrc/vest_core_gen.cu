@@ -75,13 +75,13 @@ __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0
 // X: the round's Gram columns [column][36] (fp64, or fp32 when the products are
 // fp32 -- half the shared-memory traffic of the fragment loads and column
 // stores); the residual column (last) is always read in fp64 from Xr
-template <int NT, class XT>
-__device__ __forceinline__ void gram_nt(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane,
-                                        int nv) {
+// KK k-steps of 4 entries (straight-line, so the fragment loads of the next
+// k-step are scheduled under this one's DMMAs)
+template <int NT, int KK, class XT>
+__device__ __forceinline__ void gram_kk(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane) {
   const int g = lane >> 2, tq = lane & 3;
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    if (4 * kk >= nv) break;  // a chunk's last round: k-steps past its entries are all zero (warp-uniform)
+  for (int kk = 0; kk < KK; ++kk) {
     const int e = 4 * kk + tq;
     double f[NT];
 #pragma unroll
@@ -93,6 +93,16 @@ __device__ __forceinline__ void gram_nt(const XT* X, const double* Xr, double (&
 #pragma unroll
       for (int J = I; J < NT; ++J) { dmma884(d[t][0], d[t][1], f[I], f[J]); ++t; }
   }
+}
+// a chunk's last round holds nv < 32 entries: k-steps past them are all zero
+// and skipped in steps of 8 entries (warp-uniform branch)
+template <int NT, class XT>
+__device__ __forceinline__ void gram_nt(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane,
+                                        int nv) {
+  if (nv > 24) gram_kk<NT, 8>(X, Xr, d, lane);
+  else if (nv > 16) gram_kk<NT, 6>(X, Xr, d, lane);
+  else if (nv > 8) gram_kk<NT, 4>(X, Xr, d, lane);
+  else gram_kk<NT, 2>(X, Xr, d, lane);
 }
 )CUDA";
 
@@ -188,9 +198,9 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
     const Cur nn = next(ahead);
     coords(nn, inx);
     if (PNF > 0 && valid) {
-      @PT@ t = 0;
+      @PT@ t0 = 0, t1 = 0, t2 = 0, t3 = 0;  // four partial sums: no 31-deep dependent chain
 @PREV@
-      r -= (double)t;
+      r -= (double)((t0 + t1) + (t2 + t3));
       @STR@;
     }
     if (KIND == 2 || WSQ) sq = fma(r, r, sq);
@@ -376,7 +386,8 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     const bool pf32 = cp_f32(c);
     const char* PT = pf32 ? "float" : "double";
     products(c, prev, pv, [pf32](int f, const std::string& e) {
-      return std::string(pf32 ? "t = fmaf(" : "t = fma(") + e + ", sq_q[warp][" + std::to_string(f) + "], t);";
+      const std::string t = "t" + std::to_string(f & 3);
+      return t + (pf32 ? " = fmaf(" : " = fma(") + e + ", sq_q[warp][" + std::to_string(f) + "], " + t + ");";
     }, used, PT);
     products(c, cur, cv, [pf32](int f, const std::string& e) {
       return "X[" + std::to_string(f * 36) + " + lane] = " + e + ";";
