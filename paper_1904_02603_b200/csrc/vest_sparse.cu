@@ -137,6 +137,17 @@ bool sd_hint() {
   return v;
 }
 
+// VEST_SD_LPF=1 (A/B; off): L1 prefetch of the lazily read rows at the top of
+// the iteration, next to the other rows' loads -- measured slower (config 4
+// factor modes 55.8 -> 58.8 ms per iteration).
+bool sd_lazy_prefetch() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_SD_LPF");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>& oth, int e, const std::string& pos,
                     int lazy = 0, bool f32 = false) {
   const std::string E = std::to_string(e);
@@ -147,6 +158,8 @@ void emit_row_loads(std::ostringstream& o, const Ctx& c, const std::vector<int>&
     if (lvl < lazy && lvl + 1 < (int)oth.size()) {  // read where the prefix opens (emit_cells), not held in registers
       o << "    const " << (c.gather_f32 ? "float" : "double") << "* " << rk << " = a." << (c.gather_f32 ? "g" : "f")
         << "[" << k << "] + (unsigned long long)" << (sd_hint() ? "__ldcs" : "__ldg") << "(a.oc[" << k << "] + " << pos << ") * " << ld << "ull;\n";
+      if (sd_lazy_prefetch())  // the row's first lazy read would otherwise miss to DRAM inside the contraction
+        o << "    asm volatile(\"prefetch.global.L1 [%0];\" ::\"l\"(" << rk << "));\n";
       continue;
     }
     if (c.gather_f32) {  // fp32 copy of the row, widened to fp64 in registers (kept fp32 in the fp32 contraction)
