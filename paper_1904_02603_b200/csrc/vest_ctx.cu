@@ -3,7 +3,6 @@
 // (make_tensor / build_mode_index, sparse_tensor.hpp:68-137), model storage,
 // the orchestration of the hot path (update_all_factors, core sweep,
 // residuals, responsibilities, prune), and the C-ABI of include/vest.h.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -160,21 +159,20 @@ __global__ void k_cellbeta(uint32_t* cb, int G, int N, DevModel m) {
   cb[lin] = packed;
 }
 
-static void cub_sort(Ctx& c, const uint32_t* kin, uint32_t* kout, const uint32_t* vin, uint32_t* vout, uint64_t n,
-                     int end_bit, void*& tmp, size_t& tmp_bytes) {
-  size_t need = 0;
-  check(cub::DeviceRadixSort::SortPairs(nullptr, need, kin, kout, vin, vout, (int64_t)n, 0, end_bit, c.stream),
-        "cub sort size");
+// stable sort of (key, value) pairs by the key's low end_bit bits (vest_sort.cu)
+static void sort_pairs(Ctx& c, const uint32_t* kin, uint32_t* kout, const uint32_t* vin, uint32_t* vout, uint64_t n,
+                       int end_bit, void*& tmp, size_t& tmp_bytes) {
+  const size_t need = radix_sort_tmp_bytes(n);
   if (need > tmp_bytes) {
     if (tmp) {
       check(cudaStreamSynchronize(c.stream), "sync");
       cudaFree(tmp);
     }
-    check(cudaMalloc(&tmp, need), "cub tmp");
+    check(cudaMalloc(&tmp, need), "sort tmp");
     tmp_bytes = need;
   }
-  check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int64_t)n, 0, end_bit, c.stream),
-        "cub sort");
+  count_launch(radix_sort_pairs(kin, kout, vin, vout, n, end_bit, tmp, c.stream));
+  check(cudaGetLastError(), "radix sort");
 }
 
 static int bits_for(uint64_t d) {
@@ -267,11 +265,11 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
     k_iota<<<grid, 256, 0, c.stream>>>(perm, nnz);
     for (int k = N - 1; k >= 0; --k) {
       k_gather_key<<<grid, 256, 0, c.stream>>>(d_coords, perm, nnz, N, k, keys);
-      cub_sort(c, keys, keys2, perm, perm2, nnz, bits_for(c.dims[k]), tmp, tmp_bytes);
+      sort_pairs(c, keys, keys2, perm, perm2, nnz, bits_for(c.dims[k]), tmp, tmp_bytes);
       std::swap(perm, perm2);
     }
     k_dups<<<grid, 256, 0, c.stream>>>(d_coords, perm, nnz, N, d_flag + 1);
-    count_launch(2 + 2 * N);
+    count_launch(2 + N);
     check(cudaMemcpyAsync(flags + 1, d_flag + 1, sizeof(int), cudaMemcpyDeviceToHost, c.stream), "dupflag");
     check(cudaStreamSynchronize(c.stream), "dups");
     if (flags[1]) {
@@ -291,12 +289,12 @@ void build_csf(Ctx& c, const uint32_t* h_coords, const double* h_values) {
     if (nnz) {
       k_gather_key<<<grid, 256, 0, c.stream>>>(d_coords, nullptr, nnz, N, n, keys);
       k_iota<<<grid, 256, 0, c.stream>>>(perm, nnz);
-      cub_sort(c, keys, keys2, perm, md.d_eid, nnz, bits_for(c.dims[n]), tmp, tmp_bytes);
+      sort_pairs(c, keys, keys2, perm, md.d_eid, nnz, bits_for(c.dims[n]), tmp, tmp_bytes);
       k_offsets<<<grid, 256, 0, c.stream>>>(keys2, nnz, c.dims[n], md.d_offsets);
       for (int k = 0; k < N; ++k)
         if (k != n) k_csf_fill<<<grid, 256, 0, c.stream>>>(d_coords, d_values, md.d_eid, nnz, N, k, md.d_oc[k], nullptr);
       k_csf_fill<<<grid, 256, 0, c.stream>>>(d_coords, d_values, md.d_eid, nnz, N, 0, nullptr, md.d_val);
-      count_launch(4 + N);
+      count_launch(3 + N);
     } else {
       check(cudaMemsetAsync(md.d_offsets, 0, (c.dims[n] + 1) * sizeof(uint64_t), c.stream), "off0");
     }

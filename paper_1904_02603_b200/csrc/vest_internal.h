@@ -101,6 +101,11 @@ struct ModeData {
   std::vector<uint64_t> h_offsets;
 };
 
+// vest_sort.cu: stable LSD radix sort of (uint32 key, uint32 value) pairs
+size_t radix_sort_tmp_bytes(uint64_t n);
+int radix_sort_pairs(const uint32_t* kin, uint32_t* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, int end_bit,
+                     void* tmp, cudaStream_t stream);
+
 struct Ctx;
 struct SparseState;  // vest_sparse.cu: NVRTC module of the mask-specialised delta contraction
 struct CoreGenState;  // vest_core_gen.cu: NVRTC module of the plan-specialised core passes

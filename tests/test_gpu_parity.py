@@ -135,3 +135,33 @@ def test_init_random_matches_reference():
         dev.init_random(int(g[f"case{k}_seed"]))
         md = dev.get_model()
         assert np.array_equal(md.core, g[f"case{k}_core"])
+
+
+@pytest.mark.parametrize("dims,nnz", [([70000, 300, 5], 1_500_001), ([3, 1 << 20], 400_000), ([40, 30, 20], 8193)])
+def test_mode_index_radix_sort_vs_stable_argsort(dims, nnz):
+    """K1 (vest_sort.cu, the hand-written stable LSD radix sort behind the CSF
+    build): per-mode index == a stable argsort of each coordinate
+    (sparse_tensor.hpp:119-137: ids ascending within a slice), over 1-3 radix
+    passes per mode, a partial last tile, a Zipf-skewed mode and a 20-bit mode;
+    a duplicate coordinate is still detected through the sorted order."""
+    rng = np.random.default_rng(17)
+    total = int(np.prod([float(d) for d in dims]))
+    nnz = min(nnz, total // 2)
+    # distinct coordinates: distinct linear ids, skewed towards low indices of mode 0
+    lin = np.unique((rng.random(2 * nnz) ** 2 * total).astype(np.int64))[:nnz]
+    rng.shuffle(lin)
+    coords = np.stack(np.unravel_index(lin, dims), 1).astype(np.uint32)
+    vals = rng.random(len(lin))
+    x = st.SparseTensor(list(dims), coords, vals)
+    dev = st.Device(x, [2] * len(dims))
+    for n in range(len(dims)):
+        off, ids = dev.mode_index(n)
+        want = np.argsort(coords[:, n], kind="stable")
+        assert np.array_equal(ids, want.astype(ids.dtype))
+        cnt = np.bincount(coords[:, n], minlength=dims[n])
+        assert np.array_equal(off, np.concatenate([[0], np.cumsum(cnt)]).astype(off.dtype))
+    dev.close()
+    bad = coords.copy()
+    bad[-1] = bad[len(bad) // 3]
+    with pytest.raises(ValueError, match="duplicate coordinate"):
+        st.make_tensor(list(dims), bad, vals)
