@@ -197,7 +197,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
     issue(ahead, p, inx);
     const Cur nn = next(ahead);
     coords(nn, inx);
-    if (PNF > 0 && valid) {
+    if (PNF > 0 && valid && @PROBE@ != 2) {
       @PT@ t0 = 0, t1 = 0, t2 = 0, t3 = 0;  // four partial sums: no 31-deep dependent chain
 @PREV@
       r -= (double)((t0 + t1) + (t2 + t3));
@@ -205,10 +205,12 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
     }
     if (KIND == 2 || WSQ) sq = fma(r, r, sq);
     if (KIND != 2) {
+      if (@PROBE@ != 2) {
 @CUR@
+      }
       Xr[lane] = r;
       __syncwarp();
-      gram_nt<NT>(X, Xr, d, lane, (int)min(32u, cur.end - cur.base));
+      if (@PROBE@ != 1) gram_nt<NT>(X, Xr, d, lane, (int)min(32u, cur.end - cur.base));
     }
     __syncwarp();
     if (nxt.ci != cur.ci) {
@@ -429,6 +431,10 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@MINB@", std::to_string(cp_min_blocks(pf32)));
     replace_all(p, "@STATS_T@", c.stats_f32 ? "float" : "double");
     replace_all(p, "@PT@", PT);
+    {  // timing probes only (results invalid): 1 = no Gram, 2 = no products / residual update
+      const char* e = getenv("VEST_CP_PROBE");
+      replace_all(p, "@PROBE@", e ? std::to_string(atoi(e)) : "0");
+    }
     replace_all(p, "@XT@", PT);
     replace_all(p, "@NBUF@", std::to_string(cp_depth(c)));
     replace_all(p, "@XD@", std::to_string(pf32 ? NT * 8 * 18 : NT * 8 * 36));
