@@ -47,6 +47,7 @@ struct CoreGenState {
   int ldr = 0;
   bool xf32 = false;  // Gram columns staged as fp32 (fp32 products)
   int nbuf = 1;       // staged rounds in flight
+  bool pipe = false;  // statistics passes software-pipelined (two column buffers)
 };
 
 namespace {
@@ -77,22 +78,25 @@ __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0
 // stores); the residual column (last) is always read in fp64 from Xr
 // KK k-steps of 4 entries (straight-line, so the fragment loads of the next
 // k-step are scheduled under this one's DMMAs)
+template <int NT, class XT>
+__device__ __forceinline__ void gram_step(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int g, int tq,
+                                          int kk) {
+  const int e = 4 * kk + tq;
+  double f[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) f[i] = (double)X[(8 * i + g) * 36 + e];
+  if (g == 7) f[NT - 1] = Xr[e];
+  int t = 0;
+#pragma unroll
+  for (int I = 0; I < NT; ++I)
+#pragma unroll
+    for (int J = I; J < NT; ++J) { dmma884(d[t][0], d[t][1], f[I], f[J]); ++t; }
+}
 template <int NT, int KK, class XT>
 __device__ __forceinline__ void gram_kk(const XT* X, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane) {
   const int g = lane >> 2, tq = lane & 3;
 #pragma unroll
-  for (int kk = 0; kk < KK; ++kk) {
-    const int e = 4 * kk + tq;
-    double f[NT];
-#pragma unroll
-    for (int i = 0; i < NT; ++i) f[i] = (double)X[(8 * i + g) * 36 + e];
-    if (g == 7) f[NT - 1] = Xr[e];
-    int t = 0;
-#pragma unroll
-    for (int I = 0; I < NT; ++I)
-#pragma unroll
-      for (int J = I; J < NT; ++J) { dmma884(d[t][0], d[t][1], f[I], f[J]); ++t; }
-  }
+  for (int kk = 0; kk < KK; ++kk) gram_step<NT>(X, Xr, d, g, tq, kk);
 }
 // a chunk's last round holds nv < 32 entries: k-steps past them are all zero
 // and skipped in steps of 8 entries (warp-uniform branch)
@@ -252,6 +256,187 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
 }
 )CUDA";
 
+// The statistics pass, software-pipelined inside the warp: while the DMMA Gram
+// of round g runs from one column buffer, the products of round g + 1 (its
+// residual update and Gram columns) are formed into the other -- the generated
+// source interleaves a slice of the product code after every k-step of the
+// Gram, so the FP32/LSU work sits in the issue slots the DMMAs leave free.
+const char* kPassPipe = R"CUDA(
+extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenArgs a) {
+  constexpr int M = @M@, LDR = @LDR@, NT = @NT@, NC = NT * 8, NTT = NT * (NT + 1) / 2;
+  constexpr int NF = @NF@, PNF = @PNF@, JM = @JM@, RSLOT = @RSLOT@, XD = @XD@;
+  constexpr bool WSQ = @WSQ@;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ @PT@ sq_q[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per warp: one round's staged rows | two rounds' Gram columns | their residual columns
+  double* const stage = smem + (unsigned long long)warp * (32 * LDR + 2 * XD + 64);
+  @XT@* const X0 = reinterpret_cast<@XT@*>(stage + 32 * LDR);
+  double* const Xr0 = stage + 32 * LDR + 2 * XD;
+  constexpr int XE = NC * 36;  // elements of one column buffer
+  for (int t = lane; t < 2 * XE; t += 32) X0[t] = 0;
+  Xr0[lane] = 0.0;
+  Xr0[32 + lane] = 0.0;
+  const unsigned wstride = gridDim.x * 4;
+  struct Cur { unsigned ci, end, base, row; };
+  auto first = [&](unsigned ci) {
+    Cur c{ci, 0, 0, 0};
+    if (ci < a.nchunks) { const Chunk ch = a.chunks[ci]; c.end = ch.end; c.base = ch.beg; c.row = ch.row; }
+    return c;
+  };
+  auto next = [&](const Cur& c) {
+    if (c.base + 32 < c.end) return Cur{c.ci, c.end, c.base + 32, c.row};
+    return first(c.ci + wstride);
+  };
+  auto coords = [&](const Cur& c, unsigned (&idx)[M]) {
+    const bool v = c.ci < a.nchunks && c.base + lane < c.end;
+#pragma unroll
+    for (int k = 0; k < M; ++k) idx[k] = v ? @LDC@(a.oc[k] + c.base + lane) : 0u;
+  };
+  const unsigned sbase = su32(stage);
+  auto issue = [&](const Cur& c, int b, const unsigned (&idx)[M]) {
+    if (c.ci < a.nchunks && c.base + lane < c.end) {
+      const unsigned st = sbase + (unsigned)((b * 32 + lane) * LDR) * 8u;
+@ISSUE@
+      cp8(st + RSLOT * 8u, a.r + c.base + lane);
+    } else {
+      double* sp = stage + (b * 32 + lane) * LDR;
+#pragma unroll
+      for (int t = 0; t < LDR; ++t) sp[t] = 0.0;
+    }
+    cp_commit();
+  };
+  auto prologue = [&](const Cur& c) {
+    if (PNF > 0) {
+      double t = 0.0;
+      if (lane < PNF) {
+        const double* arow = a.f[M] + (unsigned long long)c.row * @LDM@;
+#pragma unroll
+        for (int q = 0; q < JM; ++q) t = fma(__ldg(arow + q), __ldg(a.prev_dg + lane * JM + q), t);
+      }
+      sq_q[warp][lane] = (@PT@)t;
+      __syncwarp();
+    }
+  };
+  double sq = 0.0;
+  auto flush_sq = [&](unsigned ci) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) a.chunk_sq[ci] = sq;
+    sq = 0.0;
+  };
+  Cur cur = first(blockIdx.x * 4 + warp);
+  if (cur.ci >= a.nchunks) return;
+  { unsigned i0[M]; coords(cur, i0); issue(cur, 0, i0); }
+  Cur nxt = next(cur);
+  unsigned inx[M];
+  coords(nxt, inx);
+  prologue(cur);
+  double d[NTT][2];
+#pragma unroll
+  for (int t = 0; t < NTT; ++t) d[t][0] = d[t][1] = 0.0;
+  Cur g = cur;  // the round whose Gram is due
+  {  // first round: columns into buffer 0
+    cp_wait0();
+    __syncwarp();
+    const double* st = stage + lane * LDR;
+    const unsigned pos = cur.base + lane;
+    const bool valid = pos < cur.end;
+    double r = st[RSLOT];
+@LOADU@
+    __syncwarp();
+    issue(nxt, 0, inx);
+    const Cur nn = next(nxt);
+    coords(nn, inx);
+    @PT@ t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    @XT@* const X = X0;
+@PREV@
+@FINAL@
+@CUR@
+    Xr0[lane] = r;
+    cur = nxt;
+    nxt = nn;
+  }
+  int p = 0;
+  while (true) {
+    __syncwarp();  // column buffer p is complete
+    const bool more = cur.ci < a.nchunks;
+    const @XT@* const Xg = X0 + p * XE;
+    const double* const Xrg = Xr0 + 32 * p;
+    const int nv = (int)min(32u, g.end - g.base);
+    const bool last_of_chunk = !more || cur.ci != g.ci;
+    Cur nn = cur;
+    if (more) {
+      if (cur.ci != g.ci) {
+        if (WSQ) flush_sq(g.ci);  // every round of g's chunk has had its residual update
+        prologue(cur);
+      }
+      cp_wait0();
+      __syncwarp();
+      const double* st = stage + lane * LDR;
+      const unsigned pos = cur.base + lane;
+      const bool valid = pos < cur.end;
+      double r = st[RSLOT];
+@LOADU@
+      __syncwarp();
+      issue(nxt, 0, inx);
+      nn = next(nxt);
+      coords(nn, inx);
+      @PT@ t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+      @XT@* const X = X0 + (p ^ 1) * XE;
+      if (nv == 32) {
+        const int g_ = lane >> 2, tq_ = lane & 3;
+@INTER@
+      } else {
+        gram_nt<NT>(Xg, Xrg, d, lane, nv);
+@PREV@
+@FINAL@
+@CUR@
+      }
+      Xr0[32 * (p ^ 1) + lane] = r;
+    } else {
+      gram_nt<NT>(Xg, Xrg, d, lane, nv);
+    }
+    if (last_of_chunk) {
+      @STATS_T@* out = reinterpret_cast<@STATS_T@*>(a.stats) + (unsigned long long)g.ci * a.stride;
+      constexpr int NS = NF * (NF + 1) / 2;
+      const int gg = lane >> 2, tq = lane & 3;
+      int t = 0;
+#pragma unroll
+      for (int I = 0; I < NT; ++I) {
+#pragma unroll
+        for (int J = I; J < NT; ++J) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int row = 8 * I + gg, col = 8 * J + 2 * tq + i;
+            if (row <= col && col < NF) out[row * NF - row * (row - 1) / 2 + (col - row)] = (@STATS_T@)d[t][i];
+            else if (col == NC - 1 && row < NF) out[NS + row] = (@STATS_T@)d[t][i];
+            d[t][i] = 0.0;
+          }
+          ++t;
+        }
+      }
+    }
+    if (!more) break;
+    g = cur;
+    cur = nxt;
+    nxt = nn;
+    p ^= 1;
+  }
+  if (WSQ) flush_sq(g.ci);
+  cp_wait0();
+}
+)CUDA";
+
+// VEST_CP_PIPE=0/1 (A/B): the software-pipelined statistics passes.
+bool cp_pipe(const Ctx& c) {
+  static const int env = [] {
+    const char* e = getenv("VEST_CP_PIPE");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return env >= 0 ? env == 1 : false;
+}
+
 // CTAs per SM the passes are register-budgeted for (VEST_CP_MINB: A/B).
 // Config 4, ms per iteration -- fp64 products: no bound 259, 1: 254, 3: 250
 // (kept), 4 (128 registers, spills): 318; fp32 products with fp32-staged Gram
@@ -304,19 +489,26 @@ void fiber_beta(const Ctx& c, uint32_t p, int* beta) {
 }
 
 // straight-line products of a block's fibers; emit(f, expr) consumes each
-void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream& o,
+void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream& out,
               const std::function<std::string(int, const std::string&)>& emit, std::vector<bool>& used,
-              const char* T = "double") {
+              const char* T = "double", std::vector<std::string>* blocks = nullptr) {
   const int M = c.N - 1;
   int prev[VEST_MAXN];
   bool open = false;
+  std::ostringstream o;
+  auto close = [&]() {  // one prefix's products: a self-contained block
+    o << "      }\n";
+    out << o.str();
+    if (blocks) blocks->push_back(o.str());
+    o.str("");
+  };
   for (size_t f = 0; f < fib.size(); ++f) {
     int beta[VEST_MAXN];
     fiber_beta(c, fib[f], beta);
     bool same = open;
     for (int k = 0; k + 1 < M && same; ++k) same = beta[k] == prev[k];
     if (!same) {
-      if (open) o << "      }\n";
+      if (open) close();
       o << "      { const " << T << " w = ";
       if (M == 1) {
         o << "1";
@@ -333,7 +525,37 @@ void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream
     used[(M - 1) * 16 + beta[M - 1]] = true;
     o << "        " << emit((int)f, "w * " + uname(M - 1, beta[M - 1])) << "\n";
   }
-  if (open) o << "      }\n";
+  if (open) close();
+}
+
+// The pipelined pass's interleaved region: one Gram k-step, then a slice of
+// the next round's product code (residual-update blocks in the first slices,
+// then the update itself, Gram-column blocks spread over all eight).
+std::string interleave(const std::vector<std::string>& prev, const std::vector<std::string>& cur,
+                       const std::string& fin) {
+  auto weight = [](const std::string& b) { return (int)std::count(b.begin(), b.end(), '\n'); };
+  std::vector<std::string> slice(8);
+  std::vector<int> w(8, 0);
+  for (size_t i = 0; i < prev.size(); ++i) {  // slices 0..2, lightest first
+    int k = 0;
+    for (int q = 1; q < 3; ++q)
+      if (w[q] < w[k]) k = q;
+    slice[k] += prev[i];
+    w[k] += weight(prev[i]);
+  }
+  slice[prev.empty() ? 0 : 3] += fin;
+  w[prev.empty() ? 0 : 3] += 3;
+  for (size_t i = 0; i < cur.size(); ++i) {
+    int k = 0;
+    for (int q = 1; q < 8; ++q)
+      if (w[q] < w[k]) k = q;
+    slice[k] += cur[i];
+    w[k] += weight(cur[i]);
+  }
+  std::string o;
+  for (int kk = 0; kk < 8; ++kk)
+    o += "        gram_step<NT>(Xg, Xrg, d, g_, tq_, " + std::to_string(kk) + ");\n" + slice[kk];
+  return o;
 }
 
 }  // namespace
@@ -385,15 +607,17 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     nts.push_back(NT);
     std::vector<bool> used(VEST_MAXN * 16, false);
     std::ostringstream pv, cv;
+    std::vector<std::string> pblk, cblk;
     const bool pf32 = cp_f32(c);
+    const bool pipe = cp_pipe(c) && i < nb;  // the final (r^2 only) pass has no Gram to overlap
     const char* PT = pf32 ? "float" : "double";
     products(c, prev, pv, [pf32](int f, const std::string& e) {
       const std::string t = "t" + std::to_string(f & 3);
       return t + (pf32 ? " = fmaf(" : " = fma(") + e + ", sq_q[warp][" + std::to_string(f) + "], " + t + ");";
-    }, used, PT);
+    }, used, PT, &pblk);
     products(c, cur, cv, [pf32](int f, const std::string& e) {
       return "X[" + std::to_string(f * 36) + " + lane] = " + e + ";";
-    }, used, PT);
+    }, used, PT, &cblk);
     std::ostringstream iss, lu;
     for (int k = 0; k < M; ++k) {
       if (f32) {  // fp32 row copies: ld floats, 16-byte pieces when ld % 4 == 0, else 8-byte
@@ -416,7 +640,14 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
       for (int b = 0; b < c.ranks[k]; ++b)
         if (used[k * 16 + b]) lu << "    const double " << uname(k, b) << " = st[" << soff[k] + b << "];\n";
     }
-    std::string p = kPass;
+    std::string p = pipe ? kPassPipe : kPass;
+    if (pipe) {
+      const std::string fin =
+          "      if (PNF > 0 && valid) { r -= (double)((t0 + t1) + (t2 + t3)); @STR@; }\n"
+          "      if (WSQ) sq = fma(r, r, sq);\n";
+      replace_all(p, "@INTER@", interleave(pblk, cblk, fin));
+      replace_all(p, "@FINAL@", fin);
+    }
     replace_all(p, "@NAME@", "vest_cp_" + std::to_string(i));
     replace_all(p, "@M@", std::to_string(M));
     replace_all(p, "@LDR@", std::to_string(ldr));
@@ -464,6 +695,7 @@ bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, 
   s->nt = nts;
   s->xf32 = cp_f32(c);
   s->nbuf = cp_depth(c);
+  s->pipe = cp_pipe(c);
   check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "core gen load");
   s->k.resize(nb + 1);
   for (int i = 0; i <= nb; ++i) {
@@ -496,7 +728,9 @@ void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stri
   a.nchunks = csf.nchunks;
   a.stride = stride;
   const int NT = s.nt[i];
-  const size_t sm = (unsigned long long)4 * (s.nbuf * 32 * s.ldr + NT * 8 * (s.xf32 ? 18 : 36) + 32) * sizeof(double);
+  const bool pipe = s.pipe && i + 1 < (int)s.k.size();
+  const int xd = NT * 8 * (s.xf32 ? 18 : 36);
+  const size_t sm = (unsigned long long)4 * (pipe ? 32 * s.ldr + 2 * xd + 64 : s.nbuf * 32 * s.ldr + xd + 32) * sizeof(double);
   const void* fn = reinterpret_cast<const void*>(s.k[i]);
   check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "core gen smem");
   int per_sm = 0, sms = 0;
