@@ -48,6 +48,7 @@ struct CoreGenState {
   bool xf32 = false;  // Gram columns staged as fp32 (fp32 products)
   int nbuf = 1;       // staged rounds in flight
   bool pipe = false;  // statistics passes software-pipelined (two column buffers)
+  bool xt = false;    // entry-major Gram columns (640 doubles per warp)
 };
 
 namespace {
@@ -98,6 +99,42 @@ __device__ __forceinline__ void gram_kk(const XT* X, const double* Xr, double (&
 #pragma unroll
   for (int kk = 0; kk < KK; ++kk) gram_step<NT>(X, Xr, d, g, tq, kk);
 }
+// Entry-major columns (fp32 products only): Xt[entry][4 g + i] holds Gram column
+// 8 i + g of that entry (pitch 40 floats), so a lane stores its 32 products with
+// 8 16-byte stores and loads the four fragments of a k-step with ONE 16-byte
+// load (both conflict-free) -- the pass is issue-bound (a DMMA holds the
+// scheduler's dispatch for its 16 cycles), so every instruction saved outside
+// the Gram is time saved.
+template <int NT>
+__device__ __forceinline__ void gram_step_t(const float* Xt, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int g,
+                                            int tq, int kk) {
+  const int e = 4 * kk + tq;
+  const float4 v = *reinterpret_cast<const float4*>(Xt + e * 40 + 4 * g);
+  const float vv[4] = {v.x, v.y, v.z, v.w};
+  double f[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) f[i] = (double)vv[i];
+  if (g == 7) f[NT - 1] = Xr[e];
+  int t = 0;
+#pragma unroll
+  for (int I = 0; I < NT; ++I)
+#pragma unroll
+    for (int J = I; J < NT; ++J) { dmma884(d[t][0], d[t][1], f[I], f[J]); ++t; }
+}
+template <int NT, int KK>
+__device__ __forceinline__ void gram_kk_t(const float* Xt, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk) gram_step_t<NT>(Xt, Xr, d, g, tq, kk);
+}
+template <int NT>
+__device__ __forceinline__ void gram_nt_t(const float* Xt, const double* Xr, double (&d)[NT * (NT + 1) / 2][2], int lane,
+                                          int nv) {
+  if (nv > 24) gram_kk_t<NT, 8>(Xt, Xr, d, lane);
+  else if (nv > 16) gram_kk_t<NT, 6>(Xt, Xr, d, lane);
+  else if (nv > 8) gram_kk_t<NT, 4>(Xt, Xr, d, lane);
+  else gram_kk_t<NT, 2>(Xt, Xr, d, lane);
+}
 // a chunk's last round holds nv < 32 entries: k-steps past them are all zero
 // and skipped in steps of 8 entries (warp-uniform branch)
 template <int NT, class XT>
@@ -123,7 +160,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
   double* const stage = smem + (unsigned long long)warp * (NBUF * 32 * LDR + @XD@ + 32);  // NBUF rounds' rows
   @XT@* const X = reinterpret_cast<@XT@*>(stage + NBUF * 32 * LDR);
   double* const Xr = stage + NBUF * 32 * LDR + @XD@;  // the residual column, fp64
-  for (int t = lane; t < NC * 36; t += 32) X[t] = 0;
+  for (int t = lane; t < @XN@; t += 32) X[t] = 0;
   Xr[lane] = 0.0;
   const unsigned wstride = gridDim.x * 4;
   struct Cur { unsigned ci, end, base, row; };
@@ -214,7 +251,7 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
       }
       Xr[lane] = r;
       __syncwarp();
-      if (@PROBE@ != 1) gram_nt<NT>(X, Xr, d, lane, (int)min(32u, cur.end - cur.base));
+      if (@PROBE@ != 1) @GRAM@<NT>(X, Xr, d, lane, (int)min(32u, cur.end - cur.base));
     }
     __syncwarp();
     if (nxt.ci != cur.ci) {
@@ -428,6 +465,15 @@ extern "C" __global__ void __launch_bounds__(128, @MINB@) @NAME@(const CoreGenAr
 }
 )CUDA";
 
+// VEST_CP_XT=0/1 (A/B): entry-major Gram columns (fp32 products, non-pipelined passes).
+bool cp_xt(const Ctx& c) {
+  static const bool env = [] {
+    const char* e = getenv("VEST_CP_XT");
+    return !(e && e[0] == '0');
+  }();
+  return env;
+}
+
 // VEST_CP_PIPE=0/1 (A/B): the software-pipelined statistics passes.
 bool cp_pipe(const Ctx& c) {
   static const int env = [] {
@@ -491,12 +537,19 @@ void fiber_beta(const Ctx& c, uint32_t p, int* beta) {
 // straight-line products of a block's fibers; emit(f, expr) consumes each
 void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream& out,
               const std::function<std::string(int, const std::string&)>& emit, std::vector<bool>& used,
-              const char* T = "double", std::vector<std::string>* blocks = nullptr) {
+              const char* T = "double", std::vector<std::string>* blocks = nullptr,
+              const std::function<std::string(int)>& dot_coef = nullptr, const char* fma_name = "fma") {
+  // dot_coef (the residual update): sum_f (w u_f) q_f is formed per prefix as
+  // w * (sum_f u_f q_f) -- one FMA per fiber plus one per prefix instead of a
+  // multiply and an FMA per fiber; emit(block index, "w * in") consumes it
   const int M = c.N - 1;
   int prev[VEST_MAXN];
-  bool open = false;
+  bool open = false, first_in = true;
+  int nblk = 0;
   std::ostringstream o;
   auto close = [&]() {  // one prefix's products: a self-contained block
+    if (dot_coef) o << "        " << emit(nblk, "w, in") << "\n";
+    ++nblk;
     o << "      }\n";
     out << o.str();
     if (blocks) blocks->push_back(o.str());
@@ -520,9 +573,17 @@ void products(const Ctx& c, const std::vector<uint32_t>& fib, std::ostringstream
       }
       o << ";\n";
       open = true;
+      first_in = true;
     }
     for (int k = 0; k < M; ++k) prev[k] = beta[k];
     used[(M - 1) * 16 + beta[M - 1]] = true;
+    if (dot_coef) {
+      const std::string u = uname(M - 1, beta[M - 1]), q = dot_coef((int)f);
+      if (first_in) o << "        " << T << " in = " << u << " * " << q << ";\n";
+      else o << "        in = " << fma_name << "(" << u << ", " << q << ", in);\n";
+      first_in = false;
+      continue;
+    }
     o << "        " << emit((int)f, "w * " + uname(M - 1, beta[M - 1])) << "\n";
   }
   if (open) close();
@@ -611,13 +672,24 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     const bool pf32 = cp_f32(c);
     const bool pipe = cp_pipe(c) && i < nb;  // the final (r^2 only) pass has no Gram to overlap
     const char* PT = pf32 ? "float" : "double";
-    products(c, prev, pv, [pf32](int f, const std::string& e) {
-      const std::string t = "t" + std::to_string(f & 3);
-      return t + (pf32 ? " = fmaf(" : " = fma(") + e + ", sq_q[warp][" + std::to_string(f) + "], " + t + ");";
-    }, used, PT, &pblk);
-    products(c, cur, cv, [pf32](int f, const std::string& e) {
+    products(c, prev, pv, [pf32](int b, const std::string& e) {  // e = "w, in" of prefix block b
+      const std::string t = "t" + std::to_string(b & 3);
+      return t + (pf32 ? " = fmaf(" : " = fma(") + e + ", " + t + ");";
+    }, used, PT, &pblk, [](int f) { return "sq_q[warp][" + std::to_string(f) + "]"; }, pf32 ? "fmaf" : "fma");
+    const bool xt = pf32 && !pipe && cp_xt(c);
+    if (xt) {
+      cv << "      float p0 = 0.f";
+      for (int f = 1; f < 32; ++f) cv << ", p" << f << " = 0.f";
+      cv << ";\n";
+    }
+    products(c, cur, cv, [pf32, xt](int f, const std::string& e) {
+      if (xt) return "p" + std::to_string(f) + " = " + e + ";";
       return "X[" + std::to_string(f * 36) + " + lane] = " + e + ";";
     }, used, PT, &cblk);
+    if (xt)
+      for (int g = 0; g < 8; ++g)
+        cv << "      *reinterpret_cast<float4*>(X + lane * 40 + " << 4 * g << ") = make_float4(p" << g << ", p" << 8 + g
+           << ", p" << 16 + g << ", p" << 24 + g << ");\n";
     std::ostringstream iss, lu;
     for (int k = 0; k < M; ++k) {
       if (f32) {  // fp32 row copies: ld floats, 16-byte pieces when ld % 4 == 0, else 8-byte
@@ -668,7 +740,9 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     }
     replace_all(p, "@XT@", PT);
     replace_all(p, "@NBUF@", std::to_string(cp_depth(c)));
-    replace_all(p, "@XD@", std::to_string(pf32 ? NT * 8 * 18 : NT * 8 * 36));
+    replace_all(p, "@XD@", std::to_string(xt ? 640 : (pf32 ? NT * 8 * 18 : NT * 8 * 36)));
+    replace_all(p, "@XN@", xt ? "32 * 40" : "NC * 36");
+    replace_all(p, "@GRAM@", xt ? "gram_nt_t" : "gram_nt");
     replace_all(p, "@LDC@", hint ? "__ldcs" : "__ldg");
     replace_all(p, "@STR@", hint ? "__stcs(a.r + pos, r)" : "a.r[pos] = r");
     replace_all(p, "@ISSUE@", iss.str());
@@ -696,6 +770,7 @@ bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, 
   s->xf32 = cp_f32(c);
   s->nbuf = cp_depth(c);
   s->pipe = cp_pipe(c);
+  s->xt = s->xf32 && !s->pipe && cp_xt(c);
   check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "core gen load");
   s->k.resize(nb + 1);
   for (int i = 0; i <= nb; ++i) {
@@ -729,7 +804,7 @@ void core_gen_pass(Ctx& c, int i, const double* prev_dg, double* stats, int stri
   a.stride = stride;
   const int NT = s.nt[i];
   const bool pipe = s.pipe && i + 1 < (int)s.k.size();
-  const int xd = NT * 8 * (s.xf32 ? 18 : 36);
+  const int xd = s.xt ? 640 : NT * 8 * (s.xf32 ? 18 : 36);
   const size_t sm = (unsigned long long)4 * (pipe ? 32 * s.ldr + 2 * xd + 64 : s.nbuf * 32 * s.ldr + xd + 32) * sizeof(double);
   const void* fn = reinterpret_cast<const void*>(s.k[i]);
   check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "core gen smem");
