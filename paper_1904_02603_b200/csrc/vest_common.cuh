@@ -312,7 +312,8 @@ __device__ __forceinline__ void gram_dmma(const double* X, double (&d)[3][2], in
     if constexpr (NC > 8) {
       const double f1 = X[(8 + g) * ld + e];
       dmma884(d[1][0], d[1][1], f0, f1);
-      dmma884(d[2][0], d[2][1], f1, f1);
+      // NC == 9 (J == 8): the second tile row holds x alone, tile (1,1) would be x . x, which no one reads
+      if constexpr (NC > 9) dmma884(d[2][0], d[2][1], f1, f1);
     }
   }
 }
