@@ -10,8 +10,8 @@
 //   2. scan          exclusive prefix over hist in (digit, tile) order: the
 //                    global position of each tile's first element per digit
 //   3. k_rs_scatter  the warp walks its tile 32 elements at a time, in order;
-//                    lanes with equal digits find each other with
-//                    __match_any_sync, a lane's rank among them is the popcount
+//                    lanes with equal digits find each other with eight
+//                    ballots (one per digit bit), a lane's rank among them is the popcount
 //                    of the lower lanes -- stable without any atomics -- and
 //                    the tile's running per-digit position lives in shared
 //                    memory.
@@ -34,6 +34,20 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Lanes holding the same 8-bit digit as this one (valid lanes only): eight
+// ballots, one per digit bit -- a fixed cost, where match.any iterates once per
+// distinct value in the warp (~32 for random digits).
+__device__ __forceinline__ uint32_t same_digit(uint32_t d, bool valid) {
+  uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
+  }
+  return m;
+}
+
 __global__ void __launch_bounds__(kRsWarps * 32) k_rs_hist(const uint32_t* __restrict__ keys, uint64_t n, int shift,
                                                            uint32_t mask, uint32_t ntiles,
                                                            uint32_t* __restrict__ hist) {
@@ -47,8 +61,8 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_hist(const uint32_t* __res
     for (uint64_t i0 = beg; i0 < end; i0 += 32) {
       const uint64_t i = i0 + lane;
       const bool valid = i < end;
-      const uint32_t d = valid ? (__ldg(keys + i) >> shift) & mask : 0x10000u | lane;
-      const uint32_t m = __match_any_sync(0xffffffffu, d);
+      const uint32_t d = valid ? (__ldg(keys + i) >> shift) & mask : 0u;
+      const uint32_t m = same_digit(d, valid);
       if (valid && (m & lanemask_lt()) == 0) h[warp][d] += __popc(m);  // one leader per digit
       __syncwarp();
     }
@@ -70,13 +84,18 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
     for (int j = 0; j < 8; ++j) base[warp][lane + 32 * j] = offs[(uint64_t)(lane + 32 * j) * ntiles + tile];
     __syncwarp();
     const uint64_t beg = (uint64_t)tile * kRsTile, end = min(n, beg + kRsTile);
+    uint32_t nkey = beg + lane < end ? __ldg(kin + beg + lane) : 0u;  // one step ahead
+    uint32_t nval = beg + lane < end ? __ldg(vin + beg + lane) : 0u;
     for (uint64_t i0 = beg; i0 < end; i0 += 32) {
       const uint64_t i = i0 + lane;
       const bool valid = i < end;
-      const uint32_t key = valid ? __ldg(kin + i) : 0u;
-      const uint32_t val = valid ? __ldg(vin + i) : 0u;
-      const uint32_t d = valid ? (key >> shift) & mask : 0x10000u | lane;
-      const uint32_t m = __match_any_sync(0xffffffffu, d);
+      const uint32_t key = nkey, val = nval;
+      if (i + 32 < end) {
+        nkey = __ldg(kin + i + 32);
+        nval = __ldg(vin + i + 32);
+      }
+      const uint32_t d = valid ? (key >> shift) & mask : 0u;
+      const uint32_t m = same_digit(d, valid);
       const uint32_t rank = __popc(m & lanemask_lt());
       if (valid) {
         const uint32_t pos = base[warp][d] + rank;
@@ -187,6 +206,10 @@ int radix_sort_pairs(const uint32_t* kin, uint32_t* kout, const uint32_t* vin, u
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const unsigned grid = (unsigned)std::min<uint64_t>((ntiles + kRsWarps - 1) / kRsWarps, (uint64_t)sms * 8);
+  // the scatter's write frontier is (resident warps) x 256 bins x 2 arrays x one
+  // 32-byte sector: 2 CTAs per SM keep it (~39 MB) inside the L2, so sectors
+  // fill there before they are written back
+  const unsigned sgrid = (unsigned)std::min<uint64_t>((ntiles + kRsWarps - 1) / kRsWarps, (uint64_t)sms * 2);
   const uint32_t* sk = kin;
   const uint32_t* sv = vin;
   int launches = 0;
@@ -201,7 +224,7 @@ int radix_sort_pairs(const uint32_t* kin, uint32_t* kout, const uint32_t* vin, u
     k_scan_sums<<<nb, kScanThreads, 0, stream>>>(hist, len, sums);
     k_scan_top<<<1, kScanThreads, 0, stream>>>(sums, nb);
     k_scan_apply<<<nb, kScanThreads, 0, stream>>>(hist, len, sums);
-    k_rs_scatter<<<grid, kRsWarps * 32, 0, stream>>>(sk, sv, dk, dv, n, shift, mask, ntiles, hist);
+    k_rs_scatter<<<sgrid, kRsWarps * 32, 0, stream>>>(sk, sv, dk, dv, n, shift, mask, ntiles, hist);
     launches += 5;
     sk = dk;
     sv = dv;
