@@ -495,7 +495,13 @@ def run_ours(args, rank, world, local_rank):
         return
     peak = C.c_double()
     pclk = Clocks(local_rank).__enter__()  # the peak is quoted with the SM clock it ran at
-    L.vest_measure_fp64_peak(local_rank, C.byref(peak))
+    best, t_end = 0.0, time.perf_counter() + 0.6  # repeated for ~0.6 s so the 50 ms clock sampler sees it
+    while True:
+        L.vest_measure_fp64_peak(local_rank, C.byref(peak))
+        best = max(best, peak.value)
+        if time.perf_counter() >= t_end:
+            break
+    peak.value = best
     pclk.__exit__(None, None, None)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
