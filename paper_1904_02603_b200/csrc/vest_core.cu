@@ -1381,6 +1381,38 @@ void core_apply_pending_general(Ctx& c) {
   c.r_pending_general = false;
 }
 
+// Key of a plan's generated module: the plan, plus the two sweep-level choices
+// the source depends on (fp32 chunk statistics, deferred last pass).
+static uint64_t gen_module_key(uint64_t pk, bool stats_f32, bool defer_last) {
+  return pk * 1099511628211ull ^ (0x9E3779B97F4A7C15ull + (stats_f32 ? 2u : 0u) + (defer_last ? 1u : 0u));
+}
+
+// Start compiling the plan-specialised passes of the current mask on a host
+// thread (note_sweep: the first sweep with a new mask; auto mode switches them
+// in from the second).  The source is generated here, with the sweep-level
+// flags the second sweep will use.
+void core_gen_prefetch(Ctx& c) {
+  if (c.core_gen_mode >= 0) return;  // forced on: compiled where first used; off: never
+  if (!(c.ops && !c.force_generic && c.core_block == 0 && nvrtc_available()) || structured_ops(c)) return;
+  const int F = pick_block(c);
+  const Blocks b = plan_general(c, F);
+  if (b.fib.empty()) return;
+  bool elig = true;
+  for (size_t bi = 0; bi < b.start.size(); ++bi) elig = elig && hsample_eligible(c, b.len[bi], b.nlive[bi]);
+  const bool sf = c.gather_f32 && elig, dl = defer_last_enabled() && elig;
+  const uint64_t key = gen_module_key(plan_key(c, b, F), sf, dl);
+  if (c.pre_gen.valid && c.pre_gen.key == key) return;
+  const bool sf0 = c.stats_f32, dl0 = c.defer_last;
+  c.stats_f32 = sf;
+  c.defer_last = dl;
+  std::vector<int> nts;
+  int ldr = 0;
+  std::string src = core_gen_source(c, block_lists(b), nts, ldr);
+  c.stats_f32 = sf0;
+  c.defer_last = dl0;
+  prefetch_cubin(c, c.pre_gen, key, std::move(src), "vest_core_gen.cu");
+}
+
 // the general plan's blocks (host-only compile check of the generated passes)
 std::vector<std::vector<uint32_t>> core_gen_plan(const Ctx& c) { return block_lists(plan_general(c, pick_block(c))); }
 
@@ -1440,7 +1472,7 @@ static void core_sweep_impl(Ctx& c, int reg, double lambda) {
   c.defer_last = gen && defer_last_enabled();
   for (size_t bi = 0; c.defer_last && bi < b.start.size(); ++bi)
     c.defer_last = hsample_eligible(c, b.len[bi], b.nlive[bi]);
-  if (gen) core_gen_prepare(c, block_lists(b), plan_key(c, b, F));
+  if (gen) core_gen_prepare(c, block_lists(b), gen_module_key(plan_key(c, b, F), c.stats_f32, c.defer_last));
   if (!sops) upload_hsample_tables(c, b);
   for (int bi = 0; bi <= nb; ++bi) {
     const bool last = bi == nb;

@@ -761,7 +761,9 @@ bool core_gen_prepare(Ctx& c, const std::vector<std::vector<uint32_t>>& blocks, 
   core_gen_free(c);
   std::vector<int> nts;
   int ldr = 0;
-  const std::vector<char> cubin = nvrtc_compile(core_gen_source(c, blocks, nts, ldr), "vest_core_gen.cu");
+  const std::string src = core_gen_source(c, blocks, nts, ldr);  // also the passes' tile counts and row pitch
+  std::vector<char> cubin;
+  if (!take_cubin(c.pre_gen, plan_key, cubin)) cubin = nvrtc_compile(src, "vest_core_gen.cu");
   const int nb = (int)blocks.size();
   auto* s = new CoreGenState;
   s->key = plan_key;

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <future>
 #include <string>
 #include <vector>
 
@@ -212,6 +213,17 @@ struct Ctx {
   // an NVRTC compile, a stable one pays it once)
   uint64_t mask_key = 0;
   int mask_sweeps = 0;
+  // The mask's kernels are NVRTC-compiled on host threads from the FIRST sweep
+  // with a new mask on (the sweep itself runs the precompiled kernels), so the
+  // second sweep -- where they are switched in -- waits only for what is left of
+  // the compile.  Which kernels run in which sweep is unchanged (deterministic).
+  struct AsyncCubin {
+    bool valid = false;
+    uint64_t key = 0;
+    std::shared_future<std::vector<char>> fut;
+  };
+  AsyncCubin pre_sparse, pre_gen;
+  std::vector<std::shared_future<std::vector<char>>> pre_stale;  // superseded compiles still running
   // CUDA graph of one CD iteration (3-mode all-prefix path, single GPU):
   // captured once the iteration's host logic has repeated with the same key
   bool capturing = false;            // inside stream capture: no host syncs
@@ -288,6 +300,9 @@ cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunk
                                  uint64_t dstride, uint64_t p0, cudaStream_t s, bool f32);  // delta fp32 or fp64
 bool sparse_delta_enabled(const Ctx& c);
 bool sparse_delta_eligible(const Ctx& c);
+void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src, const char* name);
+bool take_cubin(Ctx::AsyncCubin& slot, uint64_t key, std::vector<char>& out);
+void core_gen_prefetch(Ctx& c);  // vest_core.cu: the general plan's passes for the current mask
 void note_sweep(Ctx& c);  // a factor sweep starts (mode 0): count sweeps per core mask
 void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out);
 void sparse_free(Ctx& c);

@@ -25,6 +25,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -513,7 +514,7 @@ std::string gen_source(const Ctx& c) {
       << "  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < " << c.G << "; i += gridDim.x * blockDim.x) Gf_src[i] = (float)s[i];\n"
       << "}\n";
   for (int n = 0; n < c.N; ++n) emit_mode(o, c, n);
-  if (fused_ok(c)) {
+  if (sparse_fused_enabled(c)) {  // off by default: not worth half the module's compile time
     o << kFusedPrelude;
     for (int n = 0; n < c.N; ++n) emit_fused(o, c, n);
   }
@@ -531,6 +532,7 @@ uint64_t mask_key(const Ctx& c) {
   for (uint8_t m : c.h_core_mask) mix(m);
   mix(0xF32u + (uint64_t)c.gather_f32);
   mix(0x5DF32u + (uint64_t)sd_f32(c) * 16 + (uint64_t)sd_entries(c));
+  mix(0xF05Du + (uint64_t)sparse_fused_enabled(c));
   return h;
 }
 
@@ -591,6 +593,46 @@ bool sparse_delta_enabled(const Ctx& c) {
 
 uint64_t core_mask_hash(const Ctx& c) { return mask_key(c); }
 
+// VEST_NVRTC_ASYNC=0: compile the mask's kernels where they are first used (A/B)
+static bool nvrtc_async() {
+  static const bool v = [] {
+    const char* e = getenv("VEST_NVRTC_ASYNC");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+std::vector<char> nvrtc_compile(const std::string& src, const char* name);
+
+// Start compiling `src` on a host thread unless that key is already in the
+// slot.  A superseded compile that is still running is parked (its future's
+// destructor would block); while one is parked no new compile is started -- a
+// schedule that prunes every iteration must not pile up compiler threads.
+void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src, const char* name) {
+  if (!nvrtc_async()) return;
+  if (slot.valid && slot.key == key) return;
+  auto running = [](const std::shared_future<std::vector<char>>& f) {
+    return f.valid() && f.wait_for(std::chrono::seconds(0)) != std::future_status::ready;
+  };
+  if (slot.valid && running(slot.fut)) c.pre_stale.push_back(slot.fut);
+  slot.valid = false;
+  for (size_t i = 0; i < c.pre_stale.size();)
+    if (running(c.pre_stale[i])) ++i;
+    else c.pre_stale.erase(c.pre_stale.begin() + (long)i);
+  if (!c.pre_stale.empty()) return;
+  slot.key = key;
+  slot.fut = std::async(std::launch::async, [s = std::move(src), name]() { return nvrtc_compile(s, name); }).share();
+  slot.valid = true;
+}
+
+// The slot's cubin when it was compiled for `key` (waits for the compile).
+bool take_cubin(Ctx::AsyncCubin& slot, uint64_t key, std::vector<char>& out) {
+  if (!slot.valid || slot.key != key) return false;
+  slot.valid = false;
+  out = slot.fut.get();  // rethrows a compile error
+  return true;
+}
+
 void note_sweep(Ctx& c) {
   const uint64_t key = mask_key(c);
   if (key == c.mask_key && c.mask_sweeps > 0) {
@@ -598,6 +640,10 @@ void note_sweep(Ctx& c) {
   } else {
     c.mask_key = key;
     c.mask_sweeps = 1;
+    // auto mode switches the mask's kernels in from the next sweep: compile them now, off-thread
+    if (sparse_mode(c) < 0 && sparse_delta_eligible(c) && !(c.sparse && c.sparse->key == key))
+      prefetch_cubin(c, c.pre_sparse, key, gen_source(c), "vest_sparse_delta.cu");
+    core_gen_prefetch(c);
   }
 }
 
@@ -640,14 +686,15 @@ static void ensure_module(Ctx& c) {
   const uint64_t key = mask_key(c);
   if (c.sparse && c.sparse->key == key) return;
   sparse_free(c);
-  const std::vector<char> cubin = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu");
+  std::vector<char> cubin;
+  if (!take_cubin(c.pre_sparse, key, cubin)) cubin = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu");
   auto* s = new SparseState;
   s->key = key;
   check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "sparse delta load");
   for (int n = 0; n < c.N; ++n) {
     const std::string nm = "vest_sd_" + std::to_string(n);
     check(cudaLibraryGetKernel(&s->k[n], s->lib, nm.c_str()), "sparse delta kernel");
-    if (fused_ok(c)) {
+    if (sparse_fused_enabled(c)) {
       const std::string nf = "vest_sf_" + std::to_string(n);
       check(cudaLibraryGetKernel(&s->kf[n], s->lib, nf.c_str()), "fused factor kernel");
     }
