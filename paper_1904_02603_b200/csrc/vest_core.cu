@@ -1410,7 +1410,7 @@ void core_gen_prefetch(Ctx& c) {
   std::string src = core_gen_source(c, block_lists(b), nts, ldr);
   c.stats_f32 = sf0;
   c.defer_last = dl0;
-  prefetch_cubin(c, c.pre_gen, key, std::move(src), "vest_core_gen.cu");
+  prefetch_cubin(c, c.pre_gen, key, std::move(src), "vest_core_gen.cu", core_gen_compile);
 }
 
 // the general plan's blocks (host-only compile check of the generated passes)

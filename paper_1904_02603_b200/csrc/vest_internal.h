@@ -300,7 +300,10 @@ cudaError_t launch_rowpass_delta(const RowPassArgs& a, int kind, uint32_t nchunk
                                  uint64_t dstride, uint64_t p0, cudaStream_t s, bool f32);  // delta fp32 or fp64
 bool sparse_delta_enabled(const Ctx& c);
 bool sparse_delta_eligible(const Ctx& c);
-void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src, const char* name);
+using CompileFn = std::vector<char> (*)(const std::string&, const char*);
+void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src, const char* name,
+                    CompileFn fn = nullptr);  // nullptr: nvrtc_compile
+std::vector<char> core_gen_compile(const std::string& src, const char* name);  // the passes, in parallel programs
 bool take_cubin(Ctx::AsyncCubin& slot, uint64_t key, std::vector<char>& out);
 void core_gen_prefetch(Ctx& c);  // vest_core.cu: the general plan's passes for the current mask
 void note_sweep(Ctx& c);  // a factor sweep starts (mode 0): count sweeps per core mask

@@ -608,7 +608,8 @@ std::vector<char> nvrtc_compile(const std::string& src, const char* name);
 // slot.  A superseded compile that is still running is parked (its future's
 // destructor would block); while one is parked no new compile is started -- a
 // schedule that prunes every iteration must not pile up compiler threads.
-void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src, const char* name) {
+void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src, const char* name, CompileFn fn) {
+  if (!fn) fn = nvrtc_compile;
   if (!nvrtc_async()) return;
   if (slot.valid && slot.key == key) return;
   auto running = [](const std::shared_future<std::vector<char>>& f) {
@@ -621,7 +622,7 @@ void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src
     else c.pre_stale.erase(c.pre_stale.begin() + (long)i);
   if (!c.pre_stale.empty()) return;
   slot.key = key;
-  slot.fut = std::async(std::launch::async, [s = std::move(src), name]() { return nvrtc_compile(s, name); }).share();
+  slot.fut = std::async(std::launch::async, [s = std::move(src), name, fn]() { return fn(s, name); }).share();
   slot.valid = true;
 }
 
