@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <exception>
+#include <future>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -502,6 +504,8 @@ bool fused_ok(const Ctx& c) {
   return true;
 }
 
+const char* kModeMark = "//@@MODE\n";
+
 std::string gen_source(const Ctx& c) {
   std::ostringstream o;
   o << "struct SparseDeltaArgs { const unsigned* oc[" << VEST_MAXN << "]; const double* f[" << VEST_MAXN
@@ -513,10 +517,12 @@ std::string gen_source(const Ctx& c) {
       << "extern \"C\" __global__ void vest_core_f32(const double* s) {\n"
       << "  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < " << c.G << "; i += gridDim.x * blockDim.x) Gf_src[i] = (float)s[i];\n"
       << "}\n";
-  for (int n = 0; n < c.N; ++n) emit_mode(o, c, n);
-  if (sparse_fused_enabled(c)) {  // off by default: not worth half the module's compile time
-    o << kFusedPrelude;
-    for (int n = 0; n < c.N; ++n) emit_fused(o, c, n);
+  const bool fused = sparse_fused_enabled(c);  // off by default: not worth half the compile time
+  if (fused) o << kFusedPrelude;
+  for (int n = 0; n < c.N; ++n) {  // one program per mode (sparse_compile cuts here)
+    o << kModeMark;
+    emit_mode(o, c, n);
+    if (fused) emit_fused(o, c, n);
   }
   return o.str();
 }
@@ -538,21 +544,24 @@ uint64_t mask_key(const Ctx& c) {
 
 }  // namespace
 
+// One module per mode (compiled in parallel, sparse_compile): each carries its
+// own copy of the core constant bank(s), loaded before its kernel runs.
 struct SparseState {
   uint64_t key = 0;
-  cudaLibrary_t lib = nullptr;
+  cudaLibrary_t lib[VEST_MAXN] = {};
   cudaKernel_t k[VEST_MAXN] = {};
   cudaKernel_t kf[VEST_MAXN] = {};  // fused factor-mode updates (vest_sf_<n>)
-  double* G = nullptr;
-  float* Gf = nullptr;  // fp32 contraction: the bank copy and its staging buffer
-  float* Gf_src = nullptr;
-  cudaKernel_t core_f32 = nullptr;
+  double* G[VEST_MAXN] = {};
+  float* Gf[VEST_MAXN] = {};  // fp32 contraction: the bank copy and its staging buffer
+  float* Gf_src[VEST_MAXN] = {};
+  cudaKernel_t core_f32[VEST_MAXN] = {};
   double compile_s = 0.0;
 };
 
 void sparse_free(Ctx& c) {
   if (!c.sparse) return;
-  if (c.sparse->lib) cudaLibraryUnload(c.sparse->lib);
+  for (cudaLibrary_t l : c.sparse->lib)
+    if (l) cudaLibraryUnload(l);
   delete c.sparse;
   c.sparse = nullptr;
 }
@@ -603,6 +612,7 @@ static bool nvrtc_async() {
 }
 
 std::vector<char> nvrtc_compile(const std::string& src, const char* name);
+std::vector<char> sparse_compile(const std::string& src, const char* name);
 
 // Start compiling `src` on a host thread unless that key is already in the
 // slot.  A superseded compile that is still running is parked (its future's
@@ -643,7 +653,7 @@ void note_sweep(Ctx& c) {
     c.mask_sweeps = 1;
     // auto mode switches the mask's kernels in from the next sweep: compile them now, off-thread
     if (sparse_mode(c) < 0 && sparse_delta_eligible(c) && !(c.sparse && c.sparse->key == key))
-      prefetch_cubin(c, c.pre_sparse, key, gen_source(c), "vest_sparse_delta.cu");
+      prefetch_cubin(c, c.pre_sparse, key, gen_source(c), "vest_sparse_delta.cu", sparse_compile);
     core_gen_prefetch(c);
   }
 }
@@ -683,29 +693,77 @@ std::vector<char> nvrtc_compile(const std::string& src, const char* name) {
   return cubin;
 }
 
+// The common head (argument struct, constant banks, fused prelude) plus one
+// mode's kernels per program, compiled on parallel host threads; one blob
+// [count | sizes | cubins], program n = mode n.
+std::vector<char> sparse_compile(const std::string& src, const char* name) {
+  std::vector<size_t> cut;
+  for (size_t p = src.find(kModeMark); p != std::string::npos; p = src.find(kModeMark, p + 1)) cut.push_back(p);
+  const int np = (int)cut.size();
+  if (np == 0) throw RtError{"sparse delta source without mode marks"};
+  std::vector<std::string> part(np), pname(np);
+  for (int q = 0; q < np; ++q) {
+    part[q] = src.substr(0, cut[0]) + src.substr(cut[q], (q + 1 < np ? cut[q + 1] : src.size()) - cut[q]);
+    pname[q] = std::string(name) + (q ? ".m" + std::to_string(q) : "");
+  }
+  std::vector<std::future<std::vector<char>>> fut;
+  for (int q = 1; q < np; ++q)
+    fut.push_back(std::async(std::launch::async, [&part, &pname, q]() { return nvrtc_compile(part[q], pname[q].c_str()); }));
+  std::vector<std::vector<char>> bin(np);
+  std::exception_ptr err;
+  try {
+    bin[0] = nvrtc_compile(part[0], pname[0].c_str());
+  } catch (...) {
+    err = std::current_exception();
+  }
+  for (int q = 1; q < np; ++q) {
+    try {
+      bin[q] = fut[q - 1].get();
+    } catch (...) {
+      if (!err) err = std::current_exception();
+    }
+  }
+  if (err) std::rethrow_exception(err);
+  std::vector<char> blob((size_t)(1 + np) * sizeof(uint64_t));
+  uint64_t* hdr = reinterpret_cast<uint64_t*>(blob.data());
+  hdr[0] = (uint64_t)np;
+  for (int q = 0; q < np; ++q) hdr[1 + q] = bin[q].size();
+  for (int q = 0; q < np; ++q) blob.insert(blob.end(), bin[q].begin(), bin[q].end());
+  return blob;
+}
+
 static void ensure_module(Ctx& c) {
   const uint64_t key = mask_key(c);
   if (c.sparse && c.sparse->key == key) return;
   sparse_free(c);
   std::vector<char> cubin;
-  if (!take_cubin(c.pre_sparse, key, cubin)) cubin = nvrtc_compile(gen_source(c), "vest_sparse_delta.cu");
+  if (!take_cubin(c.pre_sparse, key, cubin)) cubin = sparse_compile(gen_source(c), "vest_sparse_delta.cu");
   auto* s = new SparseState;
   s->key = key;
-  check(cudaLibraryLoadData(&s->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "sparse delta load");
+  uint64_t nparts = 0;
+  memcpy(&nparts, cubin.data(), sizeof(uint64_t));
+  if ((int)nparts != c.N) throw RtError{"sparse delta: one program per mode expected"};
+  std::vector<uint64_t> sz(nparts);
+  memcpy(sz.data(), cubin.data() + sizeof(uint64_t), nparts * sizeof(uint64_t));
+  size_t off = (size_t)(1 + nparts) * sizeof(uint64_t);
   for (int n = 0; n < c.N; ++n) {
+    check(cudaLibraryLoadData(&s->lib[n], cubin.data() + off, nullptr, nullptr, 0, nullptr, nullptr, 0),
+          "sparse delta load");
+    off += sz[n];
     const std::string nm = "vest_sd_" + std::to_string(n);
-    check(cudaLibraryGetKernel(&s->k[n], s->lib, nm.c_str()), "sparse delta kernel");
+    check(cudaLibraryGetKernel(&s->k[n], s->lib[n], nm.c_str()), "sparse delta kernel");
     if (sparse_fused_enabled(c)) {
       const std::string nf = "vest_sf_" + std::to_string(n);
-      check(cudaLibraryGetKernel(&s->kf[n], s->lib, nf.c_str()), "fused factor kernel");
+      check(cudaLibraryGetKernel(&s->kf[n], s->lib[n], nf.c_str()), "fused factor kernel");
     }
-  }
-  size_t gb = 0;
-  check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->G), &gb, s->lib, "G"), "sparse delta core symbol");
-  if (sd_f32(c)) {
-    check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->Gf), &gb, s->lib, "Gf"), "sparse delta core symbol");
-    check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->Gf_src), &gb, s->lib, "Gf_src"), "sparse delta core symbol");
-    check(cudaLibraryGetKernel(&s->core_f32, s->lib, "vest_core_f32"), "sparse delta core kernel");
+    size_t gb = 0;
+    check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->G[n]), &gb, s->lib[n], "G"), "sparse delta core symbol");
+    if (sd_f32(c)) {
+      check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->Gf[n]), &gb, s->lib[n], "Gf"), "sparse delta core symbol");
+      check(cudaLibraryGetGlobal(reinterpret_cast<void**>(&s->Gf_src[n]), &gb, s->lib[n], "Gf_src"),
+            "sparse delta core symbol");
+      check(cudaLibraryGetKernel(&s->core_f32[n], s->lib[n], "vest_core_f32"), "sparse delta core kernel");
+    }
   }
   c.sparse = s;
 }
@@ -714,17 +772,18 @@ static void ensure_module(Ctx& c) {
 void sparse_delta(Ctx& c, int mode, uint64_t p0, uint64_t n, double* out) {
   ensure_module(c);
   if (n == 0) return;
-  if (c.sparse->Gf) {  // fp32 contraction: the core rounded to fp32 into its constant bank
+  if (c.sparse->Gf[mode]) {  // fp32 contraction: the core rounded to fp32 into its constant bank
     const double* src = c.d_core;
     void* cargs[] = {&src};
-    check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->core_f32), dim3((c.G + 255) / 256), dim3(256), cargs,
+    check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->core_f32[mode]), dim3((c.G + 255) / 256), dim3(256), cargs,
                            0, c.stream),
           "sparse delta core (fp32)");
     count_launch();
-    check(cudaMemcpyAsync(c.sparse->Gf, c.sparse->Gf_src, sizeof(float) * c.G, cudaMemcpyDeviceToDevice, c.stream),
+    check(cudaMemcpyAsync(c.sparse->Gf[mode], c.sparse->Gf_src[mode], sizeof(float) * c.G, cudaMemcpyDeviceToDevice,
+                          c.stream),
           "sparse delta core (fp32)");
   } else {
-    check(cudaMemcpyAsync(c.sparse->G, c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
+    check(cudaMemcpyAsync(c.sparse->G[mode], c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
           "sparse delta core");
   }
   SparseDeltaArgs a{};
@@ -796,7 +855,7 @@ void sparse_fused(Ctx& c, int mode, const RowPassArgs& ra) {
     a.stride_na = ra.stride_na;
     a.reg = ra.reg;
     a.lambda = ra.lambda;
-    check(cudaMemcpyAsync(c.sparse->G, c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
+    check(cudaMemcpyAsync(c.sparse->G[mode], c.d_core, sizeof(double) * c.G, cudaMemcpyDeviceToDevice, c.stream),
           "sparse delta core");
     void* args[] = {&a};
     check(cudaLaunchKernel(reinterpret_cast<const void*>(c.sparse->kf[mode]), dim3((ra.csf.nchunks + 7) / 8),
