@@ -17,6 +17,7 @@
 // NVRTC program holds all passes of a plan; it is rebuilt only when a prune
 // changes the mask.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <future>
@@ -781,7 +782,10 @@ std::string core_gen_source(const Ctx& c, const std::vector<std::vector<uint32_t
     replace_all(p, "@PT@", PT);
     {  // timing probes only (results invalid): 1 = no Gram, 2 = no products / residual update
       const char* e = getenv("VEST_CP_PROBE");
-      replace_all(p, "@PROBE@", e ? std::to_string(atoi(e)) : "0");
+      const int probe = e ? atoi(e) : 0;
+      if (probe != 0 && i == 0)
+        fprintf(stderr, "vest: VEST_CP_PROBE=%d -- core passes skip work for timing; RESULTS ARE INVALID\n", probe);
+      replace_all(p, "@PROBE@", std::to_string(probe));
     }
     replace_all(p, "@XT@", PT);
     replace_all(p, "@NBUF@", std::to_string(cp_depth(c)));
