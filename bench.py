@@ -460,9 +460,13 @@ def run_ours(args, rank, world, local_rank):
     alt = None
     if gf32:
         # BASELINE config 4 is the fp32 configuration: the generated kernels
-        # gather fp32 copies of the factor rows (fp64 arithmetic; north_star's
-        # stated fp32 tolerance 1e-4, tests/test_gpu_generated.py).  The same
-        # steps with fp64 gathers are timed first and reported beside it.
+        # run their fp32 mode -- fp32 copies of the gathered factor rows, fp32
+        # contraction of delta and of the core passes' fiber products, fp32 delta
+        # and chunk statistics between kernels; every Gram, solve, residual, the
+        # factors and the core stay fp64 (north_star's stated fp32 tolerance
+        # 1e-4, normwise per SURVEY 8(c); tests/test_gpu_generated.py,
+        # tests/test_gpu_fullsize.py).  The same steps in the fp64 mode are
+        # timed first and reported beside it.
         dev.set_gather_f32(False)
         dev.set_model(m0)
         ms64, _, fams64, _ = measure(dev, c, args.steps, args.warmup, world, dist, local_rank, L, _lib, torch)
@@ -533,8 +537,10 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded; BASELINE config {cfg_id} shape)",
         "config": dict(workload_config(cfg_id, world),
-                       gathers=("fp32 copies of the factor rows in the generated kernels (fp64 arithmetic and "
-                                "storage; north_star fp32 tolerance 1e-4)" if gf32 else "fp64")),
+                       gathers=("fp32 mode of the generated kernels: fp32 copies of the gathered factor rows, fp32 "
+                                "contraction of delta and of the core passes' fiber products; Grams, solves, "
+                                "residuals, factors and core fp64 (north_star fp32 tolerance 1e-4, normwise)"
+                                if gf32 else "fp64")),
         "fp64_gathers": alt,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "path": "vest_cd_iteration_host: host model in/out (pinned)"},

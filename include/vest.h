@@ -83,10 +83,11 @@ int vest_ctx_sparse_delta_active(const vest_ctx* ctx);
  * (table-driven kernel), 1 on. */
 int vest_ctx_set_core_gen(vest_ctx* ctx, int mode);
 /* fp32 mode of the generated (NVRTC) kernels: on = their factor-row gathers
- * read fp32 copies of the factors, and the delta values and per-slice
- * statistics they hand on are stored as fp32 (arithmetic stays fp64; the
- * factors and the core stay fp64).  For fp32 workloads (BASELINE config 4:
- * north_star's 1e-4 fp32 tolerance); default off. */
+ * read fp32 copies of the factors, the mask-specialised delta and the core
+ * passes' fiber products are contracted in fp32 arithmetic, and the delta
+ * values and per-slice statistics they hand on are stored as fp32; every Gram,
+ * solve and residual, the factors and the core stay fp64.  For fp32 workloads
+ * (BASELINE config 4: north_star's 1e-4 fp32 tolerance, normwise); default off. */
 int vest_ctx_set_gather_f32(vest_ctx* ctx, int on);
 /* With the mask-specialised delta: fuse the contraction with the row
  * statistics and solves in one kernel (modes other than the one carrying the

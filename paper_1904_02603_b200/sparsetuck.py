@@ -294,8 +294,10 @@ class Device:
         check(self._L.vest_ctx_set_sparse_fused(self.h, int(mode)))
 
     def set_gather_f32(self, on: bool):
-        """The generated (NVRTC) kernels gather fp32 copies of the factor rows
-        (fp64 arithmetic); for fp32 workloads (BASELINE config 4)."""
+        """fp32 mode of the generated (NVRTC) kernels: fp32 copies of the gathered
+        factor rows, fp32 contraction of delta and of the core passes' fiber
+        products; every Gram, solve, residual, the factors and the core stay
+        fp64.  For fp32 workloads (BASELINE config 4)."""
         check(self._L.vest_ctx_set_gather_f32(self.h, 1 if on else 0))
 
     def set_core_gen(self, mode: int):
