@@ -642,8 +642,9 @@ std::vector<char> core_gen_compile(const std::string& src, const char* name) {
   std::vector<std::string> pname(nparts, name);  // distinct names: VEST_NVRTC_DUMP writes one file pair per program
   for (int q = 1; q < nparts; ++q) pname[q] = std::string(name) + ".p" + std::to_string(q);
   std::vector<std::future<std::vector<char>>> fut;
-  for (int q = 1; q < nparts; ++q)
-    fut.push_back(std::async(std::launch::async, [&part, &pname, q]() { return nvrtc_compile(part[q], pname[q].c_str()); }));
+  for (int q = 1; q < nparts; ++q)  // deferred (= compiled in get() below) when no thread can be started
+    fut.push_back(std::async(std::launch::async | std::launch::deferred,
+                             [&part, &pname, q]() { return nvrtc_compile(part[q], pname[q].c_str()); }));
   std::vector<std::vector<char>> bin(nparts);
   std::exception_ptr err;
   try {

@@ -668,6 +668,9 @@ int guard(F&& f) {
   } catch (const std::bad_alloc&) {
     g_err = "host allocation failed";
     return VEST_ERUNTIME;
+  } catch (const std::exception& e) {  // e.g. std::system_error from a host thread
+    g_err = e.what();
+    return VEST_ERUNTIME;
   }
 }
 

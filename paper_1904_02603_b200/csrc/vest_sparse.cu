@@ -33,6 +33,7 @@
 #include <cstring>
 #include <sstream>
 #include <string>
+#include <system_error>
 #include <vector>
 
 #include "vest_internal.h"
@@ -632,8 +633,12 @@ void prefetch_cubin(Ctx& c, Ctx::AsyncCubin& slot, uint64_t key, std::string src
     else c.pre_stale.erase(c.pre_stale.begin() + (long)i);
   if (!c.pre_stale.empty()) return;
   slot.key = key;
-  slot.fut = std::async(std::launch::async, [s = std::move(src), name, fn]() { return fn(s, name); }).share();
-  slot.valid = true;
+  try {
+    slot.fut = std::async(std::launch::async, [s = std::move(src), name, fn]() { return fn(s, name); }).share();
+    slot.valid = true;
+  } catch (const std::system_error&) {  // no thread to be had: the kernels are compiled where first used
+    slot.valid = false;
+  }
 }
 
 // The slot's cubin when it was compiled for `key` (waits for the compile).
@@ -707,8 +712,9 @@ std::vector<char> sparse_compile(const std::string& src, const char* name) {
     pname[q] = std::string(name) + (q ? ".m" + std::to_string(q) : "");
   }
   std::vector<std::future<std::vector<char>>> fut;
-  for (int q = 1; q < np; ++q)
-    fut.push_back(std::async(std::launch::async, [&part, &pname, q]() { return nvrtc_compile(part[q], pname[q].c_str()); }));
+  for (int q = 1; q < np; ++q)  // deferred (= compiled in get() below) when no thread can be started
+    fut.push_back(std::async(std::launch::async | std::launch::deferred,
+                             [&part, &pname, q]() { return nvrtc_compile(part[q], pname[q].c_str()); }));
   std::vector<std::vector<char>> bin(np);
   std::exception_ptr err;
   try {
